@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""SOMF step throughput on B200 -- the BASELINE.json metric.
+
+metric: streamed columns/sec of the SOMF step (one iteration of Alg. 3 + Alg. 4
+of arXiv 1701.05363 on an eta-column mini-batch), with the roofline fraction
+of the dominant kernel.  Workload (BASELINE.json configs[2], the config the
+north star's >= 60 % target is quoted on): fMRI-shaped, p = 212445 voxels,
+k = 70, eta = 200, r = 12, ridge lambda = 1e-3, l1-ball atoms (DESIGN.md §3
+states the synthetic recipe; no HCP data is used).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl somf|reference]
+
+A "step" is one somf_partial_fit on a batch resident in HBM; L2 is flushed
+(256 MiB write) before every timed step, outside the step's CUDA events.
+`e2e` times the same call with the batch in pinned HOST memory (the library
+gathers the q selected rows over the host link) plus the device->host read of
+the step's codes.  `--impl reference` times the float64 CPU oracle on the same
+workload (bounded sample).  N > 1 (torchrun): independent replicas, one per
+GPU (no row sharding yet -- DESIGN.md §7), value = total columns/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOAD = dict(name="cfgC-fmri", p=212445, k=70, eta=200, lam=1e-3, nu=1.0, mu=0.0,
+                pos_code=False, pos_dict=False, r=12.0, u=0.917)
+METRIC = "streamed columns/sec (SOMF step)"
+UNIT = "columns/s"
+L2_FLUSH_BYTES = 256 << 20
+
+
+# ----------------------------------------------------------------------------
+# inputs (synthetic, seeded) -- shared with tests/test_gpu_parity.py
+# ----------------------------------------------------------------------------
+def fmri_inputs_cpu(n_cols: int, seed: int = 0, k: int = WORKLOAD["k"]):
+    """(X p x n_cols, D0 p x k) float32 numpy: the first k stream columns
+    initialise D (reading R15), the rest are batches."""
+    import synth
+    S = synth.fmri_stream(n_cols + k, seed=seed)
+    return np.ascontiguousarray(S[:, k:]), np.ascontiguousarray(S[:, :k])
+
+
+def fmri_inputs_gpu(n_batches: int, eta: int, k: int, seed: int, device):
+    """Same recipe generated on the GPU (torch, harness only): returns
+    (list of p x eta float32 CUDA batches, D0 p x k)."""
+    import torch
+    import synth
+    coords = synth.fmri_voxel_grid()
+    p = coords.shape[0]
+    Dstar = torch.tensor(synth.fmri_dictionary(coords, 70, seed=seed), dtype=torch.float32, device=device)
+    n = n_batches * eta + k
+    A = torch.tensor(synth.fmri_codes(70, 1, T=max(1200, n), seed=seed + 1)[:, :n],
+                     dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed + 2)
+    sigma = float(np.sqrt(70 / p / 0.5))
+    D0 = (Dstar @ A[:, :k] + sigma * torch.randn(p, k, generator=g, device=device)).contiguous()
+    batches = []
+    for b in range(n_batches):
+        cols = A[:, k + b * eta:k + (b + 1) * eta]
+        batches.append((Dstar @ cols + sigma * torch.randn(p, eta, generator=g, device=device)).contiguous())
+    return batches, D0
+
+
+# ----------------------------------------------------------------------------
+# roofline bookkeeping: algorithmic bytes / flops per launch
+# ----------------------------------------------------------------------------
+def phase_cost(phase: str, q: float, p: int, k: int, eta: int):
+    """(bytes, flops, bound) of one launch of the phase's dominant kernel."""
+    if phase == "contract":   # read D_M, X_M, idx; (beta | G) outputs are tiny
+        return 4 * q * (k + eta + 1), 2 * q * k * (eta + k), "hbm"
+    if phase == "bbar":       # read X_M, idx; read + write Bbar_M
+        return 4 * q * (eta + 2 * k + 1), 2 * q * k * eta, "hbm"
+    if phase == "bcd":        # read + write D_M, read Bbar_M, idx
+        return 4 * q * (3 * k + 1), 2 * q * k * k, "hbm"
+    if phase == "codes":
+        return 8 * (k * k + 2 * k * eta), k ** 3 / 3 + 2 * k * k * eta, "alu"
+    if phase == "cbar":
+        return 8 * (2 * k * k + k * eta), 2 * k * k * eta, "alu"
+    if phase == "mask":
+        return 4 * q, 0.0, "hbm"
+    if phase == "stage":
+        return 8 * q * eta, 0.0, "hbm"
+    raise KeyError(phase)
+
+
+def step_bytes(q: float, k: int, eta: int):
+    """4q(4k + eta) + 8q bytes per iteration (masked modes)."""
+    return 4 * q * (4 * k + eta) + 8 * q
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        mp = json.load(open(path))
+        return dict(hbm=mp["hbm_gbs"], bf16=mp["bf16_tflops"], src="measured",
+                    sm_max_mhz=mp.get("sm_max_mhz", 1965.0))
+    return dict(hbm=6650.0, bf16=1590.0, src="fallback", sm_max_mhz=1965.0)
+
+
+def alu_peak_tflops(sm_mhz: float, fp64: bool = True):
+    """CUDA-core FMA peak: 148 SMs x 128 FP32 lanes (64 FP64 lanes) x 2 x clock."""
+    lanes = 64 if fp64 else 128
+    return 148 * lanes * 2 * sm_mhz * 1e6 / 1e12
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle leg
+# ----------------------------------------------------------------------------
+def oracle_throughput(batches_cpu, D0, budget_s: float, max_steps: int, warm: int = 1):
+    """Time the float64 oracle (as it stands) on host cores: returns
+    (columns/s, steps timed, seconds)."""
+    from oracle.somf import SomfOracle, OracleConfig
+    w = WORKLOAD
+    ora = SomfOracle(OracleConfig(p=w["p"], k=w["k"], eta=w["eta"], lam=w["lam"], nu=w["nu"],
+                                  mu=w["mu"], r=w["r"], u=w["u"], seed=0))
+    ora.set_components(D0)
+    i = 0
+    for _ in range(warm):
+        ora.partial_fit(batches_cpu[i % len(batches_cpu)])
+        i += 1
+    t0 = time.perf_counter()
+    n = 0
+    while n < max_steps and (time.perf_counter() - t0) < budget_s:
+        ora.partial_fit(batches_cpu[i % len(batches_cpu)])
+        i += 1
+        n += 1
+    dt = time.perf_counter() - t0
+    return w["eta"] * n / dt, n, dt
+
+
+def host_cores():
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:
+        cores = os.cpu_count()
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max((i.get("num_threads", 0) for i in threadpool_info()), default=None)
+    except Exception:
+        pass
+    return cores, threads
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = WORKLOAD
+    X, D0 = fmri_inputs_cpu(4 * w["eta"], seed=0)
+    batches = [X[:, i * w["eta"]:(i + 1) * w["eta"]] for i in range(4)]
+    val, n, dt = oracle_throughput(batches, D0, budget_s=max(30.0, 8.0 * args.steps),
+                                   max_steps=args.steps, warm=args.warmup)
+    cores, threads = host_cores()
+    sample = f"{n} oracle steps of {w['name']} r={w['r']} after {args.warmup} warm-up steps (pool of 4 batches)"
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * dt / max(n, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (fMRI-shaped, DESIGN.md §3)",
+            "config": {"workload": w["name"], "p": w["p"], "k": w["k"], "eta": w["eta"], "r": w["r"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "blas_threads": threads,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# GPU leg
+# ----------------------------------------------------------------------------
+def time_steps(model, batches, start, steps, flush, stream):
+    """Per-step CUDA-event durations (ms) with an L2 flush before each step."""
+    import torch
+    evs = []
+    for i in range(steps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        model.partial_fit(batches[(start + i) % len(batches)])
+        b.record(stream)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def run_somf(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    import paper_1701_05363_b200 as somf_pkg
+    somf_pkg.lib()
+    w = WORKLOAD
+    p, k, eta, r = w["p"], w["k"], w["eta"], args.r
+    stream = torch.cuda.current_stream(dev)
+    nb = min(args.warmup + args.steps, 24)
+    batches, D0 = fmri_inputs_gpu(nb, eta, k, seed=rank, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    def make(rr):
+        m = somf_pkg.Somf(p, k, eta, lam=w["lam"], nu=w["nu"], mu=w["mu"], pos_code=w["pos_code"],
+                          pos_dict=w["pos_dict"], r=rr, u=w["u"], seed=rank, device=local, stream=stream)
+        m.set_components(D0)
+        return m
+
+    model = make(r)
+    for i in range(args.warmup):
+        model.partial_fit(batches[i % nb])
+    torch.cuda.synchronize()
+    model.profile_read()
+    model.profile_enable(True)
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_wall = time.perf_counter()
+    ms = time_steps(model, batches, args.warmup, args.steps, flush, stream)
+    t_wall = time.perf_counter() - t_wall
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    prof = model.profile_read()
+    model.profile_enable(False)
+    info = model.last_step_info()
+    step_ms = sum(ms) / len(ms)
+    if world > 1:
+        tt = torch.tensor([step_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = float(tt.item())
+    value = world * eta / (step_ms * 1e-3)
+
+    # --- roofline of the dominant kernel ------------------------------------
+    q = p / r
+    peaks = measured_peaks()
+    steps_prof = max(prof["steps"], 1)
+    phase_ms = {ph: prof["ms"][ph] / steps_prof for ph in prof["ms"]}
+    dom = max(phase_ms, key=lambda ph: phase_ms[ph])
+    by, fl, bound = phase_cost(dom, q, p, k, eta)
+    dom_ms = phase_ms[dom]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(dom)
+    if bound == "hbm":
+        achieved = by / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm"], "traffic": traffic, "kernel_phase": dom,
+                "peak_source": peaks["src"]}
+    else:
+        achieved = fl / (dom_ms * 1e-3) / 1e12
+        pk = alu_peak_tflops(peaks["sm_max_mhz"], fp64=True)
+        roof = {"bound": "alu", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+                "frac": achieved / pk, "traffic": traffic, "kernel_phase": dom,
+                "peak_source": "guide: 148 SM x 64 FP64 lanes x 2 x sm_max_mhz"}
+    roof["phase_ms_per_step"] = phase_ms
+    roof["bcd_grid_reductions_per_step"] = info["bcd_reductions"]
+    sb = step_bytes(q, k, eta)
+    step_roof = {"bytes_per_step": sb, "achieved_gbs": sb / (step_ms * 1e-3) / 1e9,
+                 "frac_of_hbm": sb / (step_ms * 1e-3) / 1e9 / peaks["hbm"]}
+
+    # --- end-to-end through the C ABI with host buffers ----------------------
+    e2e = None
+    if not args.no_e2e:
+        n_e2e = min(args.steps, 10)
+        host = [b.cpu().pin_memory() for b in batches[:2]]
+        codes = torch.empty((k, eta), dtype=torch.float32).pin_memory()
+        m2 = make(r)
+        for i in range(2):
+            m2.partial_fit(host[i % 2])
+        torch.cuda.synchronize()
+        qs, times = [], []
+        for i in range(n_e2e):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            m2.partial_fit(host[i % 2])
+            m2.get_codes(codes)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+            qs.append(m2.last_step_info()["q"])
+        e_ms = sum(times) / len(times)
+        e2e = {"value": world * eta / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(4 * eta * sum(qs) / len(qs)), "d2h_bytes_per_step": 4 * k * eta,
+               "ms_per_step": e_ms, "path": "somf_partial_fit(pinned host X) + somf_get_codes(host)"}
+        del m2
+
+    # --- r sweep (BASELINE metric lists r = 1/4/12/24) ---------------------------
+    sweep = {}
+    if not args.no_sweep:
+        for rr in (1.0, 4.0, 12.0, 24.0):
+            m3 = make(rr)
+            for i in range(3):
+                m3.partial_fit(batches[i % nb])
+            torch.cuda.synchronize()
+            t3 = time_steps(m3, batches, 3, 5, flush, stream)
+            sm = sum(t3) / len(t3)
+            sweep[f"r={int(rr)}"] = {"columns_per_s": eta / (sm * 1e-3), "ms_per_step": sm,
+                                     "bcd_grid_reductions": m3.last_step_info()["bcd_reductions"]}
+            del m3
+
+    # --- CPU oracle baseline (rank 0, N = 1) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        hb = [b.cpu().numpy() for b in batches[:3]]
+        val, n, dt = oracle_throughput(hb, D0.cpu().numpy(), budget_s=args.cpu_budget, max_steps=50)
+        cores, threads = host_cores()
+        cpu = {"value": val, "unit": UNIT, "cores": cores, "blas_threads": threads, "kind": "oracle",
+               "sample": f"{n} float64 oracle steps ({dt:.1f} s) of the same workload after 1 warm-up step"}
+
+    launches = int(sum(prof["launches"].values()))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (fMRI-shaped stand-in, DESIGN.md §3)",
+            "config": {"workload": w["name"], "p": p, "k": k, "eta": eta, "r": r, "lambda": w["lam"],
+                       "code": "ridge", "dict": "l1-ball", "b_mode": "masked",
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "parallelism": "single" if world == 1 else f"replicas x{world}"},
+            "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "gpu_launches_per_step": launches / steps_prof,
+            "clocks": clk, "sweep": sweep, "wall_s_timed": t_wall}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="somf", choices=["somf", "reference"])
+    ap.add_argument("--r", type=float, default=WORKLOAD["r"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_somf(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,100 @@
+"""ctypes loader for libsomf.so (the C ABI declared in include/somf.h).
+
+Argument marshalling only: every step of the SOMF path runs in the CUDA
+kernels of ``csrc/``.  There is no fallback: if the shared library is missing
+or cannot be loaded, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libsomf.so")
+CSRC = os.path.join(HERE, "csrc")
+NVCC_ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _sources():
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cuh"))) + [os.path.join(ROOT, "include", "somf.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile csrc/somf_capi.cu into libsomf.so for sm_100a (in-tree)."""
+    newest = max(os.path.getmtime(s) for s in _sources())
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    if not os.path.exists(nvcc):
+        nvcc = "nvcc"
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, "-O3", "-std=c++17", *NVCC_ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
+           "-shared", "-o", tmp, os.path.join(CSRC, "somf_capi.cu")]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class SomfConfig(C.Structure):
+    _fields_ = [
+        ("p", C.c_int64), ("k", C.c_int32), ("eta", C.c_int32),
+        ("lambda_", C.c_double), ("nu", C.c_double), ("pos_code", C.c_int32),
+        ("mu", C.c_double), ("pos_dict", C.c_int32),
+        ("r", C.c_double), ("u", C.c_double),
+        ("b_mode", C.c_int32), ("perm_cyclic", C.c_int32),
+        ("cd_tol", C.c_double), ("cd_max_sweeps", C.c_int32),
+        ("seed", C.c_uint64), ("row_lo", C.c_int64), ("row_hi", C.c_int64),
+        ("device", C.c_int32), ("stream", C.c_void_p), ("debug", C.c_int32),
+    ]
+
+
+# (name, restype, argtypes) of every symbol include/somf.h declares
+P = C.c_void_p
+I32, I64, U64, D = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+SIGNATURES = [
+    ("somf_config_default", None, [C.POINTER(SomfConfig)]),
+    ("somf_abi_version", I32, []),
+    ("somf_config_size", I64, []),
+    ("somf_status_string", C.c_char_p, [I32]),
+    ("somf_last_error", C.c_char_p, [P]),
+    ("somf_create", I32, [C.POINTER(SomfConfig), C.POINTER(P)]),
+    ("somf_destroy", I32, [P]),
+    ("somf_set_components", I32, [P, P, I64]),
+    ("somf_partial_fit", I32, [P, P, I64]),
+    ("somf_next_mask", I32, [P, C.POINTER(I64), P]),
+    ("somf_partial_fit_masked", I32, [P, P, I64]),
+    ("somf_get_codes", I32, [P, P]),
+    ("somf_transform", I32, [P, P, I64, I64, P]),
+    ("somf_objective", I32, [P, P, I64, I64, C.POINTER(D)]),
+    ("somf_components", I32, [P, P, I64]),
+    ("somf_get_state", I32, [P, P, P, P, P, C.POINTER(I64)]),
+    ("somf_set_state", I32, [P, P, P, P, P, I64]),
+    ("somf_last_step_info", I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(D)]),
+    ("somf_profile_enable", I32, [P, I32]),
+    ("somf_profile_read", I32, [P, P, P, C.POINTER(I64)]),
+    ("somf_mask_rows", I32, [U64, I64, I64, I64, D, P, C.POINTER(I64), P]),
+    ("somf_atom_permutation", I32, [U64, I64, I32, I32, P, P]),
+    ("somf_column_ids", I32, [U64, I64, I64, I64, P, P]),
+    ("somf_project_columns", I32, [P, I64, I32, I64, P, D, I32, P, P]),
+]
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run __graft_entry__.build() (nvcc, sm_100a); "
+                          "there is no CPU fallback")
+    lib = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.somf_config_size() != C.sizeof(SomfConfig):
+        raise ImportError("somf_config layout mismatch between libsomf.so and the binding")
+    return lib

@@ -1,0 +1,133 @@
+// common.cuh -- shared device helpers of the SOMF hot path (sm_100a).
+//
+// Philox4x32-10 (R1), warp/block reductions with a FIXED combination order
+// (so every CTA and every run produces the same bits), and a sense-reversing
+// grid barrier for cooperative launches.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace somf {
+
+constexpr int kWarp = 32;
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10: key = (seed lo, seed hi); counter (c0,c1,c2,c3).
+// Draw layout (R1): c2 = stream (1 mask, 2 atom permutation, 3 column ids).
+// ---------------------------------------------------------------------------
+struct U4 { uint32_t x, y, z, w; };
+
+__host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint64_t seed) {
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int rnd = 0; rnd < 10; ++rnd) {
+    if (rnd) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+#ifdef __CUDA_ARCH__
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+#else
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+    const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+#endif
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+  }
+  return c;
+}
+
+__host__ __device__ __forceinline__ uint32_t u4_word(const U4& v, int lane) {
+  return lane == 0 ? v.x : lane == 1 ? v.y : lane == 2 ? v.z : v.w;
+}
+
+enum : uint32_t { kStreamMask = 1, kStreamPerm = 2, kStreamCols = 3 };
+
+// ---------------------------------------------------------------------------
+// Fixed-order reductions.  xor-butterfly: every lane ends with the same value
+// and the combination tree does not depend on timing.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum of N values per thread; result broadcast to all threads.
+// scratch: >= N * 32 doubles of shared memory.
+template <int N>
+__device__ __forceinline__ void block_sum(double (&v)[N], double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) scratch[i * 32 + wid] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = lane < nw ? scratch[i * 32 + lane] : 0.0;
+    v[i] = warp_sum(s);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Grid barrier for cooperative launches (all CTAs co-resident).
+// bar[0] = arrival counter, bar[1] = generation.  Release/acquire at gpu scope.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned gen = ld_acquire_gpu(bar + 1);
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == nb - 1) {
+      bar[0] = 0;
+      __threadfence();
+      st_release_gpu(bar + 1, gen + 1);
+    } else {
+      while (ld_acquire_gpu(bar + 1) == gen) { __nanosleep(32); }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Small math helpers
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Root lam >= 0 of (a^2 b s/2 + rho b^2) lam^2 + (a^2 s + 2 rho b) lam
+//                 - (a S1 + b S2/2 - rho) = 0       (R17: the active-set equation
+// of the elastic-net projection, derived from its KKT conditions).
+__device__ __forceinline__ double enet_lambda(double a, double b, double rho, double s,
+                                              double S1, double S2) {
+  const double A = a * a * b * s * 0.5 + rho * b * b;
+  const double B = a * a * s + 2.0 * rho * b;
+  const double C = a * S1 + b * S2 * 0.5 - rho;
+  const double den = B + sqrt(fmax(B * B + 4.0 * A * C, 0.0));
+  return den > 0.0 ? fmax(2.0 * C / den, 0.0) : 0.0;
+}
+
+}  // namespace somf

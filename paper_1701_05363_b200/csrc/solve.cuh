@@ -1,0 +1,196 @@
+// solve.cuh -- (a2) batched code solve, Eq. (somf_alpha) P:592-596:
+//   alpha_s = argmin_a 1/2 a^T G a - a^T beta_s + lambda Omega(a)   (s = 1..m)
+//
+//  k_ridge_chol : nu = 1, no positivity: (G + lambda I) alpha = beta by a
+//                 float64 Cholesky in shared memory (k <= 160), every CTA
+//                 factorises (no inter-CTA dependency) and solves the RHS of
+//                 its warps (column-oriented substitutions, one warp per RHS).
+//  k_cd         : otherwise cyclic coordinate descent (the paper's solver,
+//                 P:1341-1342), one warp per column, maintained gradient
+//                 g = beta - G alpha in float64 registers, G packed (upper
+//                 triangle, float32) in shared memory so k = 256 fits.
+#pragma once
+#include "common.cuh"
+
+namespace somf {
+
+constexpr int kSolveThreads = 256;
+constexpr int kRidgeMaxK = 160;
+
+// smem: (k*(k+1) + k) doubles + 8 warps * k doubles
+__global__ void __launch_bounds__(kSolveThreads)
+k_ridge_chol(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
+             double lam, double* __restrict__ A64, float* __restrict__ A32,
+             int* __restrict__ err) {
+  extern __shared__ double sm[];
+  const int ld = k + 1;
+  double* M = sm;                         // k x (k+1)
+  double* invd = M + (size_t)k * ld;      // k
+  double* ys = invd + k;                  // nwarps x k
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e % k;
+    M[i * ld + j] = G[e] + (i == j ? lam : 0.0);
+  }
+  __syncthreads();
+  // right-looking, unscaled: M_il -= M_ij M_lj / M_jj for j < l <= i
+  for (int j = 0; j < k; ++j) {
+    const double djj = M[j * ld + j];
+    const int n = k - j - 1;
+    if (n > 0 && djj > 0.0) {
+      const double inv = 1.0 / djj;
+      for (int e = tid; e < n * n; e += nt) {
+        const int i = j + 1 + e / n, l = j + 1 + e % n;
+        if (l <= i) M[i * ld + l] -= M[i * ld + j] * M[l * ld + j] * inv;
+      }
+    }
+    __syncthreads();
+  }
+  // scale: L_ij = M_ij / sqrt(M_jj)
+  for (int j = tid; j < k; j += nt) {
+    const double djj = M[j * ld + j];
+    if (!(djj > 0.0) && err) atomicExch(err, 1);
+    invd[j] = djj > 0.0 ? rsqrt(djj) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += nt) {
+    const int i = e / k, j = e % k;
+    if (j <= i) M[i * ld + j] *= invd[j];
+  }
+  __syncthreads();
+  for (int j = tid; j < k; j += nt) invd[j] = M[j * ld + j] != 0.0 ? 1.0 / M[j * ld + j] : 0.0;
+  __syncthreads();
+  // substitutions: one warp per right-hand side
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  double* y = ys + (size_t)wid * k;
+  for (int s = blockIdx.x * nw + wid; s < m; s += gridDim.x * nw) {
+    for (int i = lane; i < k; i += 32) y[i] = beta[(int64_t)i * m + s];
+    __syncwarp();
+    for (int j = 0; j < k; ++j) {                 // L y = b
+      const double yj = y[j] * invd[j];
+      __syncwarp();
+      if (lane == 0) y[j] = yj;
+      for (int i = j + 1 + lane; i < k; i += 32) y[i] -= M[i * ld + j] * yj;
+      __syncwarp();
+    }
+    for (int j = k - 1; j >= 0; --j) {            // L^T x = y
+      const double xj = y[j] * invd[j];
+      __syncwarp();
+      if (lane == 0) y[j] = xj;
+      for (int i = lane; i < j; i += 32) y[i] -= M[j * ld + i] * xj;
+      __syncwarp();
+    }
+    for (int i = lane; i < k; i += 32) {
+      A64[(int64_t)i * m + s] = y[i];
+      A32[(int64_t)i * m + s] = (float)y[i];
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ int packed_off(int i, int k) { return i * k - (i * (i - 1)) / 2; }
+__device__ __forceinline__ float packed_get(const float* P, int i, int j, int k) {
+  return i <= j ? P[packed_off(i, k) + (j - i)] : P[packed_off(j, k) + (i - j)];
+}
+
+// Cyclic CD, one warp per column; KPL = ceil(k/32) coordinates per lane
+// (coordinate j lives in lane j & 31, slot j >> 5).
+template <int KPL>
+__global__ void __launch_bounds__(kSolveThreads)
+k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
+     double l1, double l2, int positive, double tol, int max_sweeps,
+     double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out) {
+  extern __shared__ float Pk[];            // packed upper triangle, k(k+1)/2
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int np = k * (k + 1) / 2;
+  for (int e = tid; e < np; e += nt) {
+    // invert packed index: row i with packed_off(i) <= e < packed_off(i+1)
+    int i = 0;
+    {
+      int lo = 0, hi = k - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (packed_off(mid, k) <= e) lo = mid; else hi = mid - 1;
+      }
+      i = lo;
+    }
+    const int j = i + (e - packed_off(i, k));
+    Pk[e] = (float)G[(int64_t)i * k + j];
+  }
+  __syncthreads();
+  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  for (int s = blockIdx.x * nw + wid; s < m; s += gridDim.x * nw) {
+    double alpha[KPL], g[KPL], den[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int row = lane + 32 * i;
+      alpha[i] = 0.0;
+      g[i] = row < k ? beta[(int64_t)row * m + s] : 0.0;
+      den[i] = row < k ? (double)packed_get(Pk, row, row, k) + l2 : 1.0;
+    }
+    int sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+      double maxd = 0.0;
+#pragma unroll
+      for (int slot = 0; slot < KPL; ++slot) {
+        for (int ol = 0; ol < 32; ++ol) {
+          const int j = slot * 32 + ol;
+          if (j >= k) break;
+          double delta = 0.0;
+          if (lane == ol) {
+            const double gjj = den[slot] - l2;
+            const double z = g[slot] + gjj * alpha[slot];
+            double nv;
+            if (!(den[slot] > 0.0)) nv = 0.0;                       // R12
+            else if (positive) nv = fmax(z - l1, 0.0) / den[slot];
+            else nv = copysign(fmax(fabs(z) - l1, 0.0), z) / den[slot];
+            delta = nv - alpha[slot];
+            alpha[slot] = nv;
+          }
+          delta = __shfl_sync(0xffffffffu, delta, ol);
+          if (delta != 0.0) {
+            maxd = fmax(maxd, fabs(delta));
+#pragma unroll
+            for (int i = 0; i < KPL; ++i) {
+              const int row = lane + 32 * i;
+              if (row < k) g[i] -= (double)packed_get(Pk, row, j, k) * delta;
+            }
+          }
+        }
+      }
+      double amax = 0.0;
+#pragma unroll
+      for (int i = 0; i < KPL; ++i) amax = fmax(amax, fabs(alpha[i]));
+      amax = warp_max(amax);
+      if (maxd <= tol * fmax(1.0, amax)) { ++sweep; break; }
+    }
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) {
+      const int row = lane + 32 * i;
+      if (row < k) {
+        A64[(int64_t)row * m + s] = alpha[i];
+        A32[(int64_t)row * m + s] = (float)alpha[i];
+      }
+    }
+    if (lane == 0 && sweeps_out) atomicMax(sweeps_out, sweep);
+  }
+}
+
+// Cbar <- (1-w) Cbar + (w/eta) A A^T  (Eq. somf_partial; batch mean R4)
+__global__ void k_cbar_update(const double* __restrict__ A64, int k, int eta,
+                              const double* __restrict__ w_dev, double* __restrict__ C64,
+                              float* __restrict__ C32) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const int a = e / k, b = e % k;
+  const double w = *w_dev;
+  double s = 0.0;
+  const double* ra = A64 + (int64_t)a * eta;
+  const double* rb = A64 + (int64_t)b * eta;
+  for (int t = 0; t < eta; ++t) s += ra[t] * rb[t];
+  const double c = (1.0 - w) * C64[e] + (w / eta) * s;
+  C64[e] = c;
+  C32[e] = (float)c;
+}
+
+}  // namespace somf

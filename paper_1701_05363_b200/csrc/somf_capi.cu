@@ -1,0 +1,823 @@
+// somf_capi.cu -- engine and C ABI of the SOMF hot path (include/somf.h).
+//
+// One SOMF iteration (Alg. 3 + Alg. 4 of arXiv 1701.05363) is the launch
+// sequence below, all on the caller's stream, with no host synchronisation
+// (dynamic sizes such as q = |S_t| stay on the device):
+//   k_step_begin      t <- t+1, w_t = t^-u
+//   k_mask_count/k_mask_scatter  S_t = rows with M_t = r   (Eq. mt)
+//   k_atom_perm       Alg. 4 atom order
+//   k_contract(+reduce) beta = r D_M^T X_M, G = r D_M^T D_M (Eq. a)
+//   k_ridge_chol | k_cd  codes                              (Eq. somf_alpha)
+//   k_cbar_update     Cbar                                   (Eq. somf_partial)
+//   k_bbar_update     P_t Bbar (and P_t^perp Bbar, mode F)
+//   k_bcd_seq         Alg. 4 on S_t (cooperative)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/somf.h"
+#include "common.cuh"
+#include "mask.cuh"
+#include "gemm.cuh"
+#include "solve.cuh"
+#include "bcd.cuh"
+
+using namespace somf;
+
+#define SOMF_EXPORT extern "C" __attribute__((visibility("default")))
+
+// ---------------------------------------------------------------------------
+// small kernels
+// ---------------------------------------------------------------------------
+__global__ void k_step_begin(int64_t* t, double* w, double u) {
+  const int64_t tt = *t + 1;
+  *t = tt;
+  *w = pow((double)tt, -u);
+}
+
+__global__ void k_set_scalar_i64(int64_t* p, int64_t v) { *p = v; }
+
+// X_M[m][:] = X[idx[m]][:] for m < q: one warp per row, the rows of a host
+// batch read once over the host link (many independent 4-byte requests in
+// flight per warp; rows are contiguous so requests coalesce per row).
+__global__ void __launch_bounds__(256)
+k_gather_rows(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, const float* __restrict__ X,
+              int64_t ldx, int eta, float* __restrict__ Xm) {
+  const int64_t q = *q_dev;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t m = warp; m < q; m += nwarps) {
+    const float* src = X + (int64_t)idx[m] * ldx;
+    float* dst = Xm + m * eta;
+    for (int s = lane; s < eta; s += 32) dst[s] = src[s];
+  }
+}
+
+__global__ void k_objective_final(const double* __restrict__ colsq, const double* __restrict__ A64,
+                                  int k, int m, double lam, double nu, double* __restrict__ out) {
+  __shared__ double scratch[32];
+  double s[1] = {0.0};
+  for (int c = threadIdx.x; c < m; c += blockDim.x) {
+    double pen = 0.0;
+    for (int a = 0; a < k; ++a) {
+      const double v = A64[(int64_t)a * m + c];
+      pen += (1.0 - nu) * fabs(v) + 0.5 * nu * v * v;
+    }
+    s[0] += 0.5 * colsq[c] + lam * pen;
+  }
+  block_sum<1>(s, scratch);
+  if (threadIdx.x == 0) *out = s[0] / m;
+}
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+struct somf_ctx {
+  somf_config cfg{};
+  int64_t rows = 0;          // local rows
+  int kp = 0;                // k padded to a multiple of 4
+  int dev = 0, nsm = 148;
+  cudaStream_t st = nullptr;
+  std::string err;
+  bool initialized = false;
+  bool mask_ready = false;   // idx/q hold the draw of iteration t+1
+  int64_t t_host = 0;
+  // iterate
+  float* D = nullptr;
+  float* Bbar = nullptr;
+  double* C64 = nullptr;
+  float* C32 = nullptr;
+  double* nslack = nullptr;
+  // per-step scratch
+  int64_t* t_dev = nullptr;
+  double* w_dev = nullptr;
+  int64_t* q_dev = nullptr;
+  int64_t* nred_dev = nullptr;
+  int* err_dev = nullptr;
+  int* sweeps_dev = nullptr;
+  int32_t* idx = nullptr;
+  int32_t* tile_counts = nullptr;
+  int ntiles = 0;
+  int32_t* perm = nullptr;
+  float* partial = nullptr;
+  size_t partial_cap = 0;    // floats
+  double* G64 = nullptr;
+  double* beta64 = nullptr;
+  double* A64 = nullptr;
+  float* A32 = nullptr;
+  double* red = nullptr;
+  unsigned* bar = nullptr;
+  int bcd_grid = 0;
+  int rows_cap = 0;          // rows per BCD CTA upper bound
+  // evaluation scratch (objective / transform)
+  int64_t eval_cap = 0;
+  double *Ge = nullptr, *betae = nullptr, *Ae64 = nullptr, *colsq = nullptr, *objd = nullptr;
+  float* Ae32 = nullptr;
+  int64_t* qfull_dev = nullptr;
+  uint64_t T = 0;            // mask threshold floor(2^32 / r)
+  float* Xstage = nullptr;   // device copy of the selected rows of a host batch
+  // profiling
+  bool prof_on = false;
+  struct Ev { int ph; cudaEvent_t a, b; };
+  std::vector<Ev> evs;
+  std::vector<cudaEvent_t> pool;
+  int64_t launches[SOMF_NPHASE] = {};
+  int64_t steps_prof = 0;
+};
+
+static cudaEvent_t take_event(somf_ctx* h) {
+  if (!h->pool.empty()) {
+    cudaEvent_t e = h->pool.back();
+    h->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  return e;
+}
+
+static void set_err(somf_ctx* h, const char* fmt, ...) {
+  if (!h) return;
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  h->err = buf;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      set_err(h, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+      return e_ == cudaErrorMemoryAllocation ? SOMF_E_OOM : SOMF_E_CUDA;                \
+    }                                                                                   \
+  } while (0)
+
+#define CKL()  CK(cudaGetLastError())
+
+static somf_status post_call(somf_ctx* h) {
+  CKL();
+  if (h->cfg.debug) {
+    CK(cudaStreamSynchronize(h->st));
+    int e = 0;
+    CK(cudaMemcpy(&e, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e) { set_err(h, "device numerical error flag %d", e); return SOMF_E_NONFINITE; }
+  }
+  return SOMF_OK;
+}
+
+// Device-readable address for a pointer that is device memory or mapped pinned host memory.
+static somf_status resolve_in(somf_ctx* h, const void* p, const void** out, bool* is_host = nullptr) {
+  if (is_host) *is_host = false;
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) { cudaGetLastError(); set_err(h, "pointer query failed"); return SOMF_E_ARG; }
+  if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) { *out = p; return SOMF_OK; }
+  if (at.type == cudaMemoryTypeHost) {
+    void* d = nullptr;
+    if (cudaHostGetDevicePointer(&d, const_cast<void*>(p), 0) != cudaSuccess || !d) {
+      cudaGetLastError();
+      set_err(h, "pinned host pointer is not mapped into the device address space");
+      return SOMF_E_ARG;
+    }
+    *out = d;
+    if (is_host) *is_host = true;
+    return SOMF_OK;
+  }
+  set_err(h, "input must be device memory or pinned (page-locked) host memory");
+  return SOMF_E_ARG;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T));
+}
+
+static int split_count(const somf_ctx* h, int tiles, int64_t q_est) {
+  int ns = std::max(1, (2 * h->nsm) / std::max(1, tiles));
+  ns = (int)std::min<int64_t>(ns, std::max<int64_t>(1, q_est / TK));
+  return std::max(1, ns);
+}
+
+static somf_status ensure_partial(somf_ctx* h, size_t floats) {
+  if (floats <= h->partial_cap) return SOMF_OK;
+  if (h->partial) CK(cudaFree(h->partial));
+  h->partial = nullptr;
+  CK(dalloc(&h->partial, floats));
+  h->partial_cap = floats;
+  return SOMF_OK;
+}
+
+// [beta | G] over rows given by idx (or all rows), scaled by r.
+static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, const int64_t* q_dev,
+                                   int64_t q_est, const float* X, int64_t ldx, int m, double r,
+                                   double* beta, double* G) {
+  const int k = h->cfg.k;
+  const int nc = m + k;
+  const int ta = (int)ceil_div(k, TM), tc = (int)ceil_div(nc, TN);
+  const int ns = split_count(h, ta * tc, q_est);
+  somf_status s = ensure_partial(h, (size_t)ns * k * nc);
+  if (s) return s;
+  dim3 grid(ta, tc, ns);
+  if (gather) {
+    if (xcompact)
+      k_contract<true, true><<<grid, kGemmThreads, 0, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial);
+    else
+      k_contract<true, false><<<grid, kGemmThreads, 0, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial);
+  } else {
+    k_contract<false, false><<<grid, kGemmThreads, 0, h->st>>>(nullptr, q_dev, h->D, h->kp, k, X, ldx, m, h->partial);
+  }
+  CKL();
+  const int64_t tot = (int64_t)k * nc;
+  k_contract_reduce<<<(unsigned)ceil_div(tot, 256), 256, 0, h->st>>>(h->partial, ns, k, m, r, beta, G);
+  CKL();
+  return SOMF_OK;
+}
+
+static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta, int m, double tol,
+                                double* A64, float* A32) {
+  const somf_config& c = h->cfg;
+  const int k = c.k;
+  const int nw = kSolveThreads / 32;
+  const int grid = (int)std::max<int64_t>(1, ceil_div(m, nw));
+  if (c.nu == 1.0 && !c.pos_code && k <= kRidgeMaxK) {
+    const size_t smem = ((size_t)k * (k + 1) + k + (size_t)nw * k) * sizeof(double);
+    CK(cudaFuncSetAttribute(k_ridge_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ridge_chol<<<grid, kSolveThreads, smem, h->st>>>(G, beta, k, m, c.lambda, A64, A32, h->err_dev);
+    CKL();
+    return SOMF_OK;
+  }
+  const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
+  const size_t smem = (size_t)k * (k + 1) / 2 * sizeof(float);
+  const int kpl = (int)ceil_div(k, 32);
+#define LAUNCH_CD(N)                                                                      \
+  case N:                                                                                 \
+    CK(cudaFuncSetAttribute(k_cd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_cd<N><<<grid, kSolveThreads, smem, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,   \
+                                                  c.cd_max_sweeps, A64, A32, h->sweeps_dev); \
+    break;
+  switch (kpl) {
+    LAUNCH_CD(1) LAUNCH_CD(2) LAUNCH_CD(3) LAUNCH_CD(4)
+    LAUNCH_CD(5) LAUNCH_CD(6) LAUNCH_CD(7) LAUNCH_CD(8)
+    default: set_err(h, "k too large for the CD kernel"); return SOMF_E_ARG;
+  }
+#undef LAUNCH_CD
+  CKL();
+  return SOMF_OK;
+}
+
+static somf_status launch_mask(somf_ctx* h, const int64_t* t_dev_ptr, int64_t idx_offset,
+                               int64_t row_lo, int64_t row_hi, uint64_t T, int32_t* idx,
+                               int32_t* tile_counts, int64_t* q_out, cudaStream_t st) {
+  const int64_t nblk = ((row_hi - 1) >> 2) - (row_lo >> 2) + 1;
+  const int ntiles = (int)ceil_div(nblk, kMaskThreads);
+  k_mask_count<<<ntiles, kMaskThreads, 0, st>>>(h->cfg.seed, t_dev_ptr, row_lo, row_hi, T, tile_counts);
+  CKL();
+  k_mask_scatter<<<ntiles, kMaskThreads, 0, st>>>(h->cfg.seed, t_dev_ptr, row_lo, row_hi, T, tile_counts,
+                                                  idx_offset, idx, q_out);
+  CKL();
+  return SOMF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+SOMF_EXPORT void somf_config_default(somf_config* c) {
+  if (!c) return;
+  std::memset(c, 0, sizeof(*c));
+  c->lambda = 0.1;
+  c->nu = 1.0;
+  c->mu = 0.0;
+  c->r = 1.0;
+  c->u = 0.917;
+  c->b_mode = SOMF_B_MASKED;
+  c->cd_tol = 1e-9;
+  c->cd_max_sweeps = 4000;
+}
+
+SOMF_EXPORT int32_t somf_abi_version(void) { return SOMF_ABI_VERSION; }
+SOMF_EXPORT int64_t somf_config_size(void) { return (int64_t)sizeof(somf_config); }
+
+SOMF_EXPORT const char* somf_status_string(somf_status s) {
+  switch (s) {
+    case SOMF_OK: return "ok";
+    case SOMF_E_ARG: return "invalid argument";
+    case SOMF_E_DIM: return "dimension mismatch";
+    case SOMF_E_NONFINITE: return "non-finite value";
+    case SOMF_E_STATE: return "invalid state";
+    case SOMF_E_CUDA: return "CUDA error";
+    case SOMF_E_NCCL: return "NCCL error";
+    case SOMF_E_OOM: return "out of device memory";
+    case SOMF_E_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+SOMF_EXPORT const char* somf_last_error(somf_handle h) { return h ? h->err.c_str() : "null handle"; }
+
+SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
+  if (!cfg || !out) return SOMF_E_ARG;
+  *out = nullptr;
+  somf_config c = *cfg;
+  if (c.row_hi == 0) c.row_hi = c.p;
+  const bool bad =
+      c.p < 1 || c.k < 1 || c.k > 256 || c.eta < 1 || c.eta > 4096 || !(c.lambda >= 0.0) ||
+      !(c.nu >= 0.0 && c.nu <= 1.0) || !(c.mu >= 0.0 && c.mu <= 1.0) || !(c.r >= 1.0) ||
+      !(c.u > 0.0 && c.u <= 1.0) || c.row_lo < 0 || c.row_hi > c.p || c.row_lo >= c.row_hi ||
+      !(c.cd_tol > 0.0) || c.cd_max_sweeps < 1 || c.row_hi - c.row_lo > (int64_t)INT32_MAX;
+  if (bad) return SOMF_E_ARG;
+  if (c.b_mode == SOMF_B_UNBIASED) return SOMF_E_UNSUPPORTED;
+  if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL) return SOMF_E_ARG;
+  somf_ctx* h = new somf_ctx();
+  h->cfg = c;
+  h->rows = c.row_hi - c.row_lo;
+  h->kp = (c.k + 3) & ~3;
+  h->st = (cudaStream_t)c.stream;
+  h->dev = c.device;
+  h->T = (uint64_t)std::floor(4294967296.0 / c.r);   // R2
+  auto fail = [&](somf_status s) { *out = h; return s; };
+  if (cudaSetDevice(c.device) != cudaSuccess) { set_err(h, "cudaSetDevice failed"); return fail(SOMF_E_CUDA); }
+  cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, c.device);
+  const int k = c.k;
+  const int64_t rows = h->rows;
+#define A(call) do { if ((call) != cudaSuccess) { set_err(h, "allocation failed: %s", #call); return fail(SOMF_E_OOM); } } while (0)
+  A(dalloc(&h->D, (size_t)rows * h->kp));
+  A(dalloc(&h->Bbar, (size_t)rows * h->kp));
+  A(dalloc(&h->C64, (size_t)k * k));
+  A(dalloc(&h->C32, (size_t)k * k));
+  A(dalloc(&h->nslack, (size_t)k));
+  A(dalloc(&h->t_dev, 1));
+  A(dalloc(&h->w_dev, 1));
+  A(dalloc(&h->q_dev, 1));
+  A(dalloc(&h->nred_dev, 1));
+  A(dalloc(&h->err_dev, 1));
+  A(dalloc(&h->sweeps_dev, 1));
+  A(dalloc(&h->idx, (size_t)rows));
+  h->ntiles = (int)ceil_div(((c.row_hi - 1) >> 2) - (c.row_lo >> 2) + 1, kMaskThreads);
+  A(dalloc(&h->tile_counts, (size_t)h->ntiles));
+  A(dalloc(&h->perm, (size_t)k));
+  A(dalloc(&h->G64, (size_t)k * k));
+  A(dalloc(&h->beta64, (size_t)k * c.eta));
+  A(dalloc(&h->A64, (size_t)k * c.eta));
+  A(dalloc(&h->A32, (size_t)k * c.eta));
+  A(dalloc(&h->bar, 2));
+  A(dalloc(&h->qfull_dev, 1));
+  // BCD grid: co-resident CTAs (cooperative launch), at most 2 per SM
+  int occ = 0;
+  h->rows_cap = (int)ceil_div(rows, h->nsm) + 1;
+  size_t smem = ((size_t)((k + 3) & ~3) + h->rows_cap) * sizeof(float);
+  if (smem > 200 * 1024) { set_err(h, "too many rows per SM for the v1 BCD kernel"); return fail(SOMF_E_UNSUPPORTED); }
+  cudaFuncSetAttribute(k_bcd_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bcd_seq, kBcdThreads, smem);
+  occ = std::max(1, std::min(occ, 2));
+  h->bcd_grid = occ * h->nsm;
+  h->rows_cap = (int)ceil_div(rows, h->bcd_grid) + 1;
+  A(dalloc(&h->red, (size_t)2 * h->bcd_grid * kRedStride));
+#undef A
+  if (cudaMemset(h->bar, 0, 2 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
+      cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
+      cudaMemset(h->C64, 0, (size_t)k * k * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->C32, 0, (size_t)k * k * sizeof(float)) != cudaSuccess ||
+      cudaMemset(h->t_dev, 0, sizeof(int64_t)) != cudaSuccess ||
+      cudaMemset(h->err_dev, 0, sizeof(int)) != cudaSuccess ||
+      cudaMemset(h->sweeps_dev, 0, sizeof(int)) != cudaSuccess ||
+      cudaMemset(h->nred_dev, 0, sizeof(int64_t)) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess) {
+    set_err(h, "initialisation failed");
+    return fail(SOMF_E_CUDA);
+  }
+  *out = h;
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
+  if (!h) return SOMF_E_ARG;
+  void* ptrs[] = {h->D, h->Bbar, h->C64, h->C32, h->nslack, h->t_dev, h->w_dev, h->q_dev,
+                  h->nred_dev, h->err_dev, h->sweeps_dev, h->idx, h->tile_counts, h->perm,
+                  h->partial, h->G64, h->beta64, h->A64, h->A32, h->red, h->bar, h->Ge,
+                  h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : h->evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
+  for (auto e : h->pool) cudaEventDestroy(e);
+  delete h;
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int64_t ld) {
+  if (!h || !D0) return SOMF_E_ARG;
+  const int k = h->cfg.k;
+  if (ld < k) { set_err(h, "ld < k"); return SOMF_E_DIM; }
+  const void* src = nullptr;
+  if (somf_status s = resolve_in(h, D0, &src)) return s;
+  CK(cudaMemsetAsync(h->D, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
+  CK(cudaMemcpy2DAsync(h->D, h->kp * sizeof(float), src, ld * sizeof(float), k * sizeof(float),
+                       h->rows, cudaMemcpyDefault, h->st));
+  k_project_columns<<<k, kBcdThreads, 0, h->st>>>(h->D, h->rows, h->kp, nullptr, 1.0, 1.0 - h->cfg.mu,
+                                                  h->cfg.mu, h->cfg.pos_dict, h->D, h->nslack);
+  CKL();
+  CK(cudaMemsetAsync(h->Bbar, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
+  CK(cudaMemsetAsync(h->C64, 0, (size_t)k * k * sizeof(double), h->st));
+  CK(cudaMemsetAsync(h->C32, 0, (size_t)k * k * sizeof(float), h->st));
+  CK(cudaMemsetAsync(h->t_dev, 0, sizeof(int64_t), h->st));
+  h->t_host = 0;
+  h->mask_ready = false;
+  h->initialized = true;
+  return post_call(h);
+}
+
+// Phase timing (somf_profile_*): an event pair around each phase.
+struct PhaseScope {
+  somf_ctx* h;
+  int ph;
+  cudaEvent_t a = nullptr, b = nullptr;
+  PhaseScope(somf_ctx* h_, int ph_) : h(h_), ph(ph_) {
+    if (h->prof_on) {
+      a = take_event(h);
+      b = take_event(h);
+      if (a) cudaEventRecord(a, h->st);
+    }
+  }
+  ~PhaseScope() {
+    if (a && b) {
+      cudaEventRecord(b, h->st);
+      h->evs.push_back({ph, a, b});
+    }
+  }
+};
+
+static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, bool compact) {
+  const somf_config& c = h->cfg;
+  const int k = c.k, eta = c.eta;
+  if (!h->initialized) { set_err(h, "partial_fit before set_components / set_state"); return SOMF_E_STATE; }
+  if (ld < eta) { set_err(h, "ld < eta"); return SOMF_E_DIM; }
+  bool host = false;
+  const void* xs = nullptr;
+  if (somf_status s = resolve_in(h, X, &xs, &host)) return s;
+  const float* Xd = (const float*)xs;
+  const int64_t q_est = (int64_t)std::ceil(h->rows / c.r) + 64;
+  {
+    PhaseScope ps(h, SOMF_PH_MASK);
+    k_step_begin<<<1, 1, 0, h->st>>>(h->t_dev, h->w_dev, c.u);             // t <- t+1, w_t
+    CKL();
+    h->launches[SOMF_PH_MASK] += 1;
+    h->t_host += 1;
+    if (!h->mask_ready) {                                                    // M_t (Eq. mt)
+      if (somf_status s = launch_mask(h, h->t_dev, c.row_lo, c.row_lo, c.row_hi, h->T, h->idx,
+                                      h->tile_counts, h->q_dev, h->st))
+        return s;
+      h->launches[SOMF_PH_MASK] += 2;
+    }
+    h->mask_ready = false;
+    const size_t smem = (size_t)2 * k * sizeof(uint32_t);                   // Alg. 4 order
+    k_atom_perm<<<1, 32, smem, h->st>>>(c.seed, h->t_dev, k, c.perm_cyclic, h->perm);
+    CKL();
+    h->launches[SOMF_PH_MASK] += 1;
+  }
+  if (host && !compact && c.b_mode == SOMF_B_MASKED) {
+    // the selected rows of a host-resident batch cross the link once
+    PhaseScope ps(h, SOMF_PH_STAGE);
+    if (!h->Xstage) CK(dalloc(&h->Xstage, (size_t)h->rows * eta));
+    const int grid = std::max(1, std::min<int>((int)ceil_div(q_est, 8), 8 * h->nsm));
+    k_gather_rows<<<grid, 256, 0, h->st>>>(h->idx, h->q_dev, Xd, ld, eta, h->Xstage);
+    CKL();
+    h->launches[SOMF_PH_STAGE] += 1;
+    Xd = h->Xstage;
+    ld = eta;
+    compact = true;
+  }
+  {
+    PhaseScope ps(h, SOMF_PH_CONTRACT);                                      // Eq. (a)
+    if (somf_status s = launch_contract(h, true, compact, h->q_dev, q_est, Xd, ld, eta, c.r, h->beta64, h->G64))
+      return s;
+    h->launches[SOMF_PH_CONTRACT] += 2;
+  }
+  {
+    PhaseScope ps(h, SOMF_PH_CODES);                                         // Eq. somf_alpha
+    if (somf_status s = launch_codes(h, h->G64, h->beta64, eta, c.cd_tol, h->A64, h->A32)) return s;
+    h->launches[SOMF_PH_CODES] += 1;
+  }
+  {
+    PhaseScope ps(h, SOMF_PH_CBAR);                                          // Eq. somf_partial
+    k_cbar_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->A64, k, eta, h->w_dev, h->C64, h->C32);
+    CKL();
+    h->launches[SOMF_PH_CBAR] += 1;
+  }
+  {
+    PhaseScope ps(h, SOMF_PH_BBAR);
+    const int grid_a = (int)ceil_div(k, TN);
+    if (c.b_mode == SOMF_B_FULL) {
+      k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
+      const int grid_r = (int)std::min<int64_t>(ceil_div(h->rows, TM), 8 * h->nsm);
+      k_bbar_update<false, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
+          nullptr, h->qfull_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+      h->launches[SOMF_PH_BBAR] += 2;
+    } else {
+      const int grid_r = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q_est, TM), 8 * h->nsm));
+      if (compact)
+        k_bbar_update<true, true><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
+            h->idx, h->q_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+      else
+        k_bbar_update<true, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
+            h->idx, h->q_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+      h->launches[SOMF_PH_BBAR] += 1;
+    }
+    CKL();
+  }
+  {
+    PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
+    BcdArgs args{};
+    args.idx = h->idx;
+    args.q_dev = h->q_dev;
+    args.D = h->D;
+    args.Bbar = h->Bbar;
+    args.C64 = h->C64;
+    args.C32 = h->C32;
+    args.nslack = h->nslack;
+    args.perm = h->perm;
+    args.k = k;
+    args.kp = h->kp;
+    args.a = 1.0 - c.mu;
+    args.b = c.mu;
+    args.pos = c.pos_dict;
+    args.red = h->red;
+    args.bar = h->bar;
+    args.nred_out = h->nred_dev;
+    const size_t smem = ((size_t)((k + 3) & ~3) + h->rows_cap) * sizeof(float);
+    void* kargs[] = {&args};
+    CK(cudaLaunchCooperativeKernel((const void*)k_bcd_seq, dim3(h->bcd_grid), dim3(kBcdThreads), kargs,
+                                   smem, h->st));
+    h->launches[SOMF_PH_BCD] += 1;
+  }
+  h->steps_prof += 1;
+  return post_call(h);
+}
+
+SOMF_EXPORT somf_status somf_partial_fit(somf_handle h, const float* X, int64_t ld) {
+  if (!h || !X) return SOMF_E_ARG;
+  return partial_fit_impl(h, X, ld, false);
+}
+
+SOMF_EXPORT somf_status somf_next_mask(somf_handle h, int64_t* q_out, int32_t* idx_out) {
+  if (!h) return SOMF_E_ARG;
+  const somf_config& c = h->cfg;
+  if (!h->mask_ready) {
+    // draw M_{t+1}: the mask kernels read t from a device scalar
+    k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->t_host + 1);
+    CKL();
+    if (somf_status s = launch_mask(h, h->qfull_dev, c.row_lo, c.row_lo, c.row_hi, h->T, h->idx,
+                                    h->tile_counts, h->q_dev, h->st))
+      return s;
+    h->mask_ready = true;
+  }
+  int64_t q = 0;
+  CK(cudaMemcpyAsync(&q, h->q_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (q_out) *q_out = q;
+  if (idx_out && q > 0) {
+    CK(cudaMemcpyAsync(idx_out, h->idx, (size_t)q * sizeof(int32_t), cudaMemcpyDefault, h->st));
+    CK(cudaStreamSynchronize(h->st));
+  }
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_partial_fit_masked(somf_handle h, const float* X_M, int64_t ld) {
+  if (!h || !X_M) return SOMF_E_ARG;
+  if (!h->mask_ready) { set_err(h, "partial_fit_masked without a preceding somf_next_mask"); return SOMF_E_STATE; }
+  if (h->cfg.b_mode != SOMF_B_MASKED) { set_err(h, "partial_fit_masked requires b_mode MASKED"); return SOMF_E_STATE; }
+  return partial_fit_impl(h, X_M, ld, true);
+}
+
+SOMF_EXPORT somf_status somf_get_codes(somf_handle h, float* A_out) {
+  if (!h || !A_out) return SOMF_E_ARG;
+  CK(cudaMemcpyAsync(A_out, h->A32, (size_t)h->cfg.k * h->cfg.eta * sizeof(float), cudaMemcpyDefault, h->st));
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, A_out) != cudaSuccess) cudaGetLastError();
+  if (at.type != cudaMemoryTypeDevice) CK(cudaStreamSynchronize(h->st));
+  return post_call(h);
+}
+
+static somf_status ensure_eval(somf_ctx* h, int64_t m) {
+  if (m <= h->eval_cap) return SOMF_OK;
+  void* ps[] = {h->Ge, h->betae, h->Ae64, h->Ae32, h->colsq, h->objd};
+  for (void* p : ps)
+    if (p) CK(cudaFree(p));
+  const int k = h->cfg.k;
+  CK(dalloc(&h->Ge, (size_t)k * k));
+  CK(dalloc(&h->betae, (size_t)k * m));
+  CK(dalloc(&h->Ae64, (size_t)k * m));
+  CK(dalloc(&h->Ae32, (size_t)k * m));
+  CK(dalloc(&h->colsq, (size_t)m));
+  CK(dalloc(&h->objd, 1));
+  h->eval_cap = m;
+  return SOMF_OK;
+}
+
+static somf_status eval_codes(somf_ctx* h, const float* X, int64_t ld, int64_t m) {
+  if (!h->initialized) { set_err(h, "no dictionary yet"); return SOMF_E_STATE; }
+  if (m < 1 || m > (1 << 20)) { set_err(h, "m out of range"); return SOMF_E_ARG; }
+  if (ld < m) { set_err(h, "ld < m"); return SOMF_E_DIM; }
+  if (somf_status s = ensure_eval(h, m)) return s;
+  k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
+  CKL();
+  if (somf_status s = launch_contract(h, false, false, h->qfull_dev, h->rows, X, ld, (int)m, 1.0, h->betae, h->Ge))
+    return s;
+  return launch_codes(h, h->Ge, h->betae, (int)m, h->cfg.cd_tol * 1e-2, h->Ae64, h->Ae32);
+}
+
+SOMF_EXPORT somf_status somf_transform(somf_handle h, const float* X, int64_t ld, int64_t m, float* A_out) {
+  if (!h || !X || !A_out) return SOMF_E_ARG;
+  const void* xs = nullptr;
+  if (somf_status s = resolve_in(h, X, &xs)) return s;
+  if (somf_status s = eval_codes(h, (const float*)xs, ld, m)) return s;
+  CK(cudaMemcpyAsync(A_out, h->Ae32, (size_t)h->cfg.k * m * sizeof(float), cudaMemcpyDefault, h->st));
+  return post_call(h);
+}
+
+SOMF_EXPORT somf_status somf_objective(somf_handle h, const float* X, int64_t ld, int64_t m, double* obj_out) {
+  if (!h || !X || !obj_out) return SOMF_E_ARG;
+  const void* xs = nullptr;
+  if (somf_status s = resolve_in(h, X, &xs)) return s;
+  if (somf_status s = eval_codes(h, (const float*)xs, ld, m)) return s;
+  const int k = h->cfg.k;
+  CK(cudaMemsetAsync(h->colsq, 0, (size_t)m * sizeof(double), h->st));
+  const int grid_r = (int)std::min<int64_t>(ceil_div(h->rows, TM), 4 * h->nsm);
+  k_residual<<<dim3(grid_r, (unsigned)ceil_div(m, TN)), kGemmThreads, 0, h->st>>>(
+      h->D, h->kp, k, h->rows, (const float*)xs, ld, (int)m, h->Ae32, h->colsq);
+  CKL();
+  k_objective_final<<<1, 256, 0, h->st>>>(h->colsq, h->Ae64, k, (int)m, h->cfg.lambda, h->cfg.nu, h->objd);
+  CKL();
+  CK(cudaMemcpyAsync(obj_out, h->objd, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return post_call(h);
+}
+
+SOMF_EXPORT somf_status somf_components(somf_handle h, float* D_out, int64_t ld) {
+  if (!h || !D_out) return SOMF_E_ARG;
+  if (ld < h->cfg.k) { set_err(h, "ld < k"); return SOMF_E_DIM; }
+  CK(cudaMemcpy2DAsync(D_out, ld * sizeof(float), h->D, h->kp * sizeof(float), h->cfg.k * sizeof(float),
+                       h->rows, cudaMemcpyDefault, h->st));
+  return post_call(h);
+}
+
+SOMF_EXPORT somf_status somf_get_state(somf_handle h, float* D, float* Bbar, double* Cbar, double* n,
+                                       int64_t* t) {
+  if (!h) return SOMF_E_ARG;
+  const int k = h->cfg.k;
+  if (D)
+    CK(cudaMemcpy2DAsync(D, k * sizeof(float), h->D, h->kp * sizeof(float), k * sizeof(float), h->rows,
+                         cudaMemcpyDefault, h->st));
+  if (Bbar)
+    CK(cudaMemcpy2DAsync(Bbar, k * sizeof(float), h->Bbar, h->kp * sizeof(float), k * sizeof(float), h->rows,
+                         cudaMemcpyDefault, h->st));
+  if (Cbar) CK(cudaMemcpyAsync(Cbar, h->C64, (size_t)k * k * sizeof(double), cudaMemcpyDefault, h->st));
+  if (n) CK(cudaMemcpyAsync(n, h->nslack, (size_t)k * sizeof(double), cudaMemcpyDefault, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (t) *t = h->t_host;
+  return post_call(h);
+}
+
+__global__ void k_c64_to_c32(const double* a, float* b, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
+}
+
+SOMF_EXPORT somf_status somf_set_state(somf_handle h, const float* D, const float* Bbar, const double* Cbar,
+                                       const double* n, int64_t t) {
+  if (!h || !D || !Bbar || !Cbar || !n || t < 0) return SOMF_E_ARG;
+  const int k = h->cfg.k;
+  CK(cudaMemsetAsync(h->D, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
+  CK(cudaMemsetAsync(h->Bbar, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
+  CK(cudaMemcpy2DAsync(h->D, h->kp * sizeof(float), D, k * sizeof(float), k * sizeof(float), h->rows,
+                       cudaMemcpyDefault, h->st));
+  CK(cudaMemcpy2DAsync(h->Bbar, h->kp * sizeof(float), Bbar, k * sizeof(float), k * sizeof(float), h->rows,
+                       cudaMemcpyDefault, h->st));
+  CK(cudaMemcpyAsync(h->C64, Cbar, (size_t)k * k * sizeof(double), cudaMemcpyDefault, h->st));
+  CK(cudaMemcpyAsync(h->nslack, n, (size_t)k * sizeof(double), cudaMemcpyDefault, h->st));
+  k_c64_to_c32<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->C64, h->C32, k * k);
+  CKL();
+  k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->t_dev, t);
+  CKL();
+  CK(cudaStreamSynchronize(h->st));
+  h->t_host = t;
+  h->mask_ready = false;
+  h->initialized = true;
+  return post_call(h);
+}
+
+SOMF_EXPORT somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* nred, double* w) {
+  if (!h) return SOMF_E_ARG;
+  if (q) CK(cudaMemcpyAsync(q, h->q_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
+  if (nred) CK(cudaMemcpyAsync(nred, h->nred_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
+  if (w) CK(cudaMemcpyAsync(w, h->w_dev, sizeof(double), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_profile_enable(somf_handle h, int32_t on) {
+  if (!h) return SOMF_E_ARG;
+  h->prof_on = on != 0;
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_profile_read(somf_handle h, double* ms, int64_t* launches, int64_t* steps) {
+  if (!h) return SOMF_E_ARG;
+  CK(cudaStreamSynchronize(h->st));
+  double acc[SOMF_NPHASE] = {};
+  for (auto& e : h->evs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, e.a, e.b));
+    acc[e.ph] += t;
+    h->pool.push_back(e.a);
+    h->pool.push_back(e.b);
+  }
+  h->evs.clear();
+  for (int i = 0; i < SOMF_NPHASE; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (launches) launches[i] = h->launches[i];
+    h->launches[i] = 0;
+  }
+  if (steps) *steps = h->steps_prof;
+  h->steps_prof = 0;
+  return SOMF_OK;
+}
+
+// ---- stateless -------------------------------------------------------------
+SOMF_EXPORT somf_status somf_mask_rows(uint64_t seed, int64_t t, int64_t row_lo, int64_t row_hi, double r,
+                                       int32_t* idx, int64_t* q_out, void* stream) {
+  if (!idx || !q_out || row_lo < 0 || row_hi <= row_lo || !(r >= 1.0)) return SOMF_E_ARG;
+  somf_ctx tmp;
+  somf_ctx* h = &tmp;
+  h->cfg.seed = seed;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* td = nullptr;
+  int64_t* qd = nullptr;
+  int32_t* tiles = nullptr;
+  const int ntiles = (int)ceil_div(((row_hi - 1) >> 2) - (row_lo >> 2) + 1, kMaskThreads);
+  CK(dalloc(&td, 1));
+  CK(dalloc(&qd, 1));
+  CK(dalloc(&tiles, (size_t)ntiles));
+  k_set_scalar_i64<<<1, 1, 0, st>>>(td, t);
+  const uint64_t T = (uint64_t)std::floor(4294967296.0 / r);
+  somf_status s = launch_mask(h, td, 0, row_lo, row_hi, T, idx, tiles, qd, st);
+  if (s == SOMF_OK) {
+    CK(cudaMemcpyAsync(q_out, qd, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  cudaFree(td);
+  cudaFree(qd);
+  cudaFree(tiles);
+  return s;
+}
+
+SOMF_EXPORT somf_status somf_atom_permutation(uint64_t seed, int64_t t, int32_t k, int32_t cyclic, int32_t* perm,
+                                              void* stream) {
+  if (!perm || k < 1 || k > 4096) return SOMF_E_ARG;
+  somf_ctx tmp;
+  somf_ctx* h = &tmp;
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t* td = nullptr;
+  CK(dalloc(&td, 1));
+  k_set_scalar_i64<<<1, 1, 0, st>>>(td, t);
+  k_atom_perm<<<1, 32, (size_t)2 * k * sizeof(uint32_t), st>>>(seed, td, k, cyclic, perm);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  cudaFree(td);
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_column_ids(uint64_t seed, int64_t n, int64_t s0, int64_t count, int64_t* ids,
+                                        void* stream) {
+  if (!ids || n < 1 || s0 < 0 || count < 0) return SOMF_E_ARG;
+  if (count == 0) return SOMF_OK;
+  somf_ctx tmp;
+  somf_ctx* h = &tmp;
+  int b = 2;
+  while ((1ll << b) < n) ++b;
+  b += b & 1;
+  k_column_ids<<<(unsigned)ceil_div(count, 256), 256, 0, (cudaStream_t)stream>>>(seed, n, s0, count, b / 2, ids);
+  CKL();
+  return SOMF_OK;
+}
+
+SOMF_EXPORT somf_status somf_project_columns(const float* U, int64_t len, int32_t m, int64_t ld,
+                                             const double* radius, double mu, int32_t positive, float* Out,
+                                             void* stream) {
+  if (!U || !Out || !radius || len < 1 || m < 1 || ld < m || !(mu >= 0.0 && mu <= 1.0)) return SOMF_E_ARG;
+  somf_ctx tmp;
+  somf_ctx* h = &tmp;
+  k_project_columns<<<m, kBcdThreads, 0, (cudaStream_t)stream>>>(U, len, ld, radius, 0.0, 1.0 - mu, mu,
+                                                                 positive, Out, nullptr);
+  CKL();
+  return SOMF_OK;
+}

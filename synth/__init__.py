@@ -14,6 +14,7 @@ from .generators import (  # noqa: F401
     fmri_dictionary,
     fmri_codes,
     fmri_matrix,
+    fmri_stream,
     hyperspectral_patches,
     nmf_matrix,
     random_state_for_step,

@@ -129,6 +129,21 @@ def fmri_matrix(shape=(61, 73, 61), p: int | None = 212445, k: int = 70,
     return X, Dstar, A
 
 
+def fmri_stream(n_cols: int, p: int = 212445, k_true: int = 70, shape=(61, 73, 61),
+                T: int = 1200, snr: float = 0.5, seed: int = 0):
+    """cfgC stand-in at full size: ``n_cols`` consecutive columns of one
+    record (float32, p x n_cols, row-major numpy), generated as in
+    ``fmri_matrix`` but without holding a float64 copy."""
+    coords = fmri_voxel_grid(shape, p)
+    Dstar = fmri_dictionary(coords, k_true, seed=seed).astype(np.float32)
+    A = fmri_codes(k_true, 1, T=max(T, n_cols), seed=seed + 1)[:, :n_cols].astype(np.float32)
+    pp = coords.shape[0]
+    rng = np.random.default_rng(seed + 2)
+    X = Dstar @ A
+    X += np.float32(math.sqrt(k_true / pp / snr)) * rng.standard_normal((pp, n_cols), dtype=np.float32)
+    return X
+
+
 # ----------------------------------------------------------------------------
 # cfgB: hyperspectral patches
 # ----------------------------------------------------------------------------

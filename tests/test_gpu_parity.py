@@ -1,0 +1,268 @@
+"""GPU (CUDA, through the C ABI) vs float64 oracle parity -- needs a B200.
+
+Bars (BASELINE.json north_star):
+  * mask indices, atom order, column ids: bit-exact;
+  * one step's alpha, Cbar, Bbar, D (and n): <= 1e-4 relative Frobenius error;
+  * held-out objective after 100 iterations: <= 1e-3 relative;
+  * projection kernel vs the oracle's exact projection: <= 2e-6 relative
+    (float32 inputs, float64 threshold arithmetic).
+The oracle always starts from the same float32-rounded state the GPU holds.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import synth  # noqa: E402
+from oracle import streams as ostreams  # noqa: E402
+from oracle.prox import enet_projection, enet_value  # noqa: E402
+from oracle.somf import SomfOracle, OracleConfig, objective, transform  # noqa: E402
+
+TOL_STEP = 1e-4
+TOL_OBJ = 1e-3
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def somf():
+    import paper_1701_05363_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+def cuda(a):
+    return torch.tensor(np.asarray(a, np.float32), device="cuda")
+
+
+# ---------------------------------------------------------------------------
+# random draws: bit-exact
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("p,r,lo,hi", [(1, 1.0, 0, 1), (3, 2.0, 0, 3), (1001, 1.0, 0, 1001),
+                                       (5003, 3.0, 0, 5003), (5003, 3.0, 1001, 3333),
+                                       (212445, 12.0, 0, 212445), (2_000_000, 24.0, 123457, 2_000_000),
+                                       (64, 1e9, 0, 64), (70001, 4.0, 7, 70001)])
+def test_mask_bit_exact(somf, p, r, lo, hi):
+    for t in (1, 2, 50):
+        got = somf.mask_rows(11, t, lo, hi, r)
+        ref = ostreams.mask_rows(11, t, p, r, lo, hi)
+        assert np.array_equal(got, ref), (p, r, lo, hi, t)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 70, 128, 256])
+def test_atom_permutation_bit_exact(somf, k):
+    for t in (1, 7, 1000):
+        assert np.array_equal(somf.atom_permutation(5, t, k), ostreams.atom_permutation(5, t, k))
+    assert np.array_equal(somf.atom_permutation(5, 1, k, cyclic=True), np.arange(k))
+
+
+@pytest.mark.parametrize("n", [1, 7, 1000, 4097, 2_400_000])
+def test_column_ids_bit_exact(somf, n):
+    for s0, cnt in ((0, 3000), (n - 5 if n > 5 else 0, 900), (5 * n + 3, 777)):
+        got = somf.column_ids(3, n, s0, cnt).cpu().numpy()
+        assert np.array_equal(got, ostreams.column_ids(3, n, s0, cnt))
+
+
+# ---------------------------------------------------------------------------
+# projection kernel
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("mu,pos", [(0.0, False), (0.5, False), (1.0, False), (0.0, True), (1.0, True),
+                                    (0.3, True)])
+def test_project_columns(somf, mu, pos):
+    rng = np.random.default_rng(1)
+    for length in (1, 37, 1000, 17704):
+        m = 9
+        U = f32(rng.standard_t(3, size=(length, m)) * rng.choice([0.01, 0.1, 1.0]))
+        radius = np.array([0.0, 1e-3, 0.1, 0.5, 1.0, 2.0, 10.0, 0.05, 1e3])
+        out = somf.project_columns(cuda(U), torch.tensor(radius), mu, pos).cpu().numpy()
+        for j in range(m):
+            ref = enet_projection(U[:, j], radius[j], mu, pos)
+            scale = max(np.abs(U[:, j]).max(), 1e-30)
+            assert np.abs(out[:, j] - ref).max() <= 2e-6 * scale, (length, j)
+
+
+# ---------------------------------------------------------------------------
+# one SOMF step from a mid-trajectory state
+# ---------------------------------------------------------------------------
+CASES = {
+    # name: (p, k, eta, kwargs, data)
+    "cfgA_ridge_l1": (256, 10, 10, dict(lam=0.1, nu=1.0, mu=0.0, r=4.0, u=0.95), "tiny"),
+    "ridge_l1_fmri_small": (3000, 24, 40, dict(lam=1e-3, nu=1.0, mu=0.0, r=12.0, u=0.917), "fmri"),
+    "lasso_l2_hyper_small": (1536, 40, 32, dict(lam=0.1, nu=0.0, mu=1.0, r=4.0, u=0.917), "hyper"),
+    "nmf_small": (2048, 24, 48, dict(lam=0.05, nu=1.0, pos_code=True, mu=1.0, pos_dict=True, r=8.0), "nmf"),
+    "enet_enet": (2500, 36, 40, dict(lam=0.05, nu=0.0, mu=0.5, r=4.0), "fmri"),
+    "ridge_l2_r1": (700, 20, 30, dict(lam=0.2, nu=1.0, mu=1.0, r=1.0), "tiny"),
+    "lasso_k256_ragged": (1520, 256, 33, dict(lam=0.05, nu=0.0, mu=1.0, r=3.0), "hyper"),
+}
+
+
+def _data(kind, p, n, seed=0):
+    if kind == "tiny":
+        X, _, _ = synth.tiny_dictionary_learning(p=p, n=n, seed=seed)
+    elif kind == "fmri":
+        X, _, _ = synth.fmri_matrix(shape=(20, 20, 20), p=p, k=16, n_records=1, T=n, seed=seed)
+    elif kind == "hyper":
+        X = synth.hyperspectral_patches(n, size=4, bands=p // 16, n_end=16, seed=seed)
+    else:
+        X = synth.nmf_matrix(p=p, n=n, k_true=12, seed=seed)
+    return f32(X)
+
+
+def _pair(somf, name, t0=5, seed=3):
+    p, k, eta, kw, kind = CASES[name]
+    X = _data(kind, p, k + (t0 + 3) * eta)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=seed, **kw))
+    ora.set_components(X[:, :k])
+    for t in range(t0):
+        ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
+    # the oracle continues from the float32-rounded state the GPU holds
+    ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
+    gpu = somf.Somf(p, k, eta, seed=seed, debug=True, **kw)
+    gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
+    return ora, gpu, X, (p, k, eta)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_one_step_parity(somf, name):
+    ora, gpu, X, (p, k, eta) = _pair(somf, name)
+    batch = X[:, k + 5 * eta:k + 6 * eta]
+    out = ora.partial_fit(batch)
+    gpu.partial_fit(cuda(batch))
+    A = gpu.get_codes().cpu().numpy()
+    st = gpu.get_state()
+    info = gpu.last_step_info()
+    assert info["q"] == out["S"].size
+    assert st["t"] == ora.t
+    errs = dict(alpha=rel(A, out["A"]), Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar),
+                D=rel(st["D"], ora.D), n=rel(st["n"], ora.n))
+    assert all(v <= TOL_STEP for v in errs.values()), errs
+    # freezing: rows outside S_t are bit-identical to the loaded state
+    notS = np.setdiff1d(np.arange(p), out["S"])
+    np.testing.assert_array_equal(st["D"][notS], ora.D[notS].astype(np.float32))
+
+
+@pytest.mark.parametrize("name", ["cfgA_ridge_l1", "lasso_l2_hyper_small", "nmf_small"])
+def test_masked_api_and_pinned_input_match(somf, name):
+    ora, gpu, X, (p, k, eta) = _pair(somf, name)
+    _, gpu2, _, _ = _pair(somf, name)
+    _, gpu3, _, _ = _pair(somf, name)
+    batch = X[:, k + 5 * eta:k + 6 * eta]
+    q, idx = gpu.next_mask()
+    ref_S = ostreams.mask_rows(3, ora.t + 1, p, CASES[name][3]["r"])
+    assert np.array_equal(idx, ref_S) and q == ref_S.size
+    gpu.partial_fit_masked(cuda(batch[idx]))
+    gpu2.partial_fit(cuda(batch))
+    pinned = torch.tensor(batch.astype(np.float32)).pin_memory()
+    gpu3.partial_fit(pinned)
+    torch.cuda.synchronize()
+    s1, s2, s3 = gpu.get_state(), gpu2.get_state(), gpu3.get_state()
+    for key in ("D", "Bbar", "Cbar", "n"):
+        np.testing.assert_array_equal(s1[key], s2[key])
+        np.testing.assert_array_equal(s3[key], s2[key])
+
+
+def test_empty_mask_step(somf):
+    """r so large that S_t is empty: codes are 0 (G = 0, beta = 0), D frozen."""
+    p, k, eta = 64, 4, 5
+    kw = dict(lam=0.1, nu=1.0, mu=0.0, r=1e9)
+    X = _data("tiny", p, 40)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=0, **kw))
+    ora.set_components(X[:, :k])
+    gpu = somf.Somf(p, k, eta, seed=0, debug=True, **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    D0 = gpu.get_state()["D"]
+    ora.partial_fit(X[:, 10:15])
+    gpu.partial_fit(cuda(X[:, 10:15]))
+    st = gpu.get_state()
+    assert gpu.last_step_info()["q"] == 0
+    np.testing.assert_array_equal(st["D"], D0)
+    assert np.abs(gpu.get_codes().cpu().numpy()).max() == 0.0
+    assert rel(st["Cbar"], ora.Cbar) == 0.0
+
+
+def test_set_components_projects_and_slacks(somf):
+    p, k = 5000, 12
+    rng = np.random.default_rng(4)
+    D0 = f32(rng.standard_normal((p, k)))
+    for mu, pos in ((0.0, False), (1.0, False), (0.5, True)):
+        ora = SomfOracle(OracleConfig(p=p, k=k, eta=4, mu=mu, pos_dict=pos))
+        ora.set_components(D0)
+        gpu = somf.Somf(p, k, 4, mu=mu, pos_dict=pos, debug=True)
+        gpu.set_components(cuda(D0))
+        st = gpu.get_state()
+        assert rel(st["D"], ora.D) < 1e-5
+        np.testing.assert_allclose(st["n"], ora.n, atol=1e-6)
+        assert st["t"] == 0 and np.abs(st["Cbar"]).max() == 0 and np.abs(st["Bbar"]).max() == 0
+
+
+# ---------------------------------------------------------------------------
+# trajectory: objective after 100 iterations
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,iters", [("cfgA_ridge_l1", 100), ("ridge_l1_fmri_small", 100),
+                                        ("nmf_small", 100)])
+def test_trajectory_objective(somf, name, iters):
+    p, k, eta, kw, kind = CASES[name]
+    X = _data(kind, p, k + iters * eta + 200, seed=1)
+    Xte = X[:, -200:]
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=9, **kw))
+    ora.set_components(X[:, :k])
+    gpu = somf.Somf(p, k, eta, seed=9, **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    Xg = cuda(X)
+    for t in range(iters):
+        ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
+        gpu.partial_fit(Xg[:, k + t * eta:k + (t + 1) * eta].contiguous())
+    f_ref = ora.objective(Xte)
+    f_gpu = gpu.objective(cuda(Xte))
+    assert abs(f_gpu - f_ref) <= TOL_OBJ * abs(f_ref), (f_gpu, f_ref)
+
+
+# ---------------------------------------------------------------------------
+# evaluation kernels
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("nu,mu,pos", [(1.0, 0.0, False), (0.0, 1.0, False), (1.0, 1.0, True), (0.3, 0.5, False)])
+def test_objective_and_transform(somf, nu, mu, pos):
+    p, k, m = 4000, 20, 300
+    rng = np.random.default_rng(5)
+    X = f32(np.abs(rng.standard_normal((p, m))) if pos else rng.standard_normal((p, m)))
+    gpu = somf.Somf(p, k, 8, lam=0.1, nu=nu, mu=mu, pos_code=pos, pos_dict=pos, debug=True)
+    gpu.set_components(cuda(X[:, :k]))
+    D = gpu.get_state()["D"].astype(np.float64)
+    f_ref = objective(D, X, 0.1, nu, pos)
+    assert abs(gpu.objective(cuda(X)) - f_ref) <= 1e-5 * abs(f_ref)
+    A_ref = transform(D, X, 0.1, nu, pos)
+    assert rel(gpu.transform(cuda(X)).cpu().numpy(), A_ref) <= TOL_STEP
+
+
+# ---------------------------------------------------------------------------
+# full-size cfgC step (BASELINE configs[2]) in the launch configuration bench.py times
+# ---------------------------------------------------------------------------
+def test_full_size_fmri_step(somf):
+    import bench
+    p, k, eta, r = 212445, 70, 200, 12.0
+    X, D0 = bench.fmri_inputs_cpu(n_cols=k + 2 * eta, seed=0)
+    kw = dict(lam=1e-3, nu=1.0, mu=0.0, r=r, u=0.917)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=0, **kw))
+    ora.set_components(D0)
+    gpu = somf.Somf(p, k, eta, seed=0, **kw)
+    gpu.set_components(cuda(D0))
+    for t in range(2):
+        batch = X[:, t * eta:(t + 1) * eta]
+        out = ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+    st = gpu.get_state()
+    S = out["S"]
+    errs = dict(alpha=rel(gpu.get_codes().cpu().numpy(), out["A"]), Cbar=rel(st["Cbar"], ora.Cbar),
+                Bbar_S=rel(st["Bbar"][S], ora.Bbar[S]), D_S=rel(st["D"][S], ora.D[S]), n=rel(st["n"], ora.n))
+    assert all(v <= TOL_STEP for v in errs.values()), errs
