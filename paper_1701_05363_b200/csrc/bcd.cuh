@@ -92,6 +92,9 @@ k_bcd_seq(BcdArgs P) {
     const int j = P.perm[pi];
     const double cjj = P.C64[(int64_t)j * k + j];
     if (!(cjj > 1e-12 * dmax)) continue;                       // R10: dead atom
+    // n_j is read before this atom's first grid barrier: block 0 rewrites it
+    // after the atom's last barrier, so every CTA sees the same n_{t-1}^(j).
+    const double nj = P.nslack[j];
     for (int l = tid; l < k; l += nt) ccol[l] = P.C32[(int64_t)j * k + l];
     __syncthreads();
     const float invc = (float)(1.0 / cjj);
@@ -113,7 +116,7 @@ k_bcd_seq(BcdArgs P) {
     }
     grid_reduce<5>(s, P.red, P.bar, parity, scratch, bcast);
     ++nred;
-    const double rho = fmax(0.0, P.nslack[j] + a * s[0] + 0.5 * b * s[1]);   // P:860, R9
+    const double rho = fmax(0.0, nj + a * s[0] + 0.5 * b * s[1]);            // P:860, R9
     const double Nv = a * s[3] + 0.5 * b * s[4];
     double lam = 0.0, Nd = Nv;
     bool zero = false;
@@ -124,17 +127,19 @@ k_bcd_seq(BcdArgs P) {
         lam = enet_lambda(a, b, rho, cnt, S1, S2);
         if (a > 0.0) {
           // Michelot: shrink the active set {|v| > a lam} until it is stable
+          // (threshold compared in float64: a float-rounded a*lam can exclude
+          // the last active entry and make the iteration cycle)
           for (int it = 0; it < 4096; ++it) {
-            const float thr = (float)(a * lam);
+            const double thr = a * lam;
             double t3[3] = {0.0, 0.0, 0.0};
             for (int64_t m = lo + tid; m < hi; m += nt) {
               const float v = vbuf[m - lo];
-              const float av = fabsf(v);
-              if (av > thr) { t3[0] += 1.0; t3[1] += av; t3[2] += (double)v * v; }
+              const double av = fabs((double)v);
+              if (av > thr) { t3[0] += 1.0; t3[1] += av; t3[2] += av * av; }
             }
             grid_reduce<3>(t3, P.red, P.bar, parity, scratch, bcast);
             ++nred;
-            if (t3[0] == cnt) break;
+            if (t3[0] == cnt || t3[0] == 0.0) break;
             cnt = t3[0]; S1 = t3[1]; S2 = t3[2];
             lam = enet_lambda(a, b, rho, cnt, S1, S2);
           }
@@ -145,7 +150,7 @@ k_bcd_seq(BcdArgs P) {
         Nd = a * sd + 0.5 * b * sd2;
       }
     }
-    const float thr = (float)(a * lam);
+    const double thr = a * lam;
     const double inv1 = 1.0 / (1.0 + b * lam);
     for (int64_t m = lo + tid; m < hi; m += nt) {
       const int64_t g = P.idx ? (int64_t)P.idx[m] : m;
@@ -153,7 +158,7 @@ k_bcd_seq(BcdArgs P) {
       float d;
       if (zero) d = 0.f;
       else if (lam == 0.0) d = v;
-      else d = copysignf((float)(fmax((double)fabsf(v) - (double)thr, 0.0) * inv1), v);
+      else d = copysignf((float)(fmax(fabs((double)v) - thr, 0.0) * inv1), v);
       P.D[g * kp + j] = d;
     }
     if (blockIdx.x == 0 && tid == 0) P.nslack[j] = rho - Nd;
@@ -192,16 +197,16 @@ k_project_columns(const float* __restrict__ U, int64_t len, int64_t ld, const do
       lam = enet_lambda(a, b, rho, cnt, S1, S2);
       if (a > 0.0) {
         for (int it = 0; it < 4096; ++it) {
-          const float thr = (float)(a * lam);
+          const double thr = a * lam;
           double t3[3] = {0.0, 0.0, 0.0};
           for (int64_t i = tid; i < len; i += nt) {
             float v = U[i * ld + j];
             if (pos) v = fmaxf(v, 0.f);
-            const float av = fabsf(v);
-            if (av > thr) { t3[0] += 1.0; t3[1] += av; t3[2] += (double)v * v; }
+            const double av = fabs((double)v);
+            if (av > thr) { t3[0] += 1.0; t3[1] += av; t3[2] += av * av; }
           }
           block_sum<3>(t3, scratch);
-          if (t3[0] == cnt) break;
+          if (t3[0] == cnt || t3[0] == 0.0) break;
           cnt = t3[0]; S1 = t3[1]; S2 = t3[2];
           lam = enet_lambda(a, b, rho, cnt, S1, S2);
         }
@@ -209,7 +214,7 @@ k_project_columns(const float* __restrict__ U, int64_t len, int64_t ld, const do
     }
   }
   __syncthreads();
-  const float thr = (float)(a * lam);
+  const double thr = a * lam;
   const double inv1 = 1.0 / (1.0 + b * lam);
   double nd[2] = {0.0, 0.0};
   for (int64_t i = tid; i < len; i += nt) {
@@ -218,7 +223,7 @@ k_project_columns(const float* __restrict__ U, int64_t len, int64_t ld, const do
     float d;
     if (zero) d = 0.f;
     else if (lam == 0.0) d = v;
-    else d = copysignf((float)(fmax((double)fabsf(v) - (double)thr, 0.0) * inv1), v);
+    else d = copysignf((float)(fmax(fabs((double)v) - thr, 0.0) * inv1), v);
     Out[i * ld + j] = d;
     nd[0] += fabs((double)d);
     nd[1] += (double)d * d;

@@ -94,6 +94,14 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// bar[2] (when non-null callers pass bar + 2 as err) receives 1 if a CTA
+// waited more than 2 s: a protocol bug must not hang the GPU.
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -106,7 +114,11 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
       __threadfence();
       st_release_gpu(bar + 1, gen + 1);
     } else {
-      while (ld_acquire_gpu(bar + 1) == gen) { __nanosleep(32); }
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu(bar + 1) == gen) {
+        __nanosleep(32);
+        if (globaltimer_ns() - t0 > 2000000000ull) { atomicExch(bar + 2, 1u); break; }
+      }
     }
     __threadfence();
   }

@@ -164,13 +164,22 @@ static void set_err(somf_ctx* h, const char* fmt, ...) {
 
 #define CKL()  CK(cudaGetLastError())
 
+// Device-side flags: err_dev (numerical) and bar[2] (grid-barrier watchdog).
+static somf_status check_flags(somf_ctx* h) {
+  int e = 0;
+  unsigned b = 0;
+  CK(cudaMemcpy(&e, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&b, h->bar + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (b) { set_err(h, "grid barrier watchdog fired in the BCD kernel (results invalid)"); return SOMF_E_CUDA; }
+  if (e) { set_err(h, "device numerical error flag %d (non-SPD system in the code solve)", e); return SOMF_E_NONFINITE; }
+  return SOMF_OK;
+}
+
 static somf_status post_call(somf_ctx* h) {
   CKL();
   if (h->cfg.debug) {
     CK(cudaStreamSynchronize(h->st));
-    int e = 0;
-    CK(cudaMemcpy(&e, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
-    if (e) { set_err(h, "device numerical error flag %d", e); return SOMF_E_NONFINITE; }
+    return check_flags(h);
   }
   return SOMF_OK;
 }
@@ -369,7 +378,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->beta64, (size_t)k * c.eta));
   A(dalloc(&h->A64, (size_t)k * c.eta));
   A(dalloc(&h->A32, (size_t)k * c.eta));
-  A(dalloc(&h->bar, 2));
+  A(dalloc(&h->bar, 4));
   A(dalloc(&h->qfull_dev, 1));
   // BCD grid: co-resident CTAs (cooperative launch), at most 2 per SM
   int occ = 0;
@@ -383,7 +392,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   h->rows_cap = (int)ceil_div(rows, h->bcd_grid) + 1;
   A(dalloc(&h->red, (size_t)2 * h->bcd_grid * kRedStride));
 #undef A
-  if (cudaMemset(h->bar, 0, 2 * sizeof(unsigned)) != cudaSuccess ||
+  if (cudaMemset(h->bar, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->C64, 0, (size_t)k * k * sizeof(double)) != cudaSuccess ||
@@ -684,6 +693,7 @@ SOMF_EXPORT somf_status somf_get_state(somf_handle h, float* D, float* Bbar, dou
   if (n) CK(cudaMemcpyAsync(n, h->nslack, (size_t)k * sizeof(double), cudaMemcpyDefault, h->st));
   CK(cudaStreamSynchronize(h->st));
   if (t) *t = h->t_host;
+  if (somf_status st = check_flags(h)) return st;
   return post_call(h);
 }
 
@@ -721,7 +731,7 @@ SOMF_EXPORT somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* 
   if (nred) CK(cudaMemcpyAsync(nred, h->nred_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, h->st));
   if (w) CK(cudaMemcpyAsync(w, h->w_dev, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
-  return SOMF_OK;
+  return check_flags(h);
 }
 
 SOMF_EXPORT somf_status somf_profile_enable(somf_handle h, int32_t on) {
