@@ -373,6 +373,7 @@ def run_somf(args):
             t3 = time_steps(m3, batches, 3, 5, flush, stream)
             sm = sum(t3) / len(t3)
             sweep[f"r={int(rr)}"] = {"columns_per_s": eta / (sm * 1e-3), "ms_per_step": sm,
+                                     "bcd_kernel": m3.bcd_variant,
                                      "bcd_grid_reductions": m3.last_step_info()["bcd_reductions"]}
             del m3
 
@@ -391,6 +392,7 @@ def run_somf(args):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (fMRI-shaped stand-in, DESIGN.md §3)",
             "config": {"workload": w["name"], "p": p, "k": k, "eta": eta, "r": r, "lambda": w["lam"],
                        "code": "ridge", "dict": "l1-ball", "b_mode": "masked",
+                       "bcd_kernel": model.bcd_variant,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "parallelism": "single" if world == 1 else f"replicas x{world}"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,

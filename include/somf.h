@@ -90,6 +90,10 @@ typedef struct somf_config {
   int32_t device;         /* CUDA device ordinal                                 */
   void* stream;           /* cudaStream_t (NULL = legacy default stream)         */
   int32_t debug;          /* 1: synchronise and check after every call          */
+  int32_t bcd_kernel;     /* Alg. 4 kernel: 0 = auto (on-chip when the masked
+                             rows fit in registers + shared memory, else global),
+                             1 = global-memory kernel, 2 = on-chip kernel
+                             (SOMF_E_UNSUPPORTED at create if it cannot fit)   */
 } somf_config;
 
 /* Fills *cfg with defaults: u = 0.917, r = 1, nu = 1, mu = 0,
@@ -176,6 +180,11 @@ somf_status somf_set_state(somf_handle h, const float* D, const float* Bbar,
  * q = |S_t|, bcd_reductions = grid-wide reductions spent in Alg. 4, w = w_t. */
 somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* bcd_reductions,
                                 double* w);
+
+/* Alg. 4 kernel this handle launches: 1 = global-memory (per-atom grid
+ * reductions, rows re-read from L2/HBM), 2 = on-chip (masked rows resident in
+ * registers + shared memory).  0 on a null handle. */
+int32_t somf_bcd_variant(somf_handle h);
 
 /* ---- per-phase timing of somf_partial_fit (CUDA events on config.stream) ---- */
 enum {

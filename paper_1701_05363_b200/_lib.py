@@ -52,6 +52,7 @@ class SomfConfig(C.Structure):
         ("cd_tol", C.c_double), ("cd_max_sweeps", C.c_int32),
         ("seed", C.c_uint64), ("row_lo", C.c_int64), ("row_hi", C.c_int64),
         ("device", C.c_int32), ("stream", C.c_void_p), ("debug", C.c_int32),
+        ("bcd_kernel", C.c_int32),
     ]
 
 
@@ -77,6 +78,7 @@ SIGNATURES = [
     ("somf_get_state", I32, [P, P, P, P, P, C.POINTER(I64)]),
     ("somf_set_state", I32, [P, P, P, P, P, I64]),
     ("somf_last_step_info", I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(D)]),
+    ("somf_bcd_variant", I32, [P]),
     ("somf_profile_enable", I32, [P, I32]),
     ("somf_profile_read", I32, [P, P, P, C.POINTER(I64)]),
     ("somf_mask_rows", I32, [U64, I64, I64, I64, D, P, C.POINTER(I64), P]),

@@ -27,6 +27,7 @@
 #include "gemm.cuh"
 #include "solve.cuh"
 #include "bcd.cuh"
+#include "bcd_onchip.cuh"
 
 using namespace somf;
 
@@ -116,6 +117,16 @@ struct somf_ctx {
   unsigned* bar = nullptr;
   int bcd_grid = 0;
   int rows_cap = 0;          // rows per BCD CTA upper bound
+  // on-chip BCD (bcd_onchip.cuh): chosen when the masked rows fit on chip
+  int64_t q_cap = 0;         // masked-row capacity (mean + 10 sigma of |S_t|)
+  const void* oc_fn = nullptr;
+  int oc_cap_rows = 0, oc_cs = 0, oc_rpw = 0, oc_kc = 0;
+  size_t oc_smem = 0;
+  double* theta_ws = nullptr;
+  double* oc_acc = nullptr;
+  unsigned* oc_accmin = nullptr;
+  double* oc_rho = nullptr;
+  unsigned* oc_bar = nullptr;
   // evaluation scratch (objective / transform)
   int64_t eval_cap = 0;
   double *Ge = nullptr, *betae = nullptr, *Ae64 = nullptr, *colsq = nullptr, *objd = nullptr;
@@ -169,8 +180,12 @@ static somf_status check_flags(somf_ctx* h) {
   int e = 0;
   unsigned b = 0;
   CK(cudaMemcpy(&e, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  unsigned b2 = 0;
   CK(cudaMemcpy(&b, h->bar + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
-  if (b) { set_err(h, "grid barrier watchdog fired in the BCD kernel (results invalid)"); return SOMF_E_CUDA; }
+  if (h->oc_bar) CK(cudaMemcpy(&b2, h->oc_bar + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (b || b2) { set_err(h, "grid barrier watchdog fired in the BCD kernel (results invalid)"); return SOMF_E_CUDA; }
+  if (e == 2) { set_err(h, "more masked rows than the on-chip BCD capacity (q > mean + 10 sigma)"); return SOMF_E_CUDA; }
+  if (e == 3) { set_err(h, "projection threshold search hit its round cap"); return SOMF_E_CUDA; }
   if (e) { set_err(h, "device numerical error flag %d (non-SPD system in the code solve)", e); return SOMF_E_NONFINITE; }
   return SOMF_OK;
 }
@@ -298,6 +313,53 @@ static somf_status launch_mask(somf_ctx* h, const int64_t* t_dev_ptr, int64_t id
 }
 
 // ---------------------------------------------------------------------------
+// on-chip BCD variants: KC = columns per lane (ceil(kp/32), 5..7 -> 8),
+// RPW = masked rows per warp; R lives in RPW*KC registers per thread.
+// ---------------------------------------------------------------------------
+struct OcVariant { int kc, rpw; const void* fn; };
+#define OCV(KC, RPW) {KC, RPW, (const void*)k_bcd_onchip<KC, RPW>}
+static const OcVariant kOcVariants[] = {
+    OCV(1, 2), OCV(1, 4), OCV(1, 8), OCV(1, 12), OCV(1, 16), OCV(1, 24), OCV(1, 32),
+    OCV(2, 2), OCV(2, 4), OCV(2, 8), OCV(2, 12), OCV(2, 16), OCV(2, 24), OCV(2, 32),
+    OCV(3, 2), OCV(3, 4), OCV(3, 8), OCV(3, 12), OCV(3, 16), OCV(3, 24),
+    OCV(4, 2), OCV(4, 4), OCV(4, 8), OCV(4, 12), OCV(4, 16),
+    OCV(8, 2), OCV(8, 4), OCV(8, 8)};
+#undef OCV
+
+// Picks the on-chip variant for this handle (h->oc_fn stays null when the
+// masked rows cannot stay on chip; the global-memory kernel k_bcd_seq is used).
+static void choose_onchip(somf_ctx* h) {
+  const int k = h->cfg.k, kp = h->kp;
+  int kc = (kp + 31) / 32;
+  if (kc > 4) kc = 8;
+  const int need = (int)ceil_div(h->q_cap, h->nsm);
+  const int cs = k <= 160;
+  for (const OcVariant& v : kOcVariants) {
+    if (v.kc != kc || v.rpw * kOcWarps < need) continue;
+    const int cap = need;
+    size_t smem = (size_t)cap * kp * sizeof(float) + (cs ? (size_t)((k * k + 3) & ~3) * sizeof(float) : 0) +
+                  (size_t)((cap + 1) & ~1) * sizeof(float) + (size_t)k * (2 * sizeof(double) + sizeof(int));
+    if (smem > 220 * 1024) return;
+    if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, kOcThreads, smem) != cudaSuccess || occ < 1) {
+      cudaGetLastError();
+      return;
+    }
+    h->oc_fn = v.fn;
+    h->oc_cap_rows = cap;
+    h->oc_cs = cs;
+    h->oc_smem = smem;
+    h->oc_rpw = v.rpw;
+    h->oc_kc = v.kc;
+    return;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
 SOMF_EXPORT void somf_config_default(somf_config* c) {
@@ -345,6 +407,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       !(c.cd_tol > 0.0) || c.cd_max_sweeps < 1 || c.row_hi - c.row_lo > (int64_t)INT32_MAX;
   if (bad) return SOMF_E_ARG;
   if (c.b_mode == SOMF_B_UNBIASED) return SOMF_E_UNSUPPORTED;
+  if (c.bcd_kernel < 0 || c.bcd_kernel > 2) return SOMF_E_ARG;
   if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL) return SOMF_E_ARG;
   somf_ctx* h = new somf_ctx();
   h->cfg = c;
@@ -391,8 +454,28 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   h->bcd_grid = occ * h->nsm;
   h->rows_cap = (int)ceil_div(rows, h->bcd_grid) + 1;
   A(dalloc(&h->red, (size_t)2 * h->bcd_grid * kRedStride));
+  {
+    // |S_t| ~ Binomial(rows, 1/r): capacity mean + 10 sigma (+32)
+    const double mean = (double)rows / c.r, sd = std::sqrt(mean * (1.0 - 1.0 / c.r));
+    h->q_cap = c.r == 1.0 ? rows : std::min<int64_t>(rows, (int64_t)std::ceil(mean + 10.0 * sd) + 32);
+  }
+  A(dalloc(&h->theta_ws, (size_t)k));
+  A(dalloc(&h->oc_acc, (size_t)kRing * kNC * 3));
+  A(dalloc(&h->oc_accmin, (size_t)kRing * kNC));
+  A(dalloc(&h->oc_rho, (size_t)2 * k));
+  A(dalloc(&h->oc_bar, 4));
+  if (c.bcd_kernel != 1) choose_onchip(h);
+  if (c.bcd_kernel == 2 && !h->oc_fn) {
+    set_err(h, "on-chip BCD requested but %lld masked rows x k = %d do not fit on chip", (long long)h->q_cap, k);
+    return fail(SOMF_E_UNSUPPORTED);
+  }
 #undef A
   if (cudaMemset(h->bar, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(h->oc_bar, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(h->oc_acc, 0, (size_t)kRing * kNC * 3 * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->oc_accmin, 0xff, (size_t)kRing * kNC * sizeof(unsigned)) != cudaSuccess ||
+      cudaMemset(h->oc_rho, 0, (size_t)2 * k * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->theta_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->C64, 0, (size_t)k * k * sizeof(double)) != cudaSuccess ||
@@ -414,7 +497,8 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
   void* ptrs[] = {h->D, h->Bbar, h->C64, h->C32, h->nslack, h->t_dev, h->w_dev, h->q_dev,
                   h->nred_dev, h->err_dev, h->sweeps_dev, h->idx, h->tile_counts, h->perm,
                   h->partial, h->G64, h->beta64, h->A64, h->A32, h->red, h->bar, h->Ge,
-                  h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage};
+                  h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
+                  h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -439,6 +523,7 @@ SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int6
   CK(cudaMemsetAsync(h->C64, 0, (size_t)k * k * sizeof(double), h->st));
   CK(cudaMemsetAsync(h->C32, 0, (size_t)k * k * sizeof(float), h->st));
   CK(cudaMemsetAsync(h->t_dev, 0, sizeof(int64_t), h->st));
+  CK(cudaMemsetAsync(h->theta_ws, 0, (size_t)k * sizeof(double), h->st));
   h->t_host = 0;
   h->mask_ready = false;
   h->initialized = true;
@@ -545,6 +630,33 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
+    if (h->oc_fn) {
+      OcArgs oa{};
+      oa.idx = h->idx;
+      oa.q_dev = h->q_dev;
+      oa.D = h->D;
+      oa.Bbar = h->Bbar;
+      oa.C64 = h->C64;
+      oa.C32 = h->C32;
+      oa.nslack = h->nslack;
+      oa.theta_ws = h->theta_ws;
+      oa.perm = h->perm;
+      oa.k = k;
+      oa.kp = h->kp;
+      oa.a = 1.0 - c.mu;
+      oa.b = c.mu;
+      oa.pos = c.pos_dict;
+      oa.cs_smem = h->oc_cs;
+      oa.cap_rows = h->oc_cap_rows;
+      oa.acc = h->oc_acc;
+      oa.accmin = h->oc_accmin;
+      oa.rho_acc = h->oc_rho;
+      oa.bar = h->oc_bar;
+      oa.nred_out = h->nred_dev;
+      oa.err = h->err_dev;
+      void* kargs[] = {&oa};
+      CK(cudaLaunchCooperativeKernel(h->oc_fn, dim3(h->nsm), dim3(kOcThreads), kargs, h->oc_smem, h->st));
+    } else {
     BcdArgs args{};
     args.idx = h->idx;
     args.q_dev = h->q_dev;
@@ -566,6 +678,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     void* kargs[] = {&args};
     CK(cudaLaunchCooperativeKernel((const void*)k_bcd_seq, dim3(h->bcd_grid), dim3(kBcdThreads), kargs,
                                    smem, h->st));
+    }
     h->launches[SOMF_PH_BCD] += 1;
   }
   h->steps_prof += 1;
@@ -718,6 +831,7 @@ SOMF_EXPORT somf_status somf_set_state(somf_handle h, const float* D, const floa
   CKL();
   k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->t_dev, t);
   CKL();
+  CK(cudaMemsetAsync(h->theta_ws, 0, (size_t)k * sizeof(double), h->st));
   CK(cudaStreamSynchronize(h->st));
   h->t_host = t;
   h->mask_ready = false;
@@ -733,6 +847,8 @@ SOMF_EXPORT somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* 
   CK(cudaStreamSynchronize(h->st));
   return check_flags(h);
 }
+
+SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->oc_fn ? 2 : 1) : 0; }
 
 SOMF_EXPORT somf_status somf_profile_enable(somf_handle h, int32_t on) {
   if (!h) return SOMF_E_ARG;

@@ -61,7 +61,7 @@ class Somf:
                  r: float = 1.0, u: float = 0.917, b_mode: str = "masked",
                  perm_cyclic: bool = False, cd_tol: float = 1e-9, cd_max_sweeps: int = 4000,
                  seed: int = 0, row_lo: int = 0, row_hi: int = 0, device: int = 0,
-                 stream=None, debug: bool = False):
+                 stream=None, debug: bool = False, bcd_kernel: str = "auto"):
         L = lib()
         cfg = _lib.SomfConfig()
         L.somf_config_default(C.byref(cfg))
@@ -80,6 +80,7 @@ class Somf:
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         cfg.stream = _stream_ptr(self.stream)
         cfg.debug = int(debug)
+        cfg.bcd_kernel = {"auto": 0, "global": 1, "onchip": 2}[bcd_kernel]
         h = C.c_void_p()
         st = L.somf_create(C.byref(cfg), C.byref(h))
         if st != 0:
@@ -189,6 +190,10 @@ class Somf:
                                        C.byref(steps)), self._h)
         return dict(ms=dict(zip(self.PHASES, ms.tolist())), launches=dict(zip(self.PHASES, nl.tolist())),
                     steps=steps.value)
+
+    @property
+    def bcd_variant(self) -> str:
+        return {1: "global", 2: "onchip"}.get(lib().somf_bcd_variant(self._h), "?")
 
     def last_step_info(self):
         q, nred, w = C.c_int64(), C.c_int64(), C.c_double()

@@ -119,7 +119,7 @@ def _data(kind, p, n, seed=0):
     return f32(X)
 
 
-def _pair(somf, name, t0=5, seed=3):
+def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
     p, k, eta, kw, kind = CASES[name]
     X = _data(kind, p, k + (t0 + 3) * eta)
     ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=seed, **kw))
@@ -128,14 +128,16 @@ def _pair(somf, name, t0=5, seed=3):
         ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
     # the oracle continues from the float32-rounded state the GPU holds
     ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
-    gpu = somf.Somf(p, k, eta, seed=seed, debug=True, **kw)
+    gpu = somf.Somf(p, k, eta, seed=seed, debug=True, bcd_kernel=bcd_kernel, **kw)
     gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
     return ora, gpu, X, (p, k, eta)
 
 
+@pytest.mark.parametrize("bcd_kernel", ["global", "onchip"])
 @pytest.mark.parametrize("name", list(CASES))
-def test_one_step_parity(somf, name):
-    ora, gpu, X, (p, k, eta) = _pair(somf, name)
+def test_one_step_parity(somf, name, bcd_kernel):
+    ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel=bcd_kernel)
+    assert gpu.bcd_variant == bcd_kernel
     batch = X[:, k + 5 * eta:k + 6 * eta]
     out = ora.partial_fit(batch)
     gpu.partial_fit(cuda(batch))
@@ -169,9 +171,13 @@ def test_masked_api_and_pinned_input_match(somf, name):
     gpu3.partial_fit(pinned)
     torch.cuda.synchronize()
     s1, s2, s3 = gpu.get_state(), gpu2.get_state(), gpu3.get_state()
+    # the three input routes feed identical bits to the same kernels; the
+    # on-chip BCD sums its grid partials with fp64 atomics (order not fixed),
+    # so runs agree to rounding, not bit for bit
     for key in ("D", "Bbar", "Cbar", "n"):
-        np.testing.assert_array_equal(s1[key], s2[key])
-        np.testing.assert_array_equal(s3[key], s2[key])
+        scale = max(np.abs(s2[key]).max(), 1.0)
+        np.testing.assert_allclose(s1[key], s2[key], rtol=0, atol=1e-6 * scale)
+        np.testing.assert_allclose(s3[key], s2[key], rtol=0, atol=1e-6 * scale)
 
 
 def test_empty_mask_step(somf):
@@ -212,7 +218,7 @@ def test_set_components_projects_and_slacks(somf):
 # trajectory: objective after 100 iterations
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("name,iters", [("cfgA_ridge_l1", 100), ("ridge_l1_fmri_small", 100),
-                                        ("nmf_small", 100)])
+                                        ("nmf_small", 100), ("enet_enet", 60)])
 def test_trajectory_objective(somf, name, iters):
     p, k, eta, kw, kind = CASES[name]
     X = _data(kind, p, k + iters * eta + 200, seed=1)
