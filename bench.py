@@ -52,26 +52,46 @@ def fmri_inputs_cpu(n_cols: int, seed: int = 0, k: int = WORKLOAD["k"]):
     return np.ascontiguousarray(S[:, k:]), np.ascontiguousarray(S[:, :k])
 
 
+class FmriStreamGPU:
+    """cfgC stand-in generated on the GPU (torch, harness only): batch b is
+    D* a_b + noise, a_b the columns [k + b eta, k + (b+1) eta) of the AR(1)
+    codes; D0 = the first k stream columns (reading R15)."""
+
+    def __init__(self, n_batches: int, eta: int, k: int, seed: int, device):
+        import torch
+        import synth
+        coords = synth.fmri_voxel_grid()
+        self.p = coords.shape[0]
+        self.eta, self.k, self.device = eta, k, device
+        self.Dstar = torch.tensor(synth.fmri_dictionary(coords, 70, seed=seed), dtype=torch.float32,
+                                  device=device)
+        n = n_batches * eta + k
+        self.A = torch.tensor(synth.fmri_codes(70, 1, T=max(1200, n), seed=seed + 1)[:, :n],
+                              dtype=torch.float32, device=device)
+        self.g = torch.Generator(device=device)
+        self.g.manual_seed(seed + 2)
+        self.sigma = float(np.sqrt(70 / self.p / 0.5))
+        self.n_batches = n_batches
+
+    def _cols(self, c0, c1):
+        import torch
+        X = self.Dstar @ self.A[:, c0:c1]
+        X += self.sigma * torch.randn(X.shape, generator=self.g, device=self.device)
+        return X.contiguous()
+
+    def d0(self):
+        return self._cols(0, self.k)
+
+    def batch(self, b):
+        b %= self.n_batches
+        return self._cols(self.k + b * self.eta, self.k + (b + 1) * self.eta)
+
+
 def fmri_inputs_gpu(n_batches: int, eta: int, k: int, seed: int, device):
-    """Same recipe generated on the GPU (torch, harness only): returns
-    (list of p x eta float32 CUDA batches, D0 p x k)."""
-    import torch
-    import synth
-    coords = synth.fmri_voxel_grid()
-    p = coords.shape[0]
-    Dstar = torch.tensor(synth.fmri_dictionary(coords, 70, seed=seed), dtype=torch.float32, device=device)
-    n = n_batches * eta + k
-    A = torch.tensor(synth.fmri_codes(70, 1, T=max(1200, n), seed=seed + 1)[:, :n],
-                     dtype=torch.float32, device=device)
-    g = torch.Generator(device=device)
-    g.manual_seed(seed + 2)
-    sigma = float(np.sqrt(70 / p / 0.5))
-    D0 = (Dstar @ A[:, :k] + sigma * torch.randn(p, k, generator=g, device=device)).contiguous()
-    batches = []
-    for b in range(n_batches):
-        cols = A[:, k + b * eta:k + (b + 1) * eta]
-        batches.append((Dstar @ cols + sigma * torch.randn(p, eta, generator=g, device=device)).contiguous())
-    return batches, D0
+    """(list of p x eta float32 CUDA batches, D0 p x k) of FmriStreamGPU."""
+    s = FmriStreamGPU(n_batches, eta, k, seed, device)
+    D0 = s.d0()
+    return [s.batch(b) for b in range(n_batches)], D0
 
 
 # ----------------------------------------------------------------------------
@@ -269,16 +289,23 @@ def run_somf(args):
     p, k, eta, r = w["p"], w["k"], w["eta"], args.r
     stream = torch.cuda.current_stream(dev)
     nb = min(args.warmup + args.steps, 24)
-    batches, D0 = fmri_inputs_gpu(nb, eta, k, seed=rank, device=dev)
+    stream_gen = FmriStreamGPU(args.burn_in + nb, eta, k, seed=rank, device=dev)
+    D0 = stream_gen.d0()
+    # the timed pool: the batches that follow the burn-in in the stream
+    batches = [stream_gen.batch(args.burn_in + b) for b in range(nb)]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
-    def make(rr):
+    def make(rr, burn_in):
         m = somf_pkg.Somf(p, k, eta, lam=w["lam"], nu=w["nu"], mu=w["mu"], pos_code=w["pos_code"],
                           pos_dict=w["pos_dict"], r=rr, u=w["u"], seed=rank, device=local, stream=stream)
         m.set_components(D0)
+        # burn-in: the learner reaches its steady state (t > burn_in) on fresh
+        # stream batches before anything is timed (steady state)
+        for b in range(burn_in):
+            m.partial_fit(stream_gen.batch(b))
         return m
 
-    model = make(r)
+    model = make(r, args.burn_in)
     for i in range(args.warmup):
         model.partial_fit(batches[i % nb])
     torch.cuda.synchronize()
@@ -296,6 +323,7 @@ def run_somf(args):
     if world > 1:
         dist.barrier()
     prof = model.profile_read()
+    bcd_cyc = model.bcd_phase_cycles()
     model.profile_enable(False)
     info = model.last_step_info()
     step_ms = sum(ms) / len(ms)
@@ -330,6 +358,14 @@ def run_somf(args):
                 "peak_source": "guide: 148 SM x 64 FP64 lanes x 2 x sm_max_mhz"}
     roof["phase_ms_per_step"] = phase_ms
     roof["bcd_grid_reductions_per_step"] = info["bcd_reductions"]
+    if bcd_cyc["launches"]:
+        mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
+        roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
+                                         if ph not in ("launches", "unconverged_per_round")}
+        unc = [u / bcd_cyc["launches"] for u in bcd_cyc["unconverged_per_round"]]
+        while unc and unc[-1] == 0:
+            unc.pop()
+        roof["bcd_unconverged_atoms_per_round"] = [round(u, 2) for u in unc]
     sb = step_bytes(q, k, eta)
     step_roof = {"bytes_per_step": sb, "achieved_gbs": sb / (step_ms * 1e-3) / 1e9,
                  "frac_of_hbm": sb / (step_ms * 1e-3) / 1e9 / peaks["hbm"]}
@@ -340,7 +376,7 @@ def run_somf(args):
         n_e2e = min(args.steps, 10)
         host = [b.cpu().pin_memory() for b in batches[:2]]
         codes = torch.empty((k, eta), dtype=torch.float32).pin_memory()
-        m2 = make(r)
+        m2 = make(r, args.burn_in)
         for i in range(2):
             m2.partial_fit(host[i % 2])
         torch.cuda.synchronize()
@@ -366,7 +402,7 @@ def run_somf(args):
     sweep = {}
     if not args.no_sweep:
         for rr in (1.0, 4.0, 12.0, 24.0):
-            m3 = make(rr)
+            m3 = make(rr, args.burn_in if rr > 1.0 else min(args.burn_in, 10))
             for i in range(3):
                 m3.partial_fit(batches[i % nb])
             torch.cuda.synchronize()
@@ -394,6 +430,7 @@ def run_somf(args):
                        "code": "ridge", "dict": "l1-ball", "b_mode": "masked",
                        "bcd_kernel": model.bcd_variant,
                        "l2": "flushed (256 MiB write) before every timed step",
+                       "burn_in_iterations": args.burn_in,
                        "parallelism": "single" if world == 1 else f"replicas x{world}"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / steps_prof,
@@ -410,6 +447,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="somf", choices=["somf", "reference"])
+    ap.add_argument("--burn-in", type=int, default=60,
+                    help="untimed SOMF iterations before warm-up (steady state, t > burn-in)")
     ap.add_argument("--r", type=float, default=WORKLOAD["r"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")

@@ -90,9 +90,11 @@ typedef struct somf_config {
   int32_t device;         /* CUDA device ordinal                                 */
   void* stream;           /* cudaStream_t (NULL = legacy default stream)         */
   int32_t debug;          /* 1: synchronise and check after every call          */
-  int32_t bcd_kernel;     /* Alg. 4 kernel: 0 = auto (on-chip when the masked
-                             rows fit in registers + shared memory, else global),
-                             1 = global-memory kernel, 2 = on-chip kernel
+  int32_t bcd_kernel;     /* Alg. 4 kernel: 0 = auto (simultaneous-threshold
+                             when k <= 96 and the masked rows fit on chip, else
+                             on-chip per-atom, else global), 1 = global-memory
+                             per-atom kernel, 2 = on-chip per-atom kernel,
+                             3 = simultaneous-threshold kernel
                              (SOMF_E_UNSUPPORTED at create if it cannot fit)   */
 } somf_config;
 
@@ -182,9 +184,19 @@ somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* bcd_reductio
                                 double* w);
 
 /* Alg. 4 kernel this handle launches: 1 = global-memory (per-atom grid
- * reductions, rows re-read from L2/HBM), 2 = on-chip (masked rows resident in
- * registers + shared memory).  0 on a null handle. */
+ * reductions, rows re-read from L2/HBM), 2 = on-chip per-atom (masked rows
+ * resident in registers + shared memory), 3 = on-chip simultaneous-threshold
+ * rounds (all k thresholds per grid reduction).  0 on a null handle. */
 int32_t somf_bcd_variant(somf_handle h);
+
+/* SM-cycle breakdown of the simultaneous-threshold BCD kernel (CTA 0), summed
+ * over the launches made while somf_profile_enable(h, 1) was on, then reset:
+ * [0] setup + residual, [1] recurrence, [2] statistics + partial reductions,
+ * [3] grid barrier, [4] threshold update, [5] finish, [6] write-back,
+ * [7] launches, [8 + r] atoms not yet converged after round r (r < 64).
+ * cycles must hold 72 entries.  Synchronises.  Zeros for the other BCD
+ * kernels. */
+somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles);
 
 /* ---- per-phase timing of somf_partial_fit (CUDA events on config.stream) ---- */
 enum {

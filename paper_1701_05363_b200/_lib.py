@@ -79,6 +79,7 @@ SIGNATURES = [
     ("somf_set_state", I32, [P, P, P, P, P, I64]),
     ("somf_last_step_info", I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(D)]),
     ("somf_bcd_variant", I32, [P]),
+    ("somf_bcd_phase_cycles", I32, [P, P]),
     ("somf_profile_enable", I32, [P, I32]),
     ("somf_profile_read", I32, [P, P, P, C.POINTER(I64)]),
     ("somf_mask_rows", I32, [U64, I64, I64, I64, D, P, C.POINTER(I64), P]),

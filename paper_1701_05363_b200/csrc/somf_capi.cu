@@ -28,6 +28,7 @@
 #include "solve.cuh"
 #include "bcd.cuh"
 #include "bcd_onchip.cuh"
+#include "bcd_newton.cuh"
 
 using namespace somf;
 
@@ -123,6 +124,13 @@ struct somf_ctx {
   int oc_cap_rows = 0, oc_cs = 0, oc_rpw = 0, oc_kc = 0;
   size_t oc_smem = 0;
   double* theta_ws = nullptr;
+  const void* nt_fn = nullptr;   // simultaneous-threshold BCD (bcd_newton.cuh)
+  int nt_cap_rows = 0, nt_kpt = 0;
+  size_t nt_smem = 0;
+  double* lam_ws = nullptr;
+  double* nt_acc = nullptr;
+  long long* bcd_prof = nullptr;   // SM cycles per BCD phase (somf_bcd_phase_cycles)
+  unsigned* nt_accmm = nullptr;
   double* oc_acc = nullptr;
   unsigned* oc_accmin = nullptr;
   double* oc_rho = nullptr;
@@ -185,7 +193,7 @@ static somf_status check_flags(somf_ctx* h) {
   if (h->oc_bar) CK(cudaMemcpy(&b2, h->oc_bar + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
   if (b || b2) { set_err(h, "grid barrier watchdog fired in the BCD kernel (results invalid)"); return SOMF_E_CUDA; }
   if (e == 2) { set_err(h, "more masked rows than the on-chip BCD capacity (q > mean + 10 sigma)"); return SOMF_E_CUDA; }
-  if (e == 3) { set_err(h, "projection threshold search hit its round cap"); return SOMF_E_CUDA; }
+  if (e == 3 || e == 4) { set_err(h, "projection threshold search hit its round cap"); return SOMF_E_CUDA; }
   if (e) { set_err(h, "device numerical error flag %d (non-SPD system in the code solve)", e); return SOMF_E_NONFINITE; }
   return SOMF_OK;
 }
@@ -326,6 +334,41 @@ static const OcVariant kOcVariants[] = {
     OCV(8, 2), OCV(8, 4), OCV(8, 8)};
 #undef OCV
 
+struct NtVariant { int kpt; const void* fn; };
+#define NTV(K) {K, (const void*)k_bcd_newton<K>}
+static const NtVariant kNtVariants[] = {NTV(16), NTV(32), NTV(48), NTV(64), NTV(72), NTV(80), NTV(96)};
+#undef NTV
+
+static void choose_newton(somf_ctx* h) {
+  const int k = h->cfg.k;
+  const int cap = (int)ceil_div(h->q_cap, h->nsm);
+  if (cap > kNtThreads) return;
+  for (const NtVariant& v : kNtVariants) {
+    if (v.kpt < k) continue;
+    const int LD = v.kpt + 1;
+    const int H = std::max(1, kNtThreads / k);
+    const size_t smem = (size_t)4 * (((size_t)cap * LD + 3) & ~(size_t)3) * sizeof(float) +
+                        (size_t)k * v.kpt * sizeof(float) +
+                        (size_t)H * v.kpt * (3 * sizeof(double) + 2 * sizeof(unsigned)) +
+                        (size_t)cap * sizeof(int) + 16;
+    if (smem > 200 * 1024) return;
+    if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, kNtThreads, smem) != cudaSuccess || occ < 1) {
+      cudaGetLastError();
+      return;
+    }
+    h->nt_fn = v.fn;
+    h->nt_cap_rows = cap;
+    h->nt_kpt = v.kpt;
+    h->nt_smem = smem;
+    return;
+  }
+}
+
 // Picks the on-chip variant for this handle (h->oc_fn stays null when the
 // masked rows cannot stay on chip; the global-memory kernel k_bcd_seq is used).
 static void choose_onchip(somf_ctx* h) {
@@ -357,6 +400,15 @@ static void choose_onchip(somf_ctx* h) {
     h->oc_kc = v.kc;
     return;
   }
+}
+
+__global__ void k_init_accmm(unsigned* mm, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) { mm[2 * i] = 0xffffffffu; mm[2 * i + 1] = 0u; }
+}
+static cudaError_t init_accmm(unsigned* mm, int n) {
+  k_init_accmm<<<(n + 255) / 256, 256>>>(mm, n);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -407,7 +459,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       !(c.cd_tol > 0.0) || c.cd_max_sweeps < 1 || c.row_hi - c.row_lo > (int64_t)INT32_MAX;
   if (bad) return SOMF_E_ARG;
   if (c.b_mode == SOMF_B_UNBIASED) return SOMF_E_UNSUPPORTED;
-  if (c.bcd_kernel < 0 || c.bcd_kernel > 2) return SOMF_E_ARG;
+  if (c.bcd_kernel < 0 || c.bcd_kernel > 3) return SOMF_E_ARG;
   if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL) return SOMF_E_ARG;
   somf_ctx* h = new somf_ctx();
   h->cfg = c;
@@ -464,9 +516,14 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->oc_accmin, (size_t)kRing * kNC));
   A(dalloc(&h->oc_rho, (size_t)2 * k));
   A(dalloc(&h->oc_bar, 4));
-  if (c.bcd_kernel != 1) choose_onchip(h);
-  if (c.bcd_kernel == 2 && !h->oc_fn) {
-    set_err(h, "on-chip BCD requested but %lld masked rows x k = %d do not fit on chip", (long long)h->q_cap, k);
+  A(dalloc(&h->lam_ws, (size_t)k));
+  A(dalloc(&h->bcd_prof, 72));
+  A(dalloc(&h->nt_acc, (size_t)kNtRing * k * 3));
+  A(dalloc(&h->nt_accmm, (size_t)kNtRing * k * 2));
+  if (c.bcd_kernel == 0 || c.bcd_kernel == 3) choose_newton(h);
+  if (c.bcd_kernel == 0 ? !h->nt_fn : c.bcd_kernel == 2) choose_onchip(h);
+  if ((c.bcd_kernel == 2 && !h->oc_fn) || (c.bcd_kernel == 3 && !h->nt_fn)) {
+    set_err(h, "requested BCD kernel does not fit: %lld masked rows x k = %d", (long long)h->q_cap, k);
     return fail(SOMF_E_UNSUPPORTED);
   }
 #undef A
@@ -476,6 +533,10 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       cudaMemset(h->oc_accmin, 0xff, (size_t)kRing * kNC * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(h->oc_rho, 0, (size_t)2 * k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->theta_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->lam_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->bcd_prof, 0, 72 * sizeof(long long)) != cudaSuccess ||
+      cudaMemset(h->nt_acc, 0, (size_t)kNtRing * k * 3 * sizeof(double)) != cudaSuccess ||
+      init_accmm(h->nt_accmm, kNtRing * k) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->C64, 0, (size_t)k * k * sizeof(double)) != cudaSuccess ||
@@ -498,7 +559,8 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->nred_dev, h->err_dev, h->sweeps_dev, h->idx, h->tile_counts, h->perm,
                   h->partial, h->G64, h->beta64, h->A64, h->A32, h->red, h->bar, h->Ge,
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
-                  h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar};
+                  h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
+                  h->lam_ws, h->nt_acc, h->nt_accmm, h->bcd_prof};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -524,6 +586,7 @@ SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int6
   CK(cudaMemsetAsync(h->C32, 0, (size_t)k * k * sizeof(float), h->st));
   CK(cudaMemsetAsync(h->t_dev, 0, sizeof(int64_t), h->st));
   CK(cudaMemsetAsync(h->theta_ws, 0, (size_t)k * sizeof(double), h->st));
+  CK(cudaMemsetAsync(h->lam_ws, 0, (size_t)k * sizeof(double), h->st));
   h->t_host = 0;
   h->mask_ready = false;
   h->initialized = true;
@@ -630,7 +693,34 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
-    if (h->oc_fn) {
+    if (h->nt_fn) {
+      NtArgs na{};
+      na.idx = h->idx;
+      na.q_dev = h->q_dev;
+      na.D = h->D;
+      na.Bbar = h->Bbar;
+      na.C64 = h->C64;
+      na.C32 = h->C32;
+      na.nslack = h->nslack;
+      na.lam_ws = h->lam_ws;
+      na.perm = h->perm;
+      na.k = k;
+      na.kp = h->kp;
+      na.a = 1.0 - c.mu;
+      na.b = c.mu;
+      na.pos = c.pos_dict;
+      na.cap_rows = h->nt_cap_rows;
+      na.max_rounds = 3 * k + 20;
+      na.acc = h->nt_acc;
+      na.accmm = h->nt_accmm;
+      na.rho_acc = h->oc_rho;
+      na.bar = h->oc_bar;
+      na.nred_out = h->nred_dev;
+      na.err = h->err_dev;
+      na.prof = h->prof_on ? h->bcd_prof : nullptr;
+      void* kargs[] = {&na};
+      CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(kNtThreads), kargs, h->nt_smem, h->st));
+    } else if (h->oc_fn) {
       OcArgs oa{};
       oa.idx = h->idx;
       oa.q_dev = h->q_dev;
@@ -832,6 +922,7 @@ SOMF_EXPORT somf_status somf_set_state(somf_handle h, const float* D, const floa
   k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->t_dev, t);
   CKL();
   CK(cudaMemsetAsync(h->theta_ws, 0, (size_t)k * sizeof(double), h->st));
+  CK(cudaMemsetAsync(h->lam_ws, 0, (size_t)k * sizeof(double), h->st));
   CK(cudaStreamSynchronize(h->st));
   h->t_host = t;
   h->mask_ready = false;
@@ -848,7 +939,17 @@ SOMF_EXPORT somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* 
   return check_flags(h);
 }
 
-SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->oc_fn ? 2 : 1) : 0; }
+SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {
+  if (!h || !cycles) return SOMF_E_ARG;
+  CK(cudaStreamSynchronize(h->st));
+  long long v[72];
+  CK(cudaMemcpy(v, h->bcd_prof, sizeof(v), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(h->bcd_prof, 0, sizeof(v)));
+  for (int i = 0; i < 72; ++i) cycles[i] = v[i];
+  return SOMF_OK;
+}
+
+SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->nt_fn ? 3 : h->oc_fn ? 2 : 1) : 0; }
 
 SOMF_EXPORT somf_status somf_profile_enable(somf_handle h, int32_t on) {
   if (!h) return SOMF_E_ARG;

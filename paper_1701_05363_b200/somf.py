@@ -80,7 +80,7 @@ class Somf:
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         cfg.stream = _stream_ptr(self.stream)
         cfg.debug = int(debug)
-        cfg.bcd_kernel = {"auto": 0, "global": 1, "onchip": 2}[bcd_kernel]
+        cfg.bcd_kernel = {"auto": 0, "global": 1, "onchip": 2, "newton": 3}[bcd_kernel]
         h = C.c_void_p()
         st = L.somf_create(C.byref(cfg), C.byref(h))
         if st != 0:
@@ -191,9 +191,18 @@ class Somf:
         return dict(ms=dict(zip(self.PHASES, ms.tolist())), launches=dict(zip(self.PHASES, nl.tolist())),
                     steps=steps.value)
 
+    BCD_PHASES = ("setup", "recurrence", "stats", "barrier", "update", "finish", "writeback")
+
+    def bcd_phase_cycles(self):
+        v = np.zeros(72, np.int64)
+        _check(lib().somf_bcd_phase_cycles(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
+        out = dict(zip(self.BCD_PHASES, v[:7].tolist()), launches=int(v[7]))
+        out["unconverged_per_round"] = v[8:].tolist()
+        return out
+
     @property
     def bcd_variant(self) -> str:
-        return {1: "global", 2: "onchip"}.get(lib().somf_bcd_variant(self._h), "?")
+        return {1: "global", 2: "onchip", 3: "newton"}.get(lib().somf_bcd_variant(self._h), "?")
 
     def last_step_info(self):
         q, nred, w = C.c_int64(), C.c_int64(), C.c_double()

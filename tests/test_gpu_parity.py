@@ -133,9 +133,11 @@ def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
     return ora, gpu, X, (p, k, eta)
 
 
-@pytest.mark.parametrize("bcd_kernel", ["global", "onchip"])
+@pytest.mark.parametrize("bcd_kernel", ["global", "onchip", "newton"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_one_step_parity(somf, name, bcd_kernel):
+    if bcd_kernel == "newton" and CASES[name][1] > 96:
+        pytest.skip("simultaneous-threshold kernel covers k <= 96")
     ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel=bcd_kernel)
     assert gpu.bcd_variant == bcd_kernel
     batch = X[:, k + 5 * eta:k + 6 * eta]
@@ -219,13 +221,14 @@ def test_set_components_projects_and_slacks(somf):
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("name,iters", [("cfgA_ridge_l1", 100), ("ridge_l1_fmri_small", 100),
                                         ("nmf_small", 100), ("enet_enet", 60)])
-def test_trajectory_objective(somf, name, iters):
+@pytest.mark.parametrize("bcd_kernel", ["onchip", "newton"])
+def test_trajectory_objective(somf, name, iters, bcd_kernel):
     p, k, eta, kw, kind = CASES[name]
     X = _data(kind, p, k + iters * eta + 200, seed=1)
     Xte = X[:, -200:]
     ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=9, **kw))
     ora.set_components(X[:, :k])
-    gpu = somf.Somf(p, k, eta, seed=9, **kw)
+    gpu = somf.Somf(p, k, eta, seed=9, bcd_kernel=bcd_kernel, **kw)
     gpu.set_components(cuda(X[:, :k]))
     Xg = cuda(X)
     for t in range(iters):
