@@ -361,7 +361,8 @@ def run_somf(args):
     if bcd_cyc["launches"]:
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
         roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
-                                         if ph not in ("launches", "unconverged_per_round")}
+                                         if ph not in ("launches", "unconverged_per_round", "ridge")}
+        roof["ridge_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["ridge"].items()}
         unc = [u / bcd_cyc["launches"] for u in bcd_cyc["unconverged_per_round"]]
         while unc and unc[-1] == 0:
             unc.pop()

@@ -193,9 +193,10 @@ int32_t somf_bcd_variant(somf_handle h);
  * over the launches made while somf_profile_enable(h, 1) was on, then reset:
  * [0] setup + residual, [1] recurrence, [2] statistics + partial reductions,
  * [3] grid barrier, [4] threshold update, [5] finish, [6] write-back,
- * [7] launches, [8 + r] atoms not yet converged after round r (r < 64).
- * cycles must hold 72 entries.  Synchronises.  Zeros for the other BCD
- * kernels. */
+ * [7] launches, [8 + r] atoms not yet converged after round r (r < 64);
+ * [72..75] ridge code kernel (CTA 0): load, factorisation, substitutions,
+ * Cbar partial.  cycles must hold 80 entries.  Synchronises.  Zeros for the
+ * kernels not launched. */
 somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles);
 
 /* ---- per-phase timing of somf_partial_fit (CUDA events on config.stream) ---- */

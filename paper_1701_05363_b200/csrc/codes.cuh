@@ -1,0 +1,275 @@
+// codes.cuh -- (a2) ridge codes and (a3) Cbar, v2:
+//
+//  k_ridge_codes<KPL> : alpha = (G + lambda I)^-1 beta  (Eq. somf_alpha,
+//                  P:592-596, nu = 1, no positivity), k <= 32 KPL.
+//                  Every CTA factorises G + lambda I redundantly in shared
+//                  memory (fp64 LL^T, right-looking in 4-column panels: the
+//                  4 x 4 diagonal block is factorised in every thread's
+//                  registers, the panel rows below are solved one row per
+//                  thread, then one rank-4 trailing update over a 16 x 16
+//                  thread grid: 2 barriers per 4 columns).  Then each warp
+//                  solves one right-hand side with 4-row block substitutions
+//                  (the solution in registers, lane l holding rows l, l+32,
+//                  ...; one shuffle round per 4 rows).  Each CTA also writes
+//                  its partial sum_s alpha_s alpha_s^T for the Cbar update.
+//  k_cbar_finalize : Cbar <- (1 - w) Cbar + (w / eta) sum_b partial_b
+//                  (Eq. somf_partial, batch mean R4), partials added in
+//                  block order (deterministic).
+#pragma once
+#include "common.cuh"
+
+namespace somf {
+
+constexpr int kRcThreads = 256;
+constexpr int kRcMaxK = 160;
+
+// 1/sqrt(d) in fp64: fp32 MUFU estimate + two Newton steps (rel. error ~1e-16),
+// ~3x shorter latency than sqrt() followed by a division
+__device__ __forceinline__ double rc_rsqrt(double d) {
+  double y = (double)rsqrtf((float)d);
+  y = y * fma(-0.5 * d, y * y, 1.5);
+  y = y * fma(-0.5 * d, y * y, 1.5);
+  return y;
+}
+
+template <int KPL>
+__device__ __forceinline__ double rc_pick(const double (&y)[KPL], int c) {
+  double v = 0.0;
+#pragma unroll
+  for (int i = 0; i < KPL; ++i)
+    if (i == c) v = y[i];
+  return v;
+}
+
+// smem: k x (k+1) doubles (L, 1/L_jj on the diagonal) + 8 warps x k doubles
+template <int KPL>
+__global__ void __launch_bounds__(kRcThreads)
+k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int k, int m, double lam,
+              double* __restrict__ A64, float* __restrict__ A32, float* __restrict__ AT32, int ldt,
+              double* __restrict__ cpart, int* __restrict__ err, long long* __restrict__ prof) {
+  extern __shared__ double rc_smem[];
+  long long t_mark = clock64();
+#define RC_MARK(slot)                                                     \
+  do {                                                                    \
+    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {                    \
+      const long long now_ = clock64();                                   \
+      prof[slot] += now_ - t_mark;                                        \
+      t_mark = now_;                                                      \
+    }                                                                     \
+  } while (0)
+  const int ld = k + 1;
+  double* M = rc_smem;                              // k x ld, lower triangle
+  double* Y = rc_smem + (size_t)k * ld;             // 8 x k
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int ty = tid >> 4, tx = tid & 15;
+#pragma unroll 4
+  for (int e = tid; e < k * k; e += kRcThreads) {
+    const int i = e / k, j = e % k;
+    const double g = G[e];
+    if (j <= i) M[i * ld + j] = g + (i == j ? lam : 0.0);
+  }
+  __syncthreads();
+  RC_MARK(0);
+  bool bad = false;
+  for (int p0 = 0; p0 < k; p0 += 4) {
+    const int pb = min(4, k - p0);
+    // 4 x 4 diagonal block, factorised in registers by every thread
+    double Ld[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) Ld[a][c] = (a < pb && c <= a) ? M[(p0 + a) * ld + p0 + c] : 0.0;
+    double inv[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c < pb) {
+        double d = Ld[c][c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < c) d -= Ld[c][u] * Ld[c][u];
+        bad |= !(d > 0.0);
+        const double ir = d > 0.0 ? rc_rsqrt(d) : 0.0;
+        inv[c] = ir;
+        Ld[c][c] = d * ir;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          if (a > c && a < pb) {
+            double v = Ld[a][c];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (u < c) v -= Ld[a][u] * Ld[c][u];
+            Ld[a][c] = v * inv[c];
+          }
+        }
+      } else {
+        inv[c] = 0.0;
+      }
+    }
+    // panel rows below: L[i][p0..p0+pb) = M[i][p0..] L_D^-T  (one row per thread)
+    for (int i = p0 + pb + tid; i < k; i += kRcThreads) {
+      double x[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < pb) {
+          double v = M[i * ld + p0 + c];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < c) v -= x[u] * Ld[c][u];
+          x[c] = v * inv[c];
+        } else {
+          x[c] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pb) M[i * ld + p0 + c] = x[c];
+    }
+    __syncthreads();                                // panel reads of the block done
+    // (static register indices only: a dynamic index would put Ld in local memory)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (tid == 4 * a + c && a < pb && c <= a) M[(p0 + a) * ld + p0 + c] = (a == c) ? inv[a] : Ld[a][c];
+    // rank-4 trailing update: M[i][l] -= sum_c L[i][p0+c] L[l][p0+c], p0+pb <= l <= i
+    const int r0 = p0 + pb, n = k - r0;
+    for (int ii = ty; ii < n; ii += 16) {
+      const int i = r0 + ii;
+      double li[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) li[c] = c < pb ? M[i * ld + p0 + c] : 0.0;
+      for (int ll = tx; ll <= ii; ll += 16) {
+        const int l = r0 + ll;
+        double v = M[i * ld + l];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < pb) v -= li[c] * M[l * ld + p0 + c];
+        M[i * ld + l] = v;
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && err) atomicExch(err, 1);
+  RC_MARK(1);
+
+  // ---- substitutions: one warp per right-hand side, 4 rows per shuffle round ----
+  for (int s0 = blockIdx.x * 8; s0 < m; s0 += gridDim.x * 8) {
+    const int s = s0 + wid;
+    double y[KPL];
+#pragma unroll
+    for (int c = 0; c < KPL; ++c) {
+      const int i = lane + 32 * c;
+      y[c] = (s < m && i < k) ? beta[(int64_t)i * m + s] : 0.0;
+    }
+    // L y = b
+    for (int jb = 0; jb < k; jb += 4) {
+      const int pb = min(4, k - jb), cs = jb >> 5, lb = jb & 31;
+      const double own = rc_pick<KPL>(y, cs);
+      double z[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (t < pb) {
+          double v = z[t];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < t) v -= M[(jb + t) * ld + jb + u] * z[u];
+          z[t] = v * M[(jb + t) * ld + jb + t];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        const int i = lane + 32 * c;
+        if (i >= jb && i < jb + pb) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (i == jb + t) y[c] = z[t];
+        } else if (i >= jb + pb && i < k) {
+          double v = y[c];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < pb) v -= M[i * ld + jb + t] * z[t];
+          y[c] = v;
+        }
+      }
+    }
+    // L^T x = y
+    for (int jb = ((k - 1) / 4) * 4; jb >= 0; jb -= 4) {
+      const int pb = min(4, k - jb), cs = jb >> 5, lb = jb & 31;
+      const double own = rc_pick<KPL>(y, cs);
+      double z[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
+#pragma unroll
+      for (int t = 3; t >= 0; --t) {
+        if (t < pb) {
+          double v = z[t];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u > t && u < pb) v -= M[(jb + u) * ld + jb + t] * z[u];
+          z[t] = v * M[(jb + t) * ld + jb + t];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        const int i = lane + 32 * c;
+        if (i >= jb && i < jb + pb) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (i == jb + t) y[c] = z[t];
+        } else if (i < jb) {
+          double v = y[c];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < pb) v -= M[(jb + t) * ld + i] * z[t];
+          y[c] = v;
+        }
+      }
+    }
+    double* Yw = Y + (size_t)wid * k;
+#pragma unroll
+    for (int c = 0; c < KPL; ++c) {
+      const int i = lane + 32 * c;
+      if (i < k) {
+        const double v = s < m ? y[c] : 0.0;
+        Yw[i] = v;
+        if (s < m) {
+          A64[(int64_t)i * m + s] = v;
+          A32[(int64_t)i * m + s] = (float)v;
+          if (AT32) AT32[(int64_t)s * ldt + i] = (float)v;     // codes transposed (eta x kp) for bbar
+        }
+      }
+    }
+  }
+  RC_MARK(2);
+  if (cpart) {
+    __syncthreads();
+    double* out = cpart + (size_t)blockIdx.x * k * k;
+    for (int e = tid; e < k * k; e += kRcThreads) {
+      const int a = e / k, b = e % k;
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) acc += Y[w * k + a] * Y[w * k + b];
+      out[e] = acc;
+    }
+  }
+  __syncthreads();
+  RC_MARK(3);
+#undef RC_MARK
+}
+
+__global__ void k_cbar_finalize(const double* __restrict__ cpart, int nparts, int k, int eta,
+                                const double* __restrict__ w_dev, double* __restrict__ C64,
+                                float* __restrict__ C32) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const double w = *w_dev;
+  double s = 0.0;
+  for (int b = 0; b < nparts; ++b) s += cpart[(size_t)b * k * k + e];
+  const double c = (1.0 - w) * C64[e] + (w / eta) * s;
+  C64[e] = c;
+  C32[e] = (float)c;
+}
+
+}  // namespace somf

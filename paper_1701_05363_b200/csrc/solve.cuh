@@ -99,7 +99,8 @@ template <int KPL>
 __global__ void __launch_bounds__(kSolveThreads)
 k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
      double l1, double l2, int positive, double tol, int max_sweeps,
-     double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out) {
+     double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out,
+     float* __restrict__ AT32, int ldt) {
   extern __shared__ float Pk[];            // packed upper triangle, k(k+1)/2
   const int tid = threadIdx.x, nt = blockDim.x;
   const int np = k * (k + 1) / 2;
@@ -170,6 +171,7 @@ k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m
       if (row < k) {
         A64[(int64_t)row * m + s] = alpha[i];
         A32[(int64_t)row * m + s] = (float)alpha[i];
+        if (AT32) AT32[(int64_t)s * ldt + row] = (float)alpha[i];
       }
     }
     if (lane == 0 && sweeps_out) atomicMax(sweeps_out, sweep);

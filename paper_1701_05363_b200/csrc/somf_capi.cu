@@ -25,6 +25,9 @@
 #include "common.cuh"
 #include "mask.cuh"
 #include "gemm.cuh"
+#include "contract.cuh"
+#include "codes.cuh"
+#include "bbar.cuh"
 #include "solve.cuh"
 #include "bcd.cuh"
 #include "bcd_onchip.cuh"
@@ -114,6 +117,9 @@ struct somf_ctx {
   double* beta64 = nullptr;
   double* A64 = nullptr;
   float* A32 = nullptr;
+  float* AT32 = nullptr;     // codes transposed, eta x kp (bbar v3)
+  double* cpart = nullptr;   // per-CTA partial A A^T of the ridge code kernel
+  int cpart_n = 0;           // partials written by the last partial_fit code solve (0: none)
   double* red = nullptr;
   unsigned* bar = nullptr;
   int bcd_grid = 0;
@@ -249,12 +255,152 @@ static somf_status ensure_partial(somf_ctx* h, size_t floats) {
   return SOMF_OK;
 }
 
+// v2 Bbar variants (bbar.cuh): KC atoms per lane, RT rows per warp and pass
+typedef void (*BbFn)(const int32_t*, const int64_t*, const float*, int64_t, int, const float*, int, float*, int,
+                     const double*);
+struct BbVariant { int kc, rt; BbFn fn[3]; };   // [0] gather+compact X, [1] gather, [2] all rows
+#define BBV(KC, RT) {KC, RT, {k_bbar_v2<KC, RT, true, true>, k_bbar_v2<KC, RT, true, false>, \
+                              k_bbar_v2<KC, RT, false, false>}}
+static const BbVariant kBbVariants[] = {
+    BBV(1, 2), BBV(1, 4), BBV(1, 8), BBV(1, 16), BBV(2, 2), BBV(2, 4), BBV(2, 8), BBV(2, 16),
+    BBV(3, 2), BBV(3, 4), BBV(3, 8), BBV(3, 16), BBV(4, 2), BBV(4, 4), BBV(4, 8), BBV(4, 16),
+    BBV(8, 2), BBV(8, 4), BBV(8, 8)};
+#undef BBV
+
+typedef void (*Bb3Fn)(const int32_t*, const int64_t*, const float*, int64_t, int, const float*, int, int, float*,
+                      const double*, int);
+struct Bb3Variant { int kc, rt; Bb3Fn fn[2]; };   // [0] compact X, [1] gathered X
+#define BB3(KC, RT) {KC, RT, {k_bbar_v3<KC, RT, true>, k_bbar_v3<KC, RT, false>}}
+static const Bb3Variant kBb3Variants[] = {BB3(1, 4), BB3(1, 8), BB3(1, 16), BB3(2, 4), BB3(2, 8), BB3(2, 16),
+                                          BB3(3, 4), BB3(3, 8), BB3(3, 16), BB3(4, 4), BB3(4, 8), BB3(4, 16)};
+#undef BB3
+
+// Bbar rows (masked list, or all rows when !gather) -- bbar.cuh.  false when
+// the layout does not allow the 16-byte path (caller uses k_bbar_update).
+static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_t* q_dev, int64_t q_est,
+                           const float* X, int64_t ldx) {
+  const int k = h->cfg.k, eta = h->cfg.eta;
+  if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15)) return false;
+  int kc = (k + 31) / 32;
+  if (kc > 4) kc = 8;
+  const int64_t per = ceil_div(std::max<int64_t>(q_est, 1), h->nsm);
+  if (gather && kc <= 4) {
+    // v3: whole slice in shared memory (rows of one segment per warp: RT <= 16)
+    const int rt = per <= 32 ? 4 : per <= 64 ? 8 : 16;
+    const int64_t seg = 8 * rt;
+    const size_t smem = ((size_t)eta * 32 * kc + (size_t)seg * eta) * sizeof(float);
+    const Bb3Variant* v3 = nullptr;
+    for (const Bb3Variant& bv : kBb3Variants)
+      if (bv.kc == kc && bv.rt == rt) v3 = &bv;
+    if (v3 && smem <= 200 * 1024) {
+      Bb3Fn fn = v3->fn[xcompact ? 0 : 1];
+      if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+          cudaSuccess) {
+        fn<<<h->nsm, kBbThreads, smem, h->st>>>(h->idx, q_dev, X, ldx, eta, h->AT32, h->kp, k, h->Bbar, h->w_dev,
+                                                (int)seg);
+        return true;
+      }
+      cudaGetLastError();
+    }
+  }
+  const BbVariant* v = nullptr;
+  for (const BbVariant& bv : kBbVariants) {
+    if (bv.kc != kc) continue;
+    v = &bv;                                   // largest RT for this kc if none covers per
+    if (8 * bv.rt >= per) break;
+  }
+  const int rt = v->rt;
+  const size_t smem = ((size_t)2 * kBbWarps * rt * kBbSC + (size_t)2 * kBbSC * 32 * kc) * sizeof(float);
+  BbFn fn = v->fn[gather ? (xcompact ? 0 : 1) : 2];
+  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  fn<<<h->nsm, kBbThreads, smem, h->st>>>(gather ? h->idx : nullptr, q_dev, X, ldx, eta, h->A32, k, h->Bbar,
+                                          h->kp, h->w_dev);
+  return true;
+}
+
+// v2 contraction variants (contract.cuh): MT = atoms / 8 per thread, NT = columns / 32 per thread
+typedef void (*CtFn)(const int32_t*, const int64_t*, const float*, int, int, const float*, int64_t, int, float*);
+struct CtVariant { int mt, nt; CtFn fn[3]; };   // fn[0] gather+compact X, [1] gather, [2] contiguous
+#define CTV(MT, NT) {MT, NT, {k_contract_v2<MT, NT, true, true>, k_contract_v2<MT, NT, true, false>, \
+                              k_contract_v2<MT, NT, false, false>}}
+static const CtVariant kCtVariants[] = {
+    CTV(2, 2), CTV(2, 4), CTV(2, 6), CTV(2, 9), CTV(4, 2), CTV(4, 4), CTV(4, 6), CTV(4, 9),
+    CTV(9, 2), CTV(9, 4), CTV(9, 6), CTV(9, 9), CTV(16, 2), CTV(16, 4), CTV(16, 6)};
+#undef CTV
+
+// v3 (whole-slice staging) variants: single output tile per CTA
+typedef void (*Ct3Fn)(const int32_t*, const int64_t*, const float*, int, int, const float*, int64_t, int, float*,
+                      int);
+struct Ct3Variant { int mt, nt; Ct3Fn fn[2]; };   // [0] compact X, [1] gathered X
+#define CT3(MT, NT) {MT, NT, {k_contract_v3<MT, NT, true>, k_contract_v3<MT, NT, false>}}
+static const Ct3Variant kCt3Variants[] = {CT3(2, 2), CT3(2, 4), CT3(2, 6), CT3(2, 9), CT3(4, 2), CT3(4, 4),
+                                          CT3(4, 6), CT3(4, 9), CT3(9, 2), CT3(9, 4), CT3(9, 6), CT3(9, 9)};
+#undef CT3
+
 // [beta | G] over rows given by idx (or all rows), scaled by r.
 static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, const int64_t* q_dev,
                                    int64_t q_est, const float* X, int64_t ldx, int m, double r,
                                    double* beta, double* G) {
   const int k = h->cfg.k;
   const int nc = m + k;
+  const bool fast = (m % 4 == 0) && (ldx % 4 == 0) && (((uintptr_t)X & 15) == 0);
+  if (fast && gather) {
+    const Ct3Variant* v3 = nullptr;
+    for (const Ct3Variant& cv : kCt3Variants)
+      if (8 * cv.mt >= k && 32 * cv.nt >= nc && (!v3 || cv.mt * cv.nt < v3->mt * v3->nt)) v3 = &cv;
+    const int LDY = m + h->kp;
+    const int64_t per = ceil_div(std::max<int64_t>(q_est, 1), h->nsm) + 8;
+    const int64_t fit = (200 * 1024) / ((int64_t)LDY * 4 + 4);
+    const int seg = (int)std::min<int64_t>(per, fit);
+    if (v3 && seg >= 32) {
+      somf_status s = ensure_partial(h, (size_t)h->nsm * k * nc);
+      if (s) return s;
+      const size_t smem = (size_t)seg * LDY * sizeof(float) + (size_t)seg * sizeof(int);
+      Ct3Fn fn = v3->fn[xcompact ? 0 : 1];
+      CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      fn<<<h->nsm, kCtThreads, smem, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial, seg);
+      CKL();
+      const int64_t tot = (int64_t)k * nc;
+      k_contract_reduce2<<<(unsigned)ceil_div(tot, 32), 256, 0, h->st>>>(h->partial, h->nsm, k, m, r, beta, G);
+      CKL();
+      return SOMF_OK;
+    }
+  }
+  if (fast) {
+    // the fewest tiles (each gathered row is staged once per tile), then the
+    // least padding; register tile MT x NT <= 96 accumulators
+    const CtVariant* v = nullptr;
+    long best_tiles = 0, best_pad = 0;
+    for (const CtVariant& cv : kCtVariants) {
+      const long ta_ = ceil_div(k, 8 * cv.mt), tc_ = ceil_div(nc, 32 * cv.nt);
+      const long pad = ta_ * 8 * cv.mt * tc_ * 32 * cv.nt;
+      const long tiles = ta_ * tc_;
+      if (!v || tiles < best_tiles || (tiles == best_tiles && pad < best_pad)) {
+        v = &cv;
+        best_tiles = tiles;
+        best_pad = pad;
+      }
+    }
+    const int mt = v->mt, nt = v->nt;
+    const int ta = (int)ceil_div(k, 8 * mt), tc = (int)ceil_div(nc, 32 * nt);
+    // one CTA per SM in total (the row slices balance exactly)
+    int ns = std::max(1, (int)(h->nsm / (ta * tc)));
+    ns = (int)std::min<int64_t>(ns, std::max<int64_t>(1, q_est / (2 * kCtTK)));
+    somf_status s = ensure_partial(h, (size_t)ns * k * nc);
+    if (s) return s;
+    const size_t smem = (size_t)kCtStages * kCtTK * (8 * mt + 32 * nt) * sizeof(float);
+    CtFn fn = v->fn[gather ? (xcompact ? 0 : 1) : 2];
+    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<dim3(ta, tc, ns), kCtThreads, smem, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial);
+    CKL();
+    const int64_t tot = (int64_t)k * nc;
+    k_contract_reduce2<<<(unsigned)ceil_div(tot, 32), 256, 0, h->st>>>(h->partial, ns, k, m, r, beta, G);
+    CKL();
+    return SOMF_OK;
+  }
   const int ta = (int)ceil_div(k, TM), tc = (int)ceil_div(nc, TN);
   const int ns = split_count(h, ta * tc, q_est);
   somf_status s = ensure_partial(h, (size_t)ns * k * nc);
@@ -276,16 +422,37 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
 }
 
 static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta, int m, double tol,
-                                double* A64, float* A32) {
+                                double* A64, float* A32, bool want_cpart = false) {
   const somf_config& c = h->cfg;
   const int k = c.k;
   const int nw = kSolveThreads / 32;
   const int grid = (int)std::max<int64_t>(1, ceil_div(m, nw));
-  if (c.nu == 1.0 && !c.pos_code && k <= kRidgeMaxK) {
-    const size_t smem = ((size_t)k * (k + 1) + k + (size_t)nw * k) * sizeof(double);
-    CK(cudaFuncSetAttribute(k_ridge_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ridge_chol<<<grid, kSolveThreads, smem, h->st>>>(G, beta, k, m, c.lambda, A64, A32, h->err_dev);
-    CKL();
+  h->cpart_n = 0;
+  if (c.nu == 1.0 && !c.pos_code && k <= kRcMaxK) {
+    // ridge closed form (v2): every CTA factorises, 8 right-hand sides per CTA
+    const size_t smem = ((size_t)k * (k + 1) + (size_t)8 * k) * sizeof(double);
+    const int g = want_cpart ? (int)ceil_div(m, 8) : (int)std::min<int64_t>(ceil_div(m, 8), 4 * h->nsm);
+    if (want_cpart) {
+      if (!h->cpart) CK(dalloc(&h->cpart, (size_t)ceil_div(c.eta, 8) * k * k));
+      h->cpart_n = g;
+    }
+    double* cp = want_cpart ? h->cpart : nullptr;
+    const void* fn = nullptr;
+    switch ((k + 31) / 32) {
+      case 1: fn = (const void*)k_ridge_codes<1>; break;
+      case 2: fn = (const void*)k_ridge_codes<2>; break;
+      case 3: fn = (const void*)k_ridge_codes<3>; break;
+      case 4: fn = (const void*)k_ridge_codes<4>; break;
+      default: fn = (const void*)k_ridge_codes<5>; break;
+    }
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    double lam = c.lambda;
+    long long* rprof = h->prof_on ? h->bcd_prof + 72 : nullptr;    // slots 72..75 (ridge phases)
+    float* at = want_cpart ? h->AT32 : nullptr;
+    int ldt = h->kp;
+    void* args[] = {(void*)&G, (void*)&beta, (void*)&k, (void*)&m, (void*)&lam, (void*)&A64, (void*)&A32,
+                    (void*)&at, (void*)&ldt, (void*)&cp, (void*)&h->err_dev, (void*)&rprof};
+    CK(cudaLaunchKernel(fn, dim3(g), dim3(kRcThreads), args, smem, h->st));
     return SOMF_OK;
   }
   const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
@@ -295,7 +462,8 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
   case N:                                                                                 \
     CK(cudaFuncSetAttribute(k_cd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     k_cd<N><<<grid, kSolveThreads, smem, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,   \
-                                                  c.cd_max_sweeps, A64, A32, h->sweeps_dev); \
+                                                  c.cd_max_sweeps, A64, A32, h->sweeps_dev,  \
+                                                  want_cpart ? h->AT32 : nullptr, h->kp);    \
     break;
   switch (kpl) {
     LAUNCH_CD(1) LAUNCH_CD(2) LAUNCH_CD(3) LAUNCH_CD(4)
@@ -493,6 +661,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->beta64, (size_t)k * c.eta));
   A(dalloc(&h->A64, (size_t)k * c.eta));
   A(dalloc(&h->A32, (size_t)k * c.eta));
+  A(dalloc(&h->AT32, (size_t)c.eta * ((k + 3) & ~3)));
   A(dalloc(&h->bar, 4));
   A(dalloc(&h->qfull_dev, 1));
   // BCD grid: co-resident CTAs (cooperative launch), at most 2 per SM
@@ -517,7 +686,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->oc_rho, (size_t)2 * k));
   A(dalloc(&h->oc_bar, 4));
   A(dalloc(&h->lam_ws, (size_t)k));
-  A(dalloc(&h->bcd_prof, 72));
+  A(dalloc(&h->bcd_prof, 80));
   A(dalloc(&h->nt_acc, (size_t)kNtRing * k * 3));
   A(dalloc(&h->nt_accmm, (size_t)kNtRing * k * 2));
   if (c.bcd_kernel == 0 || c.bcd_kernel == 3) choose_newton(h);
@@ -534,7 +703,8 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       cudaMemset(h->oc_rho, 0, (size_t)2 * k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->theta_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->lam_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
-      cudaMemset(h->bcd_prof, 0, 72 * sizeof(long long)) != cudaSuccess ||
+      cudaMemset(h->AT32, 0, (size_t)c.eta * ((k + 3) & ~3) * sizeof(float)) != cudaSuccess ||
+      cudaMemset(h->bcd_prof, 0, 80 * sizeof(long long)) != cudaSuccess ||
       cudaMemset(h->nt_acc, 0, (size_t)kNtRing * k * 3 * sizeof(double)) != cudaSuccess ||
       init_accmm(h->nt_accmm, kNtRing * k) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
@@ -560,7 +730,7 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->partial, h->G64, h->beta64, h->A64, h->A32, h->red, h->bar, h->Ge,
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
-                  h->lam_ws, h->nt_acc, h->nt_accmm, h->bcd_prof};
+                  h->lam_ws, h->nt_acc, h->nt_accmm, h->bcd_prof, h->cpart, h->AT32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : h->evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
@@ -661,12 +831,17 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_CODES);                                         // Eq. somf_alpha
-    if (somf_status s = launch_codes(h, h->G64, h->beta64, eta, c.cd_tol, h->A64, h->A32)) return s;
+    if (somf_status s = launch_codes(h, h->G64, h->beta64, eta, c.cd_tol, h->A64, h->A32, true)) return s;
     h->launches[SOMF_PH_CODES] += 1;
   }
   {
     PhaseScope ps(h, SOMF_PH_CBAR);                                          // Eq. somf_partial
-    k_cbar_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->A64, k, eta, h->w_dev, h->C64, h->C32);
+    if (h->cpart_n > 0)
+      k_cbar_finalize<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->cpart, h->cpart_n, k, eta,
+                                                                                h->w_dev, h->C64, h->C32);
+    else
+      k_cbar_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->A64, k, eta, h->w_dev, h->C64,
+                                                                                h->C32);
     CKL();
     h->launches[SOMF_PH_CBAR] += 1;
   }
@@ -675,10 +850,14 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     const int grid_a = (int)ceil_div(k, TN);
     if (c.b_mode == SOMF_B_FULL) {
       k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
-      const int grid_r = (int)std::min<int64_t>(ceil_div(h->rows, TM), 8 * h->nsm);
-      k_bbar_update<false, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
-          nullptr, h->qfull_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+      if (!launch_bbar_v2(h, false, false, h->qfull_dev, h->rows, Xd, ld)) {
+        const int grid_r = (int)std::min<int64_t>(ceil_div(h->rows, TM), 8 * h->nsm);
+        k_bbar_update<false, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
+            nullptr, h->qfull_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+      }
       h->launches[SOMF_PH_BBAR] += 2;
+    } else if (launch_bbar_v2(h, true, compact, h->q_dev, q_est, Xd, ld)) {
+      h->launches[SOMF_PH_BBAR] += 1;
     } else {
       const int grid_r = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q_est, TM), 8 * h->nsm));
       if (compact)
@@ -942,10 +1121,10 @@ SOMF_EXPORT somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* 
 SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {
   if (!h || !cycles) return SOMF_E_ARG;
   CK(cudaStreamSynchronize(h->st));
-  long long v[72];
+  long long v[80];
   CK(cudaMemcpy(v, h->bcd_prof, sizeof(v), cudaMemcpyDeviceToHost));
   CK(cudaMemset(h->bcd_prof, 0, sizeof(v)));
-  for (int i = 0; i < 72; ++i) cycles[i] = v[i];
+  for (int i = 0; i < 80; ++i) cycles[i] = v[i];
   return SOMF_OK;
 }
 

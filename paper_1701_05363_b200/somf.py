@@ -194,10 +194,11 @@ class Somf:
     BCD_PHASES = ("setup", "recurrence", "stats", "barrier", "update", "finish", "writeback")
 
     def bcd_phase_cycles(self):
-        v = np.zeros(72, np.int64)
+        v = np.zeros(80, np.int64)
         _check(lib().somf_bcd_phase_cycles(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
         out = dict(zip(self.BCD_PHASES, v[:7].tolist()), launches=int(v[7]))
-        out["unconverged_per_round"] = v[8:].tolist()
+        out["unconverged_per_round"] = v[8:72].tolist()
+        out["ridge"] = dict(zip(("load", "factor", "solve", "cbar_partial"), v[72:76].tolist()))
         return out
 
     @property
