@@ -310,7 +310,7 @@ def run_somf(args):
         model.partial_fit(batches[i % nb])
     torch.cuda.synchronize()
     model.profile_read()
-    model.profile_enable(True)
+    model.profile_enable(False)
     clocks = Clocks(local)
     if world > 1:
         dist.barrier()
@@ -322,10 +322,16 @@ def run_somf(args):
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
+    launch_counts = model.profile_read()     # launches of the timed (unprofiled) steps
+    info = model.last_step_info()
+    # per-kernel durations: the same number of steps again with CUDA events
+    # around every phase on the launching stream (kept out of the timed value)
+    model.profile_enable(True)
+    time_steps(model, batches, args.warmup + args.steps, args.steps, flush, stream)
     prof = model.profile_read()
     bcd_cyc = model.bcd_phase_cycles()
     model.profile_enable(False)
-    info = model.last_step_info()
+    prof["launches"] = launch_counts["launches"]
     step_ms = sum(ms) / len(ms)
     if world > 1:
         tt = torch.tensor([step_ms], device=dev)
@@ -361,8 +367,9 @@ def run_somf(args):
     if bcd_cyc["launches"]:
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
         roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
-                                         if ph not in ("launches", "unconverged_per_round", "ridge")}
+                                         if ph not in ("launches", "unconverged_per_round", "ridge", "setup_split")}
         roof["ridge_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["ridge"].items()}
+        roof["bcd_setup_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["setup_split"].items()}
         unc = [u / bcd_cyc["launches"] for u in bcd_cyc["unconverged_per_round"]]
         while unc and unc[-1] == 0:
             unc.pop()

@@ -195,7 +195,8 @@ int32_t somf_bcd_variant(somf_handle h);
  * [3] grid barrier, [4] threshold update, [5] finish, [6] write-back,
  * [7] launches, [8 + r] atoms not yet converged after round r (r < 64);
  * [72..75] ridge code kernel (CTA 0): load, factorisation, substitutions,
- * Cbar partial.  cycles must hold 80 entries.  Synchronises.  Zeros for the
+ * Cbar partial; [76..78] the setup of [0] split: parameters, row gathers,
+ * permutation (the residual GEMM is [0] minus these).  cycles must hold 80 entries.  Synchronises.  Zeros for the
  * kernels not launched. */
 somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles);
 

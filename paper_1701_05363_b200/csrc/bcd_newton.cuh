@@ -29,7 +29,7 @@
 
 namespace somf {
 
-constexpr int kNtThreads = 256;     // >= rows per CTA
+constexpr int kNtThreads = 384;     // 2 threads per masked row: >= 2 x rows per CTA
 constexpr int kNtRing = 3;
 // Convergence: every atom exact (its active set reproduces itself) and its
 // lambda stable to this relative tolerance between two rounds.  The
@@ -106,9 +106,14 @@ __device__ __forceinline__ void nt_red_add(double* p, double v) {
 // statically and stays in registers), then the next position.
 template <int KPT, int PP>
 struct NtRec {
-  static __device__ __forceinline__ void run(float (&R)[KPT], const float* drow, float* vrow, float* dnrow,
-                                             const float* Cpi, const float* invc_s, const float* thf_s,
-                                             const float* scf_s, const float* vlo_s, int k) {
+  // __restrict__: the v / d stores of one position must not pin the loads of
+  // the next positions (and the Cbar rows) behind them, or no two positions'
+  // dependency chains can overlap
+  static __device__ __forceinline__ void run(float (&R)[KPT], const float* __restrict__ drow,
+                                             float* __restrict__ vrow, float* __restrict__ dnrow,
+                                             const float* __restrict__ Cpi, const float* __restrict__ invc_s,
+                                             const float* __restrict__ thf_s, const float* __restrict__ scf_s,
+                                             const float* __restrict__ vlo_s, int k) {
     if (PP >= k) return;
     // branch-free: copy = (th 0, scale 1), zero = scale 0, dead = (invc 0, copy)
     const float dold = drow[PP];
@@ -137,6 +142,48 @@ template <int KPT>
 struct NtRec<KPT, KPT> {
   static __device__ __forceinline__ void run(float (&)[KPT], const float*, float*, float*, const float*,
                                              const float*, const float*, const float*, const float*, int) {}
+};
+
+// Two threads per row (lanes 2r and 2r+1): the thread of parity t holds the
+// residual of the positions p = t (mod 2) in R[p / 2].  Position PP is owned by
+// parity PP % 2 (compile-time); the owner's d - d_old reaches its partner with
+// one shuffle, then each thread updates its own later positions.  Halves the
+// FMAs per thread and doubles the warps that hide the per-position chain.
+template <int KPT, int PP>
+struct NtRec2 {
+  static __device__ __forceinline__ void run(float (&R)[KPT / 2], int par, int pairbase, bool wr,
+                                             const float* drow, float* vrow, float* dnrow, const float* Cpi,
+                                             const float* invc_s, const float* thf_s, const float* scf_s,
+                                             const float* vlo_s, int k) {
+    if (PP >= k) return;
+    constexpr int own = PP & 1;
+    const float dold = drow[PP];
+    const float u = fmaf(R[PP / 2], invc_s[PP], dold);                // P:861 (valid in the owner)
+    const float v = fmaxf(u, vlo_s[PP]);
+    const float d = copysignf(fmaxf(fabsf(v) - thf_s[PP], 0.f) * scf_s[PP], v);
+    if (wr && par == own) {
+      vrow[PP] = v;
+      dnrow[PP] = d;
+    }
+    const float delta = __shfl_sync(0xffffffffu, d - dold, pairbase | own);
+    const float* crow = Cpi + (size_t)PP * KPT;
+#pragma unroll
+    for (int l2 = PP / 2; l2 < KPT / 2; ++l2) {
+      // my position l = 2 l2 + par; update it if it comes after PP
+      const float2 c = *reinterpret_cast<const float2*>(crow + 2 * l2);
+      const float cl = par ? c.y : c.x;
+      const bool later = (2 * l2 + 1 > PP);            // parity-1 position 2 l2 + 1 is later
+      const bool later0 = (2 * l2 > PP);               // parity-0 position 2 l2 is later
+      if (par ? later : later0) R[l2] = fmaf(-delta, cl, R[l2]);
+    }
+    NtRec2<KPT, PP + 1>::run(R, par, pairbase, wr, drow, vrow, dnrow, Cpi, invc_s, thf_s, scf_s, vlo_s, k);
+  }
+};
+template <int KPT>
+struct NtRec2<KPT, KPT> {
+  static __device__ __forceinline__ void run(float (&)[KPT / 2], int, int, bool, const float*, float*, float*,
+                                             const float*, const float*, const float*, const float*, const float*,
+                                             int) {}
 };
 
 template <int KPT>
@@ -171,12 +218,38 @@ k_bcd_newton(NtArgs P) {
   int* rows_s = reinterpret_cast<int*>(part + 3 * (size_t)max(1, kNtThreads / max(k, 1)) * KPT +
                                        (size_t)max(1, kNtThreads / max(k, 1)) * KPT);   // cap
   __shared__ double dmax_s;
+  __shared__ double diag_s[KPT], lws_s[KPT], ns_s[KPT];
   long long t_mark = clock64();
-  // ---- setup ------------------------------------------------------------------
+  // ---- setup: round 1 (independent loads) ------------------------------------------
+  // Cbar (fp32, atom order) -> Rini as a staging buffer when it fits, the row
+  // indices, the atom order and the per-atom scalars, all in flight at once
+  const bool cstage = (size_t)cap * LD >= (size_t)k * k + 4;
+  if (cstage) {
+    for (int e = tid; e < (k * k + 3) / 4; e += kNtThreads) cp_async16(Rini + 4 * e, P.C32 + 4 * e);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   for (int r = tid; r < nr; r += kNtThreads) rows_s[r] = P.idx[lo + r];
+  for (int p = tid; p < k; p += kNtThreads) {
+    jmap_s[p] = P.perm[p];
+    diag_s[p] = P.C64[(int64_t)p * k + p];
+    lws_s[p] = P.lam_ws[p];
+    ns_s[p] = P.nslack[p];
+  }
+  __syncthreads();
+  // ---- round 2: the masked rows of D and Bbar (cp.async, every chunk in flight) ----
+  {
+    const int c4 = kp / 4;
+    for (int e = tid; e < nr * c4; e += kNtThreads) {
+      const int row = e / c4, c = e % c4;
+      const int64_t goff = (int64_t)rows_s[row] * kp + 4 * c;
+      cp_async16(V + (size_t)row * kp + 4 * c, P.D + goff);
+      cp_async16(Dn + (size_t)row * kp + 4 * c, P.Bbar + goff);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   if (wid == 0) {
     double dm = 1.0;
-    for (int j = lane; j < k; j += 32) dm = fmax(dm, P.C64[(int64_t)j * k + j]);
+    for (int j = lane; j < k; j += 32) dm = fmax(dm, diag_s[j]);
     dm = warp_max(dm);
     if (lane == 0) dmax_s = dm;
   }
@@ -184,16 +257,15 @@ k_bcd_newton(NtArgs P) {
   const double dmax = dmax_s;
   for (int p = tid; p < KPT; p += kNtThreads) {
     if (p < k) {
-      const int j = P.perm[p];
-      jmap_s[p] = j;
+      const int j = jmap_s[p];
       pinv_s[j] = p;
-      const double cjj = P.C64[(int64_t)j * k + j];
+      const double cjj = diag_s[j];
       const bool dead = !(cjj > 1e-12 * dmax);                      // R10
       invc_s[p] = dead ? 0.f : (float)(1.0 / cjj);
       vlo_s[p] = (P.pos && !dead) ? 0.f : -INFINITY;      // D >= 0 clamp; dead atoms keep d
-      const double lw = dead ? 0.0 : P.lam_ws[j];
+      const double lw = dead ? 0.0 : lws_s[j];
       lam_s[p] = lw;
-      rho_s[p] = P.nslack[j];     // n_{t-1}^(j); becomes rho_j after round 0
+      rho_s[p] = ns_s[j];         // n_{t-1}^(j); becomes rho_j after round 0
       mode_s[p] = dead ? kModeDead : (lw > 0.0 ? kModeShrink : kModeCopy);
       thf_s[p] = (float)(a * lw);
       scf_s[p] = (float)(1.0 / (1.0 + b * lw));
@@ -206,30 +278,17 @@ k_bcd_newton(NtArgs P) {
       lam_s[p] = 0.0;
     }
   }
+  asm volatile("cp.async.wait_group 1;" ::: "memory");     // Cbar staged
   __syncthreads();
   for (int e = tid; e < k * KPT; e += kNtThreads) {
     const int p = e / KPT, l = e % KPT;
-    Cpi[e] = l < k ? P.C32[(int64_t)jmap_s[p] * k + jmap_s[l]] : 0.f;
+    const int64_t src = (int64_t)jmap_s[p] * k + (l < k ? jmap_s[l] : 0);
+    Cpi[e] = l < k ? (cstage ? Rini[src] : __ldg(P.C32 + src)) : 0.f;
   }
-  // stage the masked rows of D and Bbar with cp.async (all 16-byte chunks of
-  // all rows in flight at once: rows are ~r rows apart in HBM), then permute
-  // the columns into pi order in shared memory
-  {
-    const int c4 = kp / 4;
-    for (int e = tid; e < nr * c4; e += kNtThreads) {
-      const int row = e / c4, c = e % c4;
-      const int64_t goff = (int64_t)rows_s[row] * kp + 4 * c;
-      cp_async16(V + (size_t)row * kp + 4 * c, P.D + goff);
-      cp_async16(Dn + (size_t)row * kp + 4 * c, P.Bbar + goff);
-    }
-    cp_async_wait_all();
-  }
-#pragma unroll 8
-  for (int e = tid; e < k * KPT; e += kNtThreads) {
-    const int p = e / KPT, l = e % KPT;
-    Cpi[e] = l < k ? __ldg(P.C32 + (int64_t)jmap_s[p] * k + jmap_s[l]) : 0.f;
-  }
+  NT_MARK(76);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");     // rows staged
   __syncthreads();
+  NT_MARK(77);
   for (int e = tid; e < nr * KPT; e += kNtThreads) {
     const int row = e / KPT, p = e % KPT;
     const bool in = p < k;
@@ -238,29 +297,34 @@ k_bcd_newton(NtArgs P) {
     Rini[(size_t)row * LD + p] = in ? Dn[(size_t)row * kp + j] : 0.f;
   }
   __syncthreads();
-  // R = P Bbar - P D Cbar, 4 rows x 4 positions per item
+  NT_MARK(78);
+  // R = P Bbar - P D Cbar: 8 rows x 8 positions per item (about one item per thread)
   {
-    const int nrb = (nr + 3) / 4, npb = (k + 3) / 4;
+    const int nrb = (nr + 7) / 8, npb = (k + 7) / 8;
     for (int it = tid; it < nrb * npb; it += kNtThreads) {
-      const int r0 = (it / npb) * 4, p0 = (it % npb) * 4;
-      float acc[4][4] = {};
-      for (int l = 0; l < k; ++l) {
-        const float4 c = *reinterpret_cast<const float4*>(Cpi + (size_t)l * KPT + p0);
+      const int r0 = (it / npb) * 8, p0 = (it % npb) * 8;
+      float acc[8][8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float d = r0 + i < nr ? Dold[(size_t)(r0 + i) * LD + l] : 0.f;
-          acc[i][0] = fmaf(d, c.x, acc[i][0]);
-          acc[i][1] = fmaf(d, c.y, acc[i][1]);
-          acc[i][2] = fmaf(d, c.z, acc[i][2]);
-          acc[i][3] = fmaf(d, c.w, acc[i][3]);
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+      for (int l = 0; l < k; ++l) {
+        const float4 c0 = *reinterpret_cast<const float4*>(Cpi + (size_t)l * KPT + p0);
+        const float4 c1 = *reinterpret_cast<const float4*>(Cpi + (size_t)l * KPT + p0 + 4);
+        const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float d = Dold[(size_t)min(r0 + i, cap - 1) * LD + l];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(d, cv[c], acc[i][c]);
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 8; ++i) {
         const int row = r0 + i;
         if (row >= nr) continue;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 8; ++c) {
           const int p = p0 + c;
           if (p < k) Rini[(size_t)row * LD + p] -= acc[i][c];
         }

@@ -510,7 +510,7 @@ static const NtVariant kNtVariants[] = {NTV(16), NTV(32), NTV(48), NTV(64), NTV(
 static void choose_newton(somf_ctx* h) {
   const int k = h->cfg.k;
   const int cap = (int)ceil_div(h->q_cap, h->nsm);
-  if (cap > kNtThreads) return;
+  if (2 * cap > kNtThreads) return;                  // two threads per masked row
   for (const NtVariant& v : kNtVariants) {
     if (v.kpt < k) continue;
     const int LD = v.kpt + 1;
@@ -645,7 +645,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->D, (size_t)rows * h->kp));
   A(dalloc(&h->Bbar, (size_t)rows * h->kp));
   A(dalloc(&h->C64, (size_t)k * k));
-  A(dalloc(&h->C32, (size_t)k * k));
+  A(dalloc(&h->C32, (size_t)k * k + 4));   // +4: 16-byte staging reads in the BCD
   A(dalloc(&h->nslack, (size_t)k));
   A(dalloc(&h->t_dev, 1));
   A(dalloc(&h->w_dev, 1));

@@ -199,6 +199,7 @@ class Somf:
         out = dict(zip(self.BCD_PHASES, v[:7].tolist()), launches=int(v[7]))
         out["unconverged_per_round"] = v[8:72].tolist()
         out["ridge"] = dict(zip(("load", "factor", "solve", "cbar_partial"), v[72:76].tolist()))
+        out["setup_split"] = dict(zip(("params", "gather", "permute"), v[76:79].tolist()))
         return out
 
     @property
