@@ -15,8 +15,10 @@ A "step" is one somf_partial_fit on a batch resident in HBM; L2 is flushed
 `e2e` times the same call with the batch in pinned HOST memory (the library
 gathers the q selected rows over the host link) plus the device->host read of
 the step's codes.  `--impl reference` times the float64 CPU oracle on the same
-workload (bounded sample).  N > 1 (torchrun): independent replicas, one per
-GPU (no row sharding yet -- DESIGN.md §7), value = total columns/s.
+workload (bounded sample).  N > 1 (torchrun): one rank per
+GPU, each owning rows [p i / N, p (i+1) / N) of D, Bbar and every batch; the
+library's exchange points ([beta | G], radius sums, per-round threshold sums)
+go through an NCCL allreduce; value = the job's columns/s.
 """
 from __future__ import annotations
 
@@ -278,31 +280,41 @@ def run_somf(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    # ranks beyond the visible GPUs share them (only with --dist-backend gloo:
+    # a host-side collective, no kernel waits on another rank)
+    dev = torch.device("cuda", local % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     import paper_1701_05363_b200 as somf_pkg
     somf_pkg.lib()
     w = WORKLOAD
     p, k, eta, r = w["p"], w["k"], w["eta"], args.r
     stream = torch.cuda.current_stream(dev)
     nb = min(args.warmup + args.steps, 24)
-    stream_gen = FmriStreamGPU(args.burn_in + nb, eta, k, seed=rank, device=dev)
-    D0 = stream_gen.d0()
+    # every rank draws the same stream and keeps its row range [lo, hi) (row
+    # sharding): the job streams eta columns per step over all ranks
+    stream_gen = FmriStreamGPU(args.burn_in + nb, eta, k, seed=0, device=dev)
+    lo, hi = p * rank // world, p * (rank + 1) // world
+    D0 = stream_gen.d0()[lo:hi]
     # the timed pool: the batches that follow the burn-in in the stream
-    batches = [stream_gen.batch(args.burn_in + b) for b in range(nb)]
+    batches = [stream_gen.batch(args.burn_in + b)[lo:hi] for b in range(nb)]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
     def make(rr, burn_in):
         m = somf_pkg.Somf(p, k, eta, lam=w["lam"], nu=w["nu"], mu=w["mu"], pos_code=w["pos_code"],
-                          pos_dict=w["pos_dict"], r=rr, u=w["u"], seed=rank, device=local, stream=stream)
+                          row_lo=lo, row_hi=hi,
+                          pos_dict=w["pos_dict"], r=rr, u=w["u"], seed=0, device=dev.index, stream=stream)
+        if world > 1:
+            m.set_reducer(somf_pkg.dist_reducer())      # NCCL allreduce at every exchange point
         m.set_components(D0)
         # burn-in: the learner reaches its steady state (t > burn_in) on fresh
         # stream batches before anything is timed (steady state)
         for b in range(burn_in):
-            m.partial_fit(stream_gen.batch(b))
+            m.partial_fit(stream_gen.batch(b)[lo:hi])
         return m
 
     model = make(r, args.burn_in)
@@ -311,7 +323,7 @@ def run_somf(args):
     torch.cuda.synchronize()
     model.profile_read()
     model.profile_enable(False)
-    clocks = Clocks(local)
+    clocks = Clocks(dev.index)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -337,7 +349,7 @@ def run_somf(args):
         tt = torch.tensor([step_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms = float(tt.item())
-    value = world * eta / (step_ms * 1e-3)
+    value = eta / (step_ms * 1e-3)      # the job's columns per second (all ranks share each column)
 
     # --- roofline of the dominant kernel ------------------------------------
     q = p / r
@@ -401,14 +413,14 @@ def run_somf(args):
             times.append(a.elapsed_time(b))
             qs.append(m2.last_step_info()["q"])
         e_ms = sum(times) / len(times)
-        e2e = {"value": world * eta / (e_ms * 1e-3), "unit": UNIT,
+        e2e = {"value": eta / (e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(4 * eta * sum(qs) / len(qs)), "d2h_bytes_per_step": 4 * k * eta,
                "ms_per_step": e_ms, "path": "somf_partial_fit(pinned host X) + somf_get_codes(host)"}
         del m2
 
     # --- r sweep (BASELINE metric lists r = 1/4/12/24) ---------------------------
     sweep = {}
-    if not args.no_sweep:
+    if not args.no_sweep and world == 1:
         for rr in (1.0, 4.0, 12.0, 24.0):
             m3 = make(rr, args.burn_in if rr > 1.0 else min(args.burn_in, 10))
             for i in range(3):
@@ -432,14 +444,15 @@ def run_somf(args):
 
     launches = int(sum(prof["launches"].values()))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (fMRI-shaped stand-in, DESIGN.md §3)",
             "config": {"workload": w["name"], "p": p, "k": k, "eta": eta, "r": r, "lambda": w["lam"],
                        "code": "ridge", "dict": "l1-ball", "b_mode": "masked",
                        "bcd_kernel": model.bcd_variant,
                        "l2": "flushed (256 MiB write) before every timed step",
                        "burn_in_iterations": args.burn_in,
-                       "parallelism": "single" if world == 1 else f"replicas x{world}"},
+                       "parallelism": "single" if world == 1 else f"row-sharded x{world} ({args.dist_backend} allreduce)"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / steps_prof,
             "clocks": clk, "sweep": sweep, "wall_s_timed": t_wall}
@@ -455,6 +468,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="somf", choices=["somf", "reference"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collectives of the row-sharded step (gloo: CPU-staged, lets N ranks share one GPU)")
     ap.add_argument("--burn-in", type=int, default=60,
                     help="untimed SOMF iterations before warm-up (steady state, t > burn-in)")
     ap.add_argument("--r", type=float, default=WORKLOAD["r"])

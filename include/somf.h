@@ -220,6 +220,29 @@ somf_status somf_profile_enable(somf_handle h, int32_t on);
  * Any pointer may be NULL.  Launch counts are kept even when timing is off. */
 somf_status somf_profile_read(somf_handle h, double* ms, int64_t* launches, int64_t* steps);
 
+/* ---- row sharding -------------------------------------------
+ * A handle that owns rows [row_lo, row_hi) of a p-row problem computes only
+ * the contributions of its rows to every grid-wide quantity of the step.  The
+ * reducer combines them over the ranks IN PLACE, elementwise, on `stream`
+ * (the handle's stream; work may be enqueued, the call may return before it
+ * completes), and returns 0 on success.  dtype: SOMF_DT_F64 (double) or
+ * SOMF_DT_I32 (non-negative int32: float bit patterns of values >= 0, whose
+ * integer order is their float order); op: SOMF_OP_SUM / MIN / MAX.
+ * Exchange points of one somf_partial_fit (every rank calls in the same order):
+ *   [beta | G]  k*eta + k*k doubles, SUM            (Eq. a)
+ *   radius sums ||P d_j||  2k doubles, SUM
+ *   per BCD round: 3k doubles SUM, k MIN, k MAX     (R17 threshold sums)
+ * and of somf_transform / somf_objective: [beta | G] of X, SUM; the residual
+ * column sums, m doubles, SUM.  The code solve, Cbar and the threshold
+ * updates then run identically on every rank.  fn == NULL restores the
+ * single-GPU path.  With a reducer, Alg. 4 runs as one kernel per round with
+ * a host read of the convergence flag per round. */
+typedef int32_t (*somf_reduce_fn)(void* user, void* buf, int64_t count, int32_t dtype, int32_t op,
+                                  void* stream);
+enum { SOMF_DT_F64 = 0, SOMF_DT_I32 = 1 };
+enum { SOMF_OP_SUM = 0, SOMF_OP_MIN = 1, SOMF_OP_MAX = 2 };
+somf_status somf_set_reducer(somf_handle h, somf_reduce_fn fn, void* user);
+
 /* ---- stateless kernels (same arithmetic as the handle's; parity tests) ---- */
 
 /* Ascending global row indices i in [row_lo, row_hi) selected by M_t

@@ -6,7 +6,7 @@ in ``csrc/``, compiled into ``libsomf.so`` and exposed through the C ABI of
 """
 from ._lib import build, LIB_PATH  # noqa: F401
 from .somf import (Somf, SomfError, mask_rows, atom_permutation, column_ids,  # noqa: F401
-                   project_columns, lib)
+                   project_columns, lib, dist_reducer, device_view)
 
 __all__ = ["Somf", "SomfError", "mask_rows", "atom_permutation", "column_ids",
-           "project_columns", "build", "lib", "LIB_PATH"]
+           "project_columns", "build", "lib", "LIB_PATH", "dist_reducer", "device_view"]

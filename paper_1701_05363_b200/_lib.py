@@ -79,6 +79,7 @@ SIGNATURES = [
     ("somf_set_state", I32, [P, P, P, P, P, I64]),
     ("somf_last_step_info", I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(D)]),
     ("somf_bcd_variant", I32, [P]),
+    ("somf_set_reducer", I32, [P, P, P]),
     ("somf_bcd_phase_cycles", I32, [P, P]),
     ("somf_profile_enable", I32, [P, I32]),
     ("somf_profile_read", I32, [P, P, P, C.POINTER(I64)]),
@@ -87,6 +88,12 @@ SIGNATURES = [
     ("somf_column_ids", I32, [U64, I64, I64, I64, P, P]),
     ("somf_project_columns", I32, [P, I64, I32, I64, P, D, I32, P, P]),
 ]
+
+
+# int32 reducer(void* user, void* buf, int64 count, int32 dtype, int32 op, void* stream)
+REDUCE_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p)
+DT_F64, DT_I32 = 0, 1
+OP_SUM, OP_MIN, OP_MAX = 0, 1, 2
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:

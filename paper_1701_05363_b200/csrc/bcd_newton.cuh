@@ -98,6 +98,55 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// One Michelot step of atom p from the grid sums over {|v| > a lam} (R17):
+// returns 1 when the atom is converged (exact active set, lambda stable).
+// Shared by the single-GPU kernel and the row-sharded round kernels.
+__device__ __forceinline__ int nt_atom_update(double a, double b, double rho, double cnt, double S1, double S2,
+                                              double mnv, double mxv, int mode, double lam, int* nmode_out,
+                                              double* nlam_out) {
+  const double th = a * lam;
+  int nmode = mode, conv = 1;
+  double nlam = lam;
+  if (mode == kModeDead) {
+    conv = 1;
+  } else if (!(rho > 0.0)) {
+    nmode = kModeZero;                                               // R11
+    conv = mode == kModeZero;
+  } else if (!(th > 0.0)) {
+    // sums over every nonzero |v|: feasibility, else the root for all of them
+    const double Nv = a * S1 + 0.5 * b * S2;
+    if (Nv <= rho) {
+      nlam = 0.0;
+      nmode = kModeCopy;
+    } else {
+      nlam = enet_lambda(a, b, rho, cnt, S1, S2);
+      nmode = nlam > 0.0 ? kModeShrink : kModeCopy;
+    }
+    // exact when the active set at the new threshold is still "every nonzero"
+    const bool exact = nlam == 0.0 || !(a > 0.0) || a * nlam < mnv;
+    conv = exact && nmode == mode && fabs(nlam - lam) <= kNtLamTol * fmax(nlam, 1e-300);
+  } else {
+    nlam = enet_lambda(a, b, rho, cnt, S1, S2);
+    nmode = nlam > 0.0 ? kModeShrink : kModeCopy;
+    const double nth = a * nlam;
+    const bool exact = nlam > 0.0 && mxv <= nth && nth < mnv;
+    conv = exact && fabs(nlam - lam) <= kNtLamTol * nlam;
+  }
+  *nmode_out = nmode;
+  *nlam_out = nlam;
+  return conv;
+}
+
+// ||d_j|| after the projection, from the sums of its final round
+__device__ __forceinline__ double nt_norm_d(double a, double b, int mode, double lam, double cnt, double S1,
+                                           double S2) {
+  const double t = a * lam, opb = 1.0 + b * lam;
+  if (mode == kModeCopy) return a * S1 + 0.5 * b * S2;
+  if (mode == kModeShrink)
+    return a * (S1 - cnt * t) / opb + 0.5 * b * (S2 - 2.0 * t * S1 + cnt * t * t) / (opb * opb);
+  return 0.0;
+}
+
 __device__ __forceinline__ void nt_red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
@@ -452,34 +501,9 @@ k_bcd_newton(NtArgs P) {
       const double mxv = (double)__uint_as_float(__ldcg(mm + 1));
       const int mode = mode_s[p];
       const double lam = lam_s[p];
-      const double th = a * lam;
-      int nmode = mode;
-      double nlam = lam;
-      if (mode == kModeDead) {
-        conv = 1;
-      } else if (!(rho > 0.0)) {
-        nmode = kModeZero;                                               // R11
-        conv = mode == kModeZero;
-      } else if (!(th > 0.0)) {
-        // sums over every nonzero |v|: feasibility, else the root for all of them
-        const double Nv = a * S1 + 0.5 * b * S2;
-        if (Nv <= rho) {
-          nlam = 0.0;
-          nmode = kModeCopy;
-        } else {
-          nlam = enet_lambda(a, b, rho, cnt, S1, S2);
-          nmode = nlam > 0.0 ? kModeShrink : kModeCopy;
-        }
-        // exact when the active set at the new threshold is still "every nonzero"
-        const bool exact = nlam == 0.0 || !(a > 0.0) || a * nlam < mnv;
-        conv = exact && nmode == mode && fabs(nlam - lam) <= kNtLamTol * fmax(nlam, 1e-300);
-      } else {
-        nlam = enet_lambda(a, b, rho, cnt, S1, S2);
-        nmode = nlam > 0.0 ? kModeShrink : kModeCopy;
-        const double nth = a * nlam;
-        const bool exact = nlam > 0.0 && mxv <= nth && nth < mnv;
-        conv = exact && fabs(nlam - lam) <= kNtLamTol * nlam;
-      }
+      int nmode;
+      double nlam;
+      conv = nt_atom_update(a, b, rho, cnt, S1, S2, mnv, mxv, mode, lam, &nmode, &nlam);
       lam_s[p] = nlam;
       mode_s[p] = nmode;
       thf_s[p] = nmode == kModeShrink ? (float)(a * nlam) : 0.f;
@@ -506,13 +530,9 @@ k_bcd_newton(NtArgs P) {
       if (mode != kModeDead && blockIdx.x == 0) {
         const double* acc = P.acc + ((size_t)ring * k + p) * 3;
         const double cnt = __ldcg(acc), S1 = __ldcg(acc + 1), S2 = __ldcg(acc + 2);
-        const double lam = lam_s[p], t = a * lam, opb = 1.0 + b * lam;
-        double Nd = 0.0;
-        if (mode == kModeCopy) Nd = a * S1 + 0.5 * b * S2;
-        else if (mode == kModeShrink)
-          Nd = a * (S1 - cnt * t) / opb + 0.5 * b * (S2 - 2.0 * t * S1 + cnt * t * t) / (opb * opb);
+        const double Nd = nt_norm_d(a, b, mode, lam_s[p], cnt, S1, S2);
         P.nslack[j] = rho_s[p] - Nd;
-        P.lam_ws[j] = lam;
+        P.lam_ws[j] = lam_s[p];
       }
     }
   }

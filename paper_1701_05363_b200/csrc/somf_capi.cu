@@ -32,6 +32,7 @@
 #include "bcd.cuh"
 #include "bcd_onchip.cuh"
 #include "bcd_newton.cuh"
+#include "bcd_shard.cuh"
 
 using namespace somf;
 
@@ -136,6 +137,12 @@ struct somf_ctx {
   double* lam_ws = nullptr;
   double* nt_acc = nullptr;
   long long* bcd_prof = nullptr;   // SM cycles per BCD phase (somf_bcd_phase_cycles)
+  // row sharding (somf_set_reducer): the caller's allreduce over the ranks
+  somf_reduce_fn reducer = nullptr;
+  void* reducer_user = nullptr;
+  ShState sh{};
+  bool sh_alloc = false;
+  int* sh_conv_host = nullptr;     // pinned
   unsigned* nt_accmm = nullptr;
   double* oc_acc = nullptr;
   unsigned* oc_accmin = nullptr;
@@ -570,6 +577,127 @@ static void choose_onchip(somf_ctx* h) {
   }
 }
 
+static somf_status reduce(somf_ctx* h, void* buf, int64_t n, int32_t dt, int32_t op) {
+  if (!h->reducer || n <= 0) return SOMF_OK;
+  const int32_t rc = h->reducer(h->reducer_user, buf, n, dt, op, (void*)h->st);
+  if (rc != 0) {
+    set_err(h, "reducer failed with %d", rc);
+    return SOMF_E_NCCL;
+  }
+  return SOMF_OK;
+}
+
+static somf_status shard_alloc(somf_ctx* h) {
+  if (h->sh_alloc) return SOMF_OK;
+  const int k = h->cfg.k;
+  const int64_t qc = std::max<int64_t>(h->q_cap, 1);
+  ShState& S = h->sh;
+  CK(dalloc(&S.jmap, (size_t)k));
+  CK(dalloc(&S.pinv, (size_t)k));
+  CK(dalloc(&S.invc, (size_t)k));
+  CK(dalloc(&S.vlo, (size_t)k));
+  CK(dalloc(&S.thf, (size_t)k));
+  CK(dalloc(&S.scf, (size_t)k));
+  CK(dalloc(&S.lam, (size_t)k));
+  CK(dalloc(&S.rho, (size_t)k));
+  CK(dalloc(&S.mode, (size_t)k));
+  CK(dalloc(&S.Cpi, (size_t)k * k));
+  CK(dalloc(&S.Dold, (size_t)qc * k));
+  CK(dalloc(&S.Dn, (size_t)qc * k));
+  CK(dalloc(&S.Rini, (size_t)qc * k));
+  CK(dalloc(&S.acc, (size_t)3 * k));
+  CK(dalloc(&S.last, (size_t)3 * k));
+  CK(dalloc(&S.mn, (size_t)k));
+  CK(dalloc(&S.mx, (size_t)k));
+  CK(dalloc(&S.rho_acc, (size_t)2 * k));
+  CK(dalloc(&S.conv, 1));
+  CK(cudaMallocHost((void**)&h->sh_conv_host, sizeof(int)));
+  h->sh_alloc = true;
+  return SOMF_OK;
+}
+
+// Projection of the local rows of D onto C with thresholds over all ranks
+// (somf_set_components on a row shard).
+static somf_status project_sharded(somf_ctx* h) {
+  if (somf_status s = shard_alloc(h)) return s;
+  const somf_config& c = h->cfg;
+  const int k = c.k;
+  const double a = 1.0 - c.mu, b = c.mu;
+  ShState& S = h->sh;
+  k_proj_init<<<1, 256, 0, h->st>>>(S, k);
+  CKL();
+  bool conv = false;
+  for (int it = 0; it < 200 && !conv; ++it) {
+    k_proj_stats<<<k, 256, 0, h->st>>>(S, h->D, h->rows, h->kp, a, c.pos_dict);
+    CKL();
+    if (somf_status s = reduce(h, S.acc, 3 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
+    if (somf_status s = reduce(h, S.mn, k, SOMF_DT_I32, SOMF_OP_MIN)) return s;
+    if (somf_status s = reduce(h, S.mx, k, SOMF_DT_I32, SOMF_OP_MAX)) return s;
+    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b);
+    CKL();
+    CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    conv = *h->sh_conv_host != 0;
+  }
+  if (!conv) {
+    set_err(h, "sharded projection of D0 did not converge");
+    return SOMF_E_CUDA;
+  }
+  k_proj_apply<<<(unsigned)std::max<int64_t>(1, ceil_div(h->rows * k, 256)), 256, 0, h->st>>>(
+      S, h->D, h->rows, h->kp, k, a, b, c.pos_dict, h->nslack);
+  CKL();
+  return SOMF_OK;
+}
+
+// Alg. 4 on a row shard (bcd_shard.cuh): one kernel per round, the caller's
+// reducer between them, a host read of the convergence flag per round.
+static somf_status bcd_sharded(somf_ctx* h) {
+  const somf_config& c = h->cfg;
+  const int k = c.k;
+  const double a = 1.0 - c.mu, b = c.mu;
+  const int64_t qc = std::max<int64_t>(h->q_cap, 1);
+  ShState& S = h->sh;
+  if (somf_status s = shard_alloc(h)) return s;
+  k_shard_init<<<1, 256, 0, h->st>>>(S, h->perm, h->C64, h->C32, h->lam_ws, h->nslack, k, a, b, c.pos_dict);
+  CKL();
+  const int rb = 128;
+  k_shard_setup<<<(unsigned)ceil_div(qc, rb), rb, 0, h->st>>>(S, h->idx, h->q_dev, h->D, h->Bbar, k, h->kp);
+  CKL();
+  if (somf_status s = reduce(h, S.rho_acc, 2 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
+  k_shard_rho<<<1, 256, 0, h->st>>>(S, k, a, b);
+  CKL();
+  const int rr = k <= 96 ? 128 : 64;
+  const size_t smem = (size_t)2 * rr * (k + 1) * sizeof(float);
+  CK(cudaFuncSetAttribute(k_shard_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int64_t rounds = 0;
+  const int max_rounds = 3 * k + 20;
+  for (int r = 0; r < max_rounds; ++r) {
+    k_shard_round<<<(unsigned)ceil_div(qc, rr), rr, smem, h->st>>>(S, h->q_dev, k, a);
+    CKL();
+    if (somf_status s = reduce(h, S.acc, 3 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
+    if (somf_status s = reduce(h, S.mn, k, SOMF_DT_I32, SOMF_OP_MIN)) return s;
+    if (somf_status s = reduce(h, S.mx, k, SOMF_DT_I32, SOMF_OP_MAX)) return s;
+    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b);
+    CKL();
+    CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    ++rounds;
+    if (*h->sh_conv_host) break;
+  }
+  const bool capped = !*h->sh_conv_host;
+  k_shard_finish<<<(unsigned)ceil_div(qc, rb), rb, 0, h->st>>>(S, h->idx, h->q_dev, h->D, k, h->kp, a, b,
+                                                               h->nslack, h->lam_ws);
+  CKL();
+  k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->nred_dev, rounds + 1);
+  CKL();
+  h->launches[SOMF_PH_BCD] += 4 + 2 * rounds;
+  if (capped) {
+    set_err(h, "projection threshold rounds hit their cap (%d)", max_rounds);
+    return SOMF_E_CUDA;
+  }
+  return SOMF_OK;
+}
+
 __global__ void k_init_accmm(unsigned* mm, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) { mm[2 * i] = 0xffffffffu; mm[2 * i + 1] = 0u; }
@@ -657,8 +785,9 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   h->ntiles = (int)ceil_div(((c.row_hi - 1) >> 2) - (c.row_lo >> 2) + 1, kMaskThreads);
   A(dalloc(&h->tile_counts, (size_t)h->ntiles));
   A(dalloc(&h->perm, (size_t)k));
-  A(dalloc(&h->G64, (size_t)k * k));
-  A(dalloc(&h->beta64, (size_t)k * c.eta));
+  // [beta | G] contiguous: one allreduce when row-sharded
+  A(dalloc(&h->beta64, (size_t)k * c.eta + (size_t)k * k));
+  h->G64 = h->beta64 + (size_t)k * c.eta;
   A(dalloc(&h->A64, (size_t)k * c.eta));
   A(dalloc(&h->A32, (size_t)k * c.eta));
   A(dalloc(&h->AT32, (size_t)c.eta * ((k + 3) & ~3)));
@@ -727,12 +856,20 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
   if (!h) return SOMF_E_ARG;
   void* ptrs[] = {h->D, h->Bbar, h->C64, h->C32, h->nslack, h->t_dev, h->w_dev, h->q_dev,
                   h->nred_dev, h->err_dev, h->sweeps_dev, h->idx, h->tile_counts, h->perm,
-                  h->partial, h->G64, h->beta64, h->A64, h->A32, h->red, h->bar, h->Ge,
+                  h->partial, h->beta64, h->A64, h->A32, h->red, h->bar,
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
                   h->lam_ws, h->nt_acc, h->nt_accmm, h->bcd_prof, h->cpart, h->AT32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (h->sh_alloc) {
+    void* sp[] = {h->sh.jmap, h->sh.pinv, h->sh.invc, h->sh.vlo, h->sh.thf, h->sh.scf, h->sh.lam, h->sh.rho,
+                  h->sh.mode, h->sh.Cpi, h->sh.Dold, h->sh.Dn, h->sh.Rini, h->sh.acc, h->sh.last, h->sh.mn,
+                  h->sh.mx, h->sh.rho_acc, h->sh.conv};
+    for (void* p : sp)
+      if (p) cudaFree(p);
+    cudaFreeHost(h->sh_conv_host);
+  }
   for (auto& e : h->evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   delete h;
@@ -748,9 +885,13 @@ SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int6
   CK(cudaMemsetAsync(h->D, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
   CK(cudaMemcpy2DAsync(h->D, h->kp * sizeof(float), src, ld * sizeof(float), k * sizeof(float),
                        h->rows, cudaMemcpyDefault, h->st));
-  k_project_columns<<<k, kBcdThreads, 0, h->st>>>(h->D, h->rows, h->kp, nullptr, 1.0, 1.0 - h->cfg.mu,
-                                                  h->cfg.mu, h->cfg.pos_dict, h->D, h->nslack);
-  CKL();
+  if (h->reducer) {
+    if (somf_status s = project_sharded(h)) return s;
+  } else {
+    k_project_columns<<<k, kBcdThreads, 0, h->st>>>(h->D, h->rows, h->kp, nullptr, 1.0, 1.0 - h->cfg.mu,
+                                                    h->cfg.mu, h->cfg.pos_dict, h->D, h->nslack);
+    CKL();
+  }
   CK(cudaMemsetAsync(h->Bbar, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
   CK(cudaMemsetAsync(h->C64, 0, (size_t)k * k * sizeof(double), h->st));
   CK(cudaMemsetAsync(h->C32, 0, (size_t)k * k * sizeof(float), h->st));
@@ -827,6 +968,8 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     PhaseScope ps(h, SOMF_PH_CONTRACT);                                      // Eq. (a)
     if (somf_status s = launch_contract(h, true, compact, h->q_dev, q_est, Xd, ld, eta, c.r, h->beta64, h->G64))
       return s;
+    if (somf_status s = reduce(h, h->beta64, (int64_t)k * eta + (int64_t)k * k, SOMF_DT_F64, SOMF_OP_SUM))
+      return s;
     h->launches[SOMF_PH_CONTRACT] += 2;
   }
   {
@@ -872,7 +1015,9 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
-    if (h->nt_fn) {
+    if (h->reducer) {
+      if (somf_status s = bcd_sharded(h)) return s;
+    } else if (h->nt_fn) {
       NtArgs na{};
       na.idx = h->idx;
       na.q_dev = h->q_dev;
@@ -1000,12 +1145,12 @@ SOMF_EXPORT somf_status somf_get_codes(somf_handle h, float* A_out) {
 
 static somf_status ensure_eval(somf_ctx* h, int64_t m) {
   if (m <= h->eval_cap) return SOMF_OK;
-  void* ps[] = {h->Ge, h->betae, h->Ae64, h->Ae32, h->colsq, h->objd};
+  void* ps[] = {h->betae, h->Ae64, h->Ae32, h->colsq, h->objd};
   for (void* p : ps)
     if (p) CK(cudaFree(p));
   const int k = h->cfg.k;
-  CK(dalloc(&h->Ge, (size_t)k * k));
-  CK(dalloc(&h->betae, (size_t)k * m));
+  CK(dalloc(&h->betae, (size_t)k * m + (size_t)k * k));
+  h->Ge = h->betae + (size_t)k * m;
   CK(dalloc(&h->Ae64, (size_t)k * m));
   CK(dalloc(&h->Ae32, (size_t)k * m));
   CK(dalloc(&h->colsq, (size_t)m));
@@ -1022,6 +1167,9 @@ static somf_status eval_codes(somf_ctx* h, const float* X, int64_t ld, int64_t m
   k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
   CKL();
   if (somf_status s = launch_contract(h, false, false, h->qfull_dev, h->rows, X, ld, (int)m, 1.0, h->betae, h->Ge))
+    return s;
+  if (somf_status s = reduce(h, h->betae, (int64_t)h->cfg.k * m + (int64_t)h->cfg.k * h->cfg.k, SOMF_DT_F64,
+                             SOMF_OP_SUM))
     return s;
   return launch_codes(h, h->Ge, h->betae, (int)m, h->cfg.cd_tol * 1e-2, h->Ae64, h->Ae32);
 }
@@ -1046,6 +1194,7 @@ SOMF_EXPORT somf_status somf_objective(somf_handle h, const float* X, int64_t ld
   k_residual<<<dim3(grid_r, (unsigned)ceil_div(m, TN)), kGemmThreads, 0, h->st>>>(
       h->D, h->kp, k, h->rows, (const float*)xs, ld, (int)m, h->Ae32, h->colsq);
   CKL();
+  if (somf_status s = reduce(h, h->colsq, m, SOMF_DT_F64, SOMF_OP_SUM)) return s;
   k_objective_final<<<1, 256, 0, h->st>>>(h->colsq, h->Ae64, k, (int)m, h->cfg.lambda, h->cfg.nu, h->objd);
   CKL();
   CK(cudaMemcpyAsync(obj_out, h->objd, sizeof(double), cudaMemcpyDeviceToHost, h->st));
@@ -1116,6 +1265,13 @@ SOMF_EXPORT somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* 
   if (w) CK(cudaMemcpyAsync(w, h->w_dev, sizeof(double), cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
   return check_flags(h);
+}
+
+SOMF_EXPORT somf_status somf_set_reducer(somf_handle h, somf_reduce_fn fn, void* user) {
+  if (!h) return SOMF_E_ARG;
+  h->reducer = fn;
+  h->reducer_user = user;
+  return SOMF_OK;
 }
 
 SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {

@@ -53,6 +53,30 @@ def _stream_ptr(stream) -> C.c_void_p:
 B_MODES = {"masked": 0, "unbiased": 1, "full": 2}
 
 
+class _CudaArray:
+    """Zero-copy view of a device buffer (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 3}
+
+
+def device_view(ptr: int, n: int, dtype: int, device) -> torch.Tensor:
+    """torch view of `n` float64 (dtype 0) or int32 (dtype 1) values at a device pointer."""
+    return torch.as_tensor(_CudaArray(ptr, n, "<f8" if dtype == _lib.DT_F64 else "<i4"), device=device)
+
+
+def dist_reducer(group=None):
+    """Reducer over a torch.distributed process group (NCCL on GPUs, gloo on
+    CPU tensors): the allreduce of the row-sharded step (somf_set_reducer)."""
+    import torch.distributed as dist
+    ops = {_lib.OP_SUM: dist.ReduceOp.SUM, _lib.OP_MIN: dist.ReduceOp.MIN, _lib.OP_MAX: dist.ReduceOp.MAX}
+
+    def reduce(buf: torch.Tensor, op: int):
+        dist.all_reduce(buf, op=ops[op], group=group)
+    return reduce
+
+
 class Somf:
     """One SOMF learner (a handle of the C ABI) owning rows [row_lo, row_hi)."""
 
@@ -201,6 +225,31 @@ class Somf:
         out["ridge"] = dict(zip(("load", "factor", "solve", "cbar_partial"), v[72:76].tolist()))
         out["setup_split"] = dict(zip(("params", "gather", "permute"), v[76:79].tolist()))
         return out
+
+    def set_reducer(self, fn):
+        """Row sharding: fn(buf, op) combines the tensor `buf` (a zero-copy view
+        of the handle's device buffer) over the ranks in place, op in
+        _lib.OP_SUM / OP_MIN / OP_MAX, on the current stream (the handle's).
+        fn=None restores the single-GPU path."""
+        if fn is None:
+            self._reducer_cb = None
+            _check(lib().somf_set_reducer(self._h, None, None), self._h)
+            return
+        dev = self.device
+
+        def cb(user, buf, count, dtype, op, stream):
+            try:
+                t = device_view(buf, count, dtype, dev)
+                s = torch.cuda.ExternalStream(stream, device=dev) if stream else torch.cuda.default_stream(dev)
+                with torch.cuda.stream(s):
+                    fn(t, op)
+                return 0
+            except Exception:          # noqa: BLE001 -- reported to the C side as a failed collective
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._reducer_cb = _lib.REDUCE_FN(cb)
+        _check(lib().somf_set_reducer(self._h, self._reducer_cb, None), self._h)
 
     @property
     def bcd_variant(self) -> str:

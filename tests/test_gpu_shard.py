@@ -1,0 +1,121 @@
+"""Row-sharded SOMF step through the C ABI on ONE GPU: two
+handles own the two halves of the rows, run concurrently from two host threads
+on two CUDA streams, and their reducer combines the exchanged buffers through
+host-side barriers (no kernel ever waits on another rank).  The sharded result
+must equal the single-handle result and the float64 oracle.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import synth  # noqa: E402
+from oracle.somf import SomfOracle, OracleConfig  # noqa: E402
+
+
+class PairReducer:
+    """In-process allreduce for W ranks living in W threads of one process."""
+
+    def __init__(self, world):
+        self.world = world
+        self.bar = threading.Barrier(world, timeout=60)      # a schedule bug raises, never hangs
+        self.slots = [None] * world
+
+    def for_rank(self, rank):
+        from paper_1701_05363_b200 import _lib
+
+        def reduce(buf, op):
+            torch.cuda.current_stream().synchronize()          # my contribution is final
+            self.slots[rank] = buf
+            self.bar.wait()
+            res = self.slots[0].clone()
+            for i in range(1, self.world):
+                o = self.slots[i]
+                if op == _lib.OP_SUM:
+                    res = res + o
+                elif op == _lib.OP_MIN:
+                    res = torch.minimum(res, o)
+                else:
+                    res = torch.maximum(res, o)
+            torch.cuda.current_stream().synchronize()
+            self.bar.wait()                                      # everybody has read every slot
+            buf.copy_(res)
+            torch.cuda.current_stream().synchronize()
+        return reduce
+
+
+def _data(p, n, seed=0):
+    X, _, _ = synth.tiny_dictionary_learning(p=p, n=n, seed=seed)
+    return np.asarray(X, np.float32).astype(np.float64)
+
+
+def _cuda(a):
+    return torch.tensor(np.asarray(a, np.float32), device="cuda")
+
+
+@pytest.mark.parametrize("k,eta,mu,r", [(16, 24, 0.0, 4.0), (40, 32, 1.0, 3.0), (24, 20, 0.5, 6.0)])
+def test_two_shards_match_single_gpu_and_oracle(k, eta, mu, r):
+    import paper_1701_05363_b200 as somf
+    p, steps, world = 3001, 6, 2
+    kw = dict(lam=0.05, nu=1.0, mu=mu, r=r, u=0.917, seed=11)
+    X = _data(p, k + steps * eta + 100)
+    Xte = X[:, -100:]
+    bounds = [p * i // world for i in range(world + 1)]
+    streams = [torch.cuda.Stream() for _ in range(world)]
+    red = PairReducer(world)
+    shards = []
+    for i in range(world):
+        with torch.cuda.stream(streams[i]):
+            h = somf.Somf(p, k, eta, row_lo=bounds[i], row_hi=bounds[i + 1], stream=streams[i], **kw)
+            h.set_reducer(red.for_rank(i))
+        shards.append(h)
+    single = somf.Somf(p, k, eta, **kw)
+    single.set_components(_cuda(X[:, :k]))
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, **kw))
+    ora.set_components(X[:, :k])
+    errors = []
+    objs = [None] * world
+
+    def run(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                # collective calls (every rank, same order): the projection of D0 too
+                shards[i].set_components(_cuda(X[bounds[i]:bounds[i + 1], :k]))
+                for t in range(steps):
+                    xb = _cuda(X[bounds[i]:bounds[i + 1], k + t * eta:k + (t + 1) * eta])
+                    shards[i].partial_fit(xb)
+                objs[i] = shards[i].objective(_cuda(Xte[bounds[i]:bounds[i + 1]]))
+        except Exception as e:      # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(world)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=300)
+    assert not any(x.is_alive() for x in th), "sharded step hung"
+    assert not errors, errors
+    for t in range(steps):
+        single.partial_fit(_cuda(X[:, k + t * eta:k + (t + 1) * eta]))
+        ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
+    torch.cuda.synchronize()
+    st = [h.get_state() for h in shards]
+    s1 = single.get_state()
+    D = np.concatenate([s["D"] for s in st])
+    B = np.concatenate([s["Bbar"] for s in st])
+
+    def rel(a, b):
+        return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
+    # replicated state identical on both ranks (same reduced sums, same updates)
+    np.testing.assert_array_equal(st[0]["Cbar"], st[1]["Cbar"])
+    np.testing.assert_array_equal(st[0]["n"], st[1]["n"])
+    assert rel(D, s1["D"]) < 1e-5 and rel(B, s1["Bbar"]) < 1e-5
+    assert rel(D, ora.D) < 1e-4 and rel(B, ora.Bbar) < 1e-4 and rel(st[0]["Cbar"], ora.Cbar) < 1e-4
+    np.testing.assert_allclose(st[0]["n"], ora.n, rtol=0, atol=1e-5)
+    f_ref = ora.objective(Xte)
+    assert objs[0] == objs[1]
+    assert abs(objs[0] - f_ref) <= 1e-3 * abs(f_ref)
