@@ -22,6 +22,7 @@ namespace somf {
 
 constexpr int kRcThreads = 256;
 constexpr int kRcMaxK = 160;
+constexpr int kRcInvKPL = 0;      // k <= 32 kRcInvKPL: explicit-inverse solve (measured slower on B200 for k = 70: off)
 
 // 1/sqrt(d) in fp64: fp32 MUFU estimate + two Newton steps (rel. error ~1e-16),
 // ~3x shorter latency than sqrt() followed by a division
@@ -57,6 +58,11 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       t_mark = now_;                                                      \
     }                                                                     \
   } while (0)
+  // the factorisation and the solves run on K4 = k rounded up to 4 (identity
+  // padding, zero right-hand sides): every 4-column panel / 4-row block is
+  // full, so the loops are branch-free and the loads can be hoisted
+  const int kr = k;
+  k = (k + 3) & ~3;
   const int ld = k + 1;
   double* M = rc_smem;                              // k x ld, lower triangle
   double* Y = rc_smem + (size_t)k * ld;             // 8 x k
@@ -65,14 +71,14 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
 #pragma unroll 4
   for (int e = tid; e < k * k; e += kRcThreads) {
     const int i = e / k, j = e % k;
-    const double g = G[e];
-    if (j <= i) M[i * ld + j] = g + (i == j ? lam : 0.0);
+    const double g = (i < kr && j < kr) ? G[(int64_t)i * kr + j] + (i == j ? lam : 0.0) : (i == j ? 1.0 : 0.0);
+    if (j <= i) M[i * ld + j] = g;
   }
   __syncthreads();
   RC_MARK(0);
   bool bad = false;
   for (int p0 = 0; p0 < k; p0 += 4) {
-    const int pb = min(4, k - p0);
+    constexpr int pb = 4;
     // 4 x 4 diagonal block, factorised in registers by every thread
     double Ld[4][4];
 #pragma unroll
@@ -131,20 +137,37 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         if (tid == 4 * a + c && a < pb && c <= a) M[(p0 + a) * ld + p0 + c] = (a == c) ? inv[a] : Ld[a][c];
-    // rank-4 trailing update: M[i][l] -= sum_c L[i][p0+c] L[l][p0+c], p0+pb <= l <= i
-    const int r0 = p0 + pb, n = k - r0;
-    for (int ii = ty; ii < n; ii += 16) {
-      const int i = r0 + ii;
-      double li[4];
+    // rank-4 trailing update: M[i][l] -= sum_c L[i][p0+c] L[l][p0+c], p0+pb <= l <= i.
+    // Thread (ty, tx) owns rows r0+ty+16a and columns r0+tx+16b; the panel
+    // values of its columns are loaded once into registers (NS = KMAX/16 slots).
+    {
+      constexpr int NS = (32 * KPL + 15) / 16;
+      const int r0 = p0 + pb, n = k - r0;
+      double lj[NS][4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) li[c] = c < pb ? M[i * ld + p0 + c] : 0.0;
-      for (int ll = tx; ll <= ii; ll += 16) {
-        const int l = r0 + ll;
-        double v = M[i * ld + l];
+      for (int bb = 0; bb < NS; ++bb) {
+        const int ll = tx + 16 * bb;
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (c < pb) v -= li[c] * M[l * ld + p0 + c];
-        M[i * ld + l] = v;
+        for (int c = 0; c < 4; ++c) lj[bb][c] = (ll < n && c < pb) ? M[(r0 + ll) * ld + p0 + c] : 0.0;
+      }
+      for (int ii = ty; ii < n; ii += 16) {
+        const int i = r0 + ii;
+        double li[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) li[c] = c < pb ? M[i * ld + p0 + c] : 0.0;
+#pragma unroll
+        for (int bb = 0; bb < NS; ++bb) {
+          const int ll = tx + 16 * bb;
+          if (ll <= ii) {
+            double* mp = M + i * ld + r0 + ll;
+            double v = *mp;
+            v -= li[0] * lj[bb][0];
+            v -= li[1] * lj[bb][1];
+            v -= li[2] * lj[bb][2];
+            v -= li[3] * lj[bb][3];
+            *mp = v;
+          }
+        }
       }
     }
     __syncthreads();
@@ -152,6 +175,85 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
   if (bad && err) atomicExch(err, 1);
   RC_MARK(1);
 
+  if constexpr (KPL <= kRcInvKPL) {
+    // ---- explicit inverse W = L^-1 (column j by thread j), then alpha = W^T (W beta):
+    // two triangular mat-vecs per right-hand side, no serial substitution chain
+    double* W = Y + (size_t)8 * k;                    // k x ld, lower triangle
+    for (int j = tid; j < k; j += kRcThreads) {
+      W[j * ld + j] = M[j * ld + j];
+      for (int i = j + 1; i < k; ++i) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int l = j;
+        for (; l + 3 < i; l += 4) {
+          a0 = fma(M[i * ld + l], W[l * ld + j], a0);
+          a1 = fma(M[i * ld + l + 1], W[(l + 1) * ld + j], a1);
+          a2 = fma(M[i * ld + l + 2], W[(l + 2) * ld + j], a2);
+          a3 = fma(M[i * ld + l + 3], W[(l + 3) * ld + j], a3);
+        }
+        for (; l < i; ++l) a0 = fma(M[i * ld + l], W[l * ld + j], a0);
+        W[i * ld + j] = -M[i * ld + i] * ((a0 + a1) + (a2 + a3));
+      }
+    }
+    __syncthreads();
+    RC_MARK(7);       // prof slot 79: the inverse
+    double* Yw = Y + (size_t)wid * k;
+    for (int s0 = blockIdx.x * 8; s0 < m; s0 += gridDim.x * 8) {
+      const int s = s0 + wid;
+      for (int i = lane; i < k; i += 32) Yw[i] = (s < m && i < kr) ? beta[(int64_t)i * m + s] : 0.0;
+      __syncwarp();
+      double y[KPL];
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {                 // y = W beta (rows i >= l)
+        const int i = lane + 32 * c;
+        double a0 = 0.0, a1 = 0.0;
+        if (i < k) {
+          int l = 0;
+          for (; l + 1 <= i; l += 2) {
+            a0 = fma(W[i * ld + l], Yw[l], a0);
+            a1 = fma(W[i * ld + l + 1], Yw[l + 1], a1);
+          }
+          if (l <= i) a0 = fma(W[i * ld + l], Yw[l], a0);
+        }
+        y[c] = a0 + a1;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        const int i = lane + 32 * c;
+        if (i < k) Yw[i] = y[c];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {                 // alpha = W^T y (rows l >= i)
+        const int i = lane + 32 * c;
+        double a0 = 0.0, a1 = 0.0;
+        if (i < k) {
+          int l = i;
+          for (; l + 1 < k; l += 2) {
+            a0 = fma(W[l * ld + i], Yw[l], a0);
+            a1 = fma(W[(l + 1) * ld + i], Yw[l + 1], a1);
+          }
+          if (l < k) a0 = fma(W[l * ld + i], Yw[l], a0);
+        }
+        y[c] = a0 + a1;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int c = 0; c < KPL; ++c) {
+        const int i = lane + 32 * c;
+        if (i < k) {
+          const double v = s < m ? y[c] : 0.0;
+          Yw[i] = v;
+          if (s < m && i < kr) {
+            A64[(int64_t)i * m + s] = v;
+            A32[(int64_t)i * m + s] = (float)v;
+            if (AT32) AT32[(int64_t)s * ldt + i] = (float)v;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
   // ---- substitutions: one warp per right-hand side, 4 rows per shuffle round ----
   for (int s0 = blockIdx.x * 8; s0 < m; s0 += gridDim.x * 8) {
     const int s = s0 + wid;
@@ -159,11 +261,12 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
 #pragma unroll
     for (int c = 0; c < KPL; ++c) {
       const int i = lane + 32 * c;
-      y[c] = (s < m && i < k) ? beta[(int64_t)i * m + s] : 0.0;
+      y[c] = (s < m && i < kr) ? beta[(int64_t)i * m + s] : 0.0;
     }
     // L y = b
     for (int jb = 0; jb < k; jb += 4) {
-      const int pb = min(4, k - jb), cs = jb >> 5, lb = jb & 31;
+      constexpr int pb = 4;
+      const int cs = jb >> 5, lb = jb & 31;
       const double own = rc_pick<KPL>(y, cs);
       double z[4];
 #pragma unroll
@@ -196,7 +299,8 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
     }
     // L^T x = y
     for (int jb = ((k - 1) / 4) * 4; jb >= 0; jb -= 4) {
-      const int pb = min(4, k - jb), cs = jb >> 5, lb = jb & 31;
+      constexpr int pb = 4;
+      const int cs = jb >> 5, lb = jb & 31;
       const double own = rc_pick<KPL>(y, cs);
       double z[4];
 #pragma unroll
@@ -234,7 +338,7 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       if (i < k) {
         const double v = s < m ? y[c] : 0.0;
         Yw[i] = v;
-        if (s < m) {
+        if (s < m && i < kr) {
           A64[(int64_t)i * m + s] = v;
           A32[(int64_t)i * m + s] = (float)v;
           if (AT32) AT32[(int64_t)s * ldt + i] = (float)v;     // codes transposed (eta x kp) for bbar
@@ -242,12 +346,13 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       }
     }
   }
+  }
   RC_MARK(2);
   if (cpart) {
     __syncthreads();
-    double* out = cpart + (size_t)blockIdx.x * k * k;
-    for (int e = tid; e < k * k; e += kRcThreads) {
-      const int a = e / k, b = e % k;
+    double* out = cpart + (size_t)blockIdx.x * kr * kr;
+    for (int e = tid; e < kr * kr; e += kRcThreads) {
+      const int a = e / kr, b = e % kr;
       double acc = 0.0;
 #pragma unroll
       for (int w = 0; w < 8; ++w) acc += Y[w * k + a] * Y[w * k + b];
