@@ -93,6 +93,65 @@ k_mask_scatter(uint64_t seed, const int64_t* __restrict__ t_dev, int64_t row_lo,
   }
 }
 
+// Alg. 4's atom order by one CTA: words drawn in parallel, swaps by thread 0.
+// sh: 2k words of shared memory.
+__device__ __forceinline__ void atom_perm_cta(uint64_t seed, uint64_t t, int k, int cyclic,
+                                              int32_t* __restrict__ perm, uint32_t* sh) {
+  uint32_t* words = sh;                       // k words
+  int32_t* pi = (int32_t*)(sh + k);           // k entries
+  for (int i = threadIdx.x; i < k; i += blockDim.x) pi[i] = i;
+  if (!cyclic) {
+    for (int b = threadIdx.x; b * 4 < k - 1; b += blockDim.x) {
+      const U4 w = philox4x32_10(U4{(uint32_t)b, (uint32_t)t, kStreamPerm, 0u}, seed);
+      for (int l = 0; l < 4; ++l)
+        if (b * 4 + l < k - 1) words[b * 4 + l] = u4_word(w, l);
+    }
+  }
+  __syncthreads();
+  if (!cyclic && threadIdx.x == 0) {
+    for (int w = 0; w < k - 1; ++w) {
+      const int i = k - 1 - w;
+      const int j = (int)(((uint64_t)words[w] * (uint64_t)(i + 1)) >> 32);
+      const int32_t tmp = pi[i];
+      pi[i] = pi[j];
+      pi[j] = tmp;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < k; i += blockDim.x) perm[i] = pi[i];
+}
+
+// One launch for the start of an iteration: CTAs 0 .. ntiles-1 count the
+// selected rows of M_t per tile (as k_mask_count); the extra last CTA writes
+// t and w_t = t^-u and draws the atom order (R13).
+// t is passed by value (the host tracks it), so no CTA reads t_dev.
+__global__ void __launch_bounds__(kMaskThreads)
+k_step_mask_count(uint64_t seed, int64_t t, double u, int64_t row_lo, int64_t row_hi, uint64_t T, int ntiles,
+                  int32_t* __restrict__ tile_counts, int64_t* __restrict__ t_dev, double* __restrict__ w_dev,
+                  int k, int cyclic, int32_t* __restrict__ perm) {
+  __shared__ uint32_t sh[2 * 256 + 8];
+  __shared__ int wsum[kMaskThreads / 32];
+  if ((int)blockIdx.x == ntiles) {
+    if (threadIdx.x == 0) {
+      *t_dev = t;
+      *w_dev = pow((double)t, -u);
+    }
+    atom_perm_cta(seed, (uint64_t)t, k, cyclic, perm, sh);
+    return;
+  }
+  const int64_t b0 = row_lo >> 2, b1 = (row_hi - 1) >> 2;
+  const int64_t blk = b0 + (int64_t)blockIdx.x * kMaskThreads + threadIdx.x;
+  const int c = blk <= b1 ? __popc(mask_bits(seed, (uint64_t)t, blk, row_lo, row_hi, T)) : 0;
+  const int s = warp_sum(c);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int i = 0; i < kMaskThreads / 32; ++i) tot += wsum[i];
+    tile_counts[blockIdx.x] = tot;
+  }
+}
+
 // Alg. 4's atom order, one warp: words drawn in parallel, swaps by lane 0.
 __global__ void k_atom_perm(uint64_t seed, const int64_t* __restrict__ t_dev, int k, int cyclic,
                             int32_t* __restrict__ perm) {

@@ -938,21 +938,22 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   const int64_t q_est = (int64_t)std::ceil(h->rows / c.r) + 64;
   {
     PhaseScope ps(h, SOMF_PH_MASK);
-    k_step_begin<<<1, 1, 0, h->st>>>(h->t_dev, h->w_dev, c.u);             // t <- t+1, w_t
+    // t <- t+1, w_t, atom order and (unless drawn ahead by somf_next_mask) the
+    // tile counts of M_t in one launch; the scatter of the index list in a second
+    h->t_host += 1;
+    const int nt = h->mask_ready ? 0 : h->ntiles;
+    k_step_mask_count<<<nt + 1, kMaskThreads, 0, h->st>>>(c.seed, h->t_host, c.u, c.row_lo, c.row_hi, h->T, nt,
+                                                          h->tile_counts, h->t_dev, h->w_dev, k, c.perm_cyclic,
+                                                          h->perm);
     CKL();
     h->launches[SOMF_PH_MASK] += 1;
-    h->t_host += 1;
     if (!h->mask_ready) {                                                    // M_t (Eq. mt)
-      if (somf_status s = launch_mask(h, h->t_dev, c.row_lo, c.row_lo, c.row_hi, h->T, h->idx,
-                                      h->tile_counts, h->q_dev, h->st))
-        return s;
-      h->launches[SOMF_PH_MASK] += 2;
+      k_mask_scatter<<<h->ntiles, kMaskThreads, 0, h->st>>>(c.seed, h->t_dev, c.row_lo, c.row_hi, h->T,
+                                                            h->tile_counts, c.row_lo, h->idx, h->q_dev);
+      CKL();
+      h->launches[SOMF_PH_MASK] += 1;
     }
     h->mask_ready = false;
-    const size_t smem = (size_t)2 * k * sizeof(uint32_t);                   // Alg. 4 order
-    k_atom_perm<<<1, 32, smem, h->st>>>(c.seed, h->t_dev, k, c.perm_cyclic, h->perm);
-    CKL();
-    h->launches[SOMF_PH_MASK] += 1;
   }
   if (host && !compact && c.b_mode == SOMF_B_MASKED) {
     // the selected rows of a host-resident batch cross the link once
