@@ -3,8 +3,8 @@
 //  k_ridge_codes<KPL> : alpha = (G + lambda I)^-1 beta  (Eq. somf_alpha,
 //                  P:592-596, nu = 1, no positivity), k <= 32 KPL.
 //                  Every CTA factorises G + lambda I redundantly in shared
-//                  memory (fp64 LL^T, right-looking in 4-column panels: the
-//                  4 x 4 diagonal block is factorised in every thread's
+//                  memory (fp64 LL^T, right-looking in 8-column panels: the
+//                  8 x 8 diagonal block is factorised in every thread's
 //                  registers, the panel rows below are solved one row per
 //                  thread, then one rank-4 trailing update over a 16 x 16
 //                  thread grid: 2 barriers per 4 columns).  Then each warp
@@ -22,6 +22,8 @@ namespace somf {
 
 constexpr int kRcThreads = 256;
 constexpr int kRcMaxK = 160;
+constexpr int kRcPW = 4;          // panel width of the factorisation (8 measured slower)
+constexpr int kRcSB = 8;          // block height of the substitutions (8 measured faster than 4); multiple of kRcPW
 constexpr int kRcInvKPL = 0;      // k <= 32 kRcInvKPL: explicit-inverse solve (measured slower on B200 for k = 70: off)
 
 // 1/sqrt(d) in fp64: fp32 MUFU estimate + two Newton steps (rel. error ~1e-16),
@@ -62,7 +64,7 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
   // padding, zero right-hand sides): every 4-column panel / 4-row block is
   // full, so the loops are branch-free and the loads can be hoisted
   const int kr = k;
-  k = (k + 3) & ~3;
+  k = (k + kRcSB - 1) & ~(kRcSB - 1);
   const int ld = k + 1;
   double* M = rc_smem;                              // k x ld, lower triangle
   double* Y = rc_smem + (size_t)k * ld;             // 8 x k
@@ -77,32 +79,32 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
   __syncthreads();
   RC_MARK(0);
   bool bad = false;
-  for (int p0 = 0; p0 < k; p0 += 4) {
-    constexpr int pb = 4;
+  for (int p0 = 0; p0 < k; p0 += kRcPW) {
+    constexpr int pb = kRcPW;
     // 4 x 4 diagonal block, factorised in registers by every thread
-    double Ld[4][4];
+    double Ld[kRcPW][kRcPW];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < kRcPW; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) Ld[a][c] = (a < pb && c <= a) ? M[(p0 + a) * ld + p0 + c] : 0.0;
-    double inv[4];
+      for (int c = 0; c < kRcPW; ++c) Ld[a][c] = (a < pb && c <= a) ? M[(p0 + a) * ld + p0 + c] : 0.0;
+    double inv[kRcPW];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < kRcPW; ++c) {
       if (c < pb) {
         double d = Ld[c][c];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kRcPW; ++u)
           if (u < c) d -= Ld[c][u] * Ld[c][u];
         bad |= !(d > 0.0);
         const double ir = d > 0.0 ? rc_rsqrt(d) : 0.0;
         inv[c] = ir;
         Ld[c][c] = d * ir;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < kRcPW; ++a) {
           if (a > c && a < pb) {
             double v = Ld[a][c];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < kRcPW; ++u)
               if (u < c) v -= Ld[a][u] * Ld[c][u];
             Ld[a][c] = v * inv[c];
           }
@@ -113,13 +115,13 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
     }
     // panel rows below: L[i][p0..p0+pb) = M[i][p0..] L_D^-T  (one row per thread)
     for (int i = p0 + pb + tid; i < k; i += kRcThreads) {
-      double x[4];
+      double x[kRcPW];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < kRcPW; ++c) {
         if (c < pb) {
           double v = M[i * ld + p0 + c];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < kRcPW; ++u)
             if (u < c) v -= x[u] * Ld[c][u];
           x[c] = v * inv[c];
         } else {
@@ -127,44 +129,42 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
         }
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < kRcPW; ++c)
         if (c < pb) M[i * ld + p0 + c] = x[c];
     }
     __syncthreads();                                // panel reads of the block done
     // (static register indices only: a dynamic index would put Ld in local memory)
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < kRcPW; ++a)
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (tid == 4 * a + c && a < pb && c <= a) M[(p0 + a) * ld + p0 + c] = (a == c) ? inv[a] : Ld[a][c];
+      for (int c = 0; c < kRcPW; ++c)
+        if (tid == kRcPW * a + c && a < pb && c <= a) M[(p0 + a) * ld + p0 + c] = (a == c) ? inv[a] : Ld[a][c];
     // rank-4 trailing update: M[i][l] -= sum_c L[i][p0+c] L[l][p0+c], p0+pb <= l <= i.
     // Thread (ty, tx) owns rows r0+ty+16a and columns r0+tx+16b; the panel
     // values of its columns are loaded once into registers (NS = KMAX/16 slots).
     {
       constexpr int NS = (32 * KPL + 15) / 16;
       const int r0 = p0 + pb, n = k - r0;
-      double lj[NS][4];
+      double lj[NS][kRcPW];
 #pragma unroll
       for (int bb = 0; bb < NS; ++bb) {
         const int ll = tx + 16 * bb;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) lj[bb][c] = (ll < n && c < pb) ? M[(r0 + ll) * ld + p0 + c] : 0.0;
+        for (int c = 0; c < kRcPW; ++c) lj[bb][c] = (ll < n && c < pb) ? M[(r0 + ll) * ld + p0 + c] : 0.0;
       }
       for (int ii = ty; ii < n; ii += 16) {
         const int i = r0 + ii;
-        double li[4];
+        double li[kRcPW];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) li[c] = c < pb ? M[i * ld + p0 + c] : 0.0;
+        for (int c = 0; c < kRcPW; ++c) li[c] = c < pb ? M[i * ld + p0 + c] : 0.0;
 #pragma unroll
         for (int bb = 0; bb < NS; ++bb) {
           const int ll = tx + 16 * bb;
           if (ll <= ii) {
             double* mp = M + i * ld + r0 + ll;
             double v = *mp;
-            v -= li[0] * lj[bb][0];
-            v -= li[1] * lj[bb][1];
-            v -= li[2] * lj[bb][2];
-            v -= li[3] * lj[bb][3];
+#pragma unroll
+            for (int c = 0; c < kRcPW; ++c) v -= li[c] * lj[bb][c];
             *mp = v;
           }
         }
@@ -264,19 +264,19 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       y[c] = (s < m && i < kr) ? beta[(int64_t)i * m + s] : 0.0;
     }
     // L y = b
-    for (int jb = 0; jb < k; jb += 4) {
-      constexpr int pb = 4;
+    for (int jb = 0; jb < k; jb += kRcSB) {
+      constexpr int pb = kRcSB;
       const int cs = jb >> 5, lb = jb & 31;
       const double own = rc_pick<KPL>(y, cs);
-      double z[4];
+      double z[kRcSB];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
+      for (int t = 0; t < kRcSB; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < kRcSB; ++t) {
         if (t < pb) {
           double v = z[t];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < kRcSB; ++u)
             if (u < t) v -= M[(jb + t) * ld + jb + u] * z[u];
           z[t] = v * M[(jb + t) * ld + jb + t];
         }
@@ -286,31 +286,31 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
         const int i = lane + 32 * c;
         if (i >= jb && i < jb + pb) {
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
+          for (int t = 0; t < kRcSB; ++t)
             if (i == jb + t) y[c] = z[t];
         } else if (i >= jb + pb && i < k) {
           double v = y[c];
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
+          for (int t = 0; t < kRcSB; ++t)
             if (t < pb) v -= M[i * ld + jb + t] * z[t];
           y[c] = v;
         }
       }
     }
     // L^T x = y
-    for (int jb = ((k - 1) / 4) * 4; jb >= 0; jb -= 4) {
-      constexpr int pb = 4;
+    for (int jb = ((k - 1) / kRcSB) * kRcSB; jb >= 0; jb -= kRcSB) {
+      constexpr int pb = kRcSB;
       const int cs = jb >> 5, lb = jb & 31;
       const double own = rc_pick<KPL>(y, cs);
-      double z[4];
+      double z[kRcSB];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
+      for (int t = 0; t < kRcSB; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
 #pragma unroll
-      for (int t = 3; t >= 0; --t) {
+      for (int t = kRcSB - 1; t >= 0; --t) {
         if (t < pb) {
           double v = z[t];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < kRcSB; ++u)
             if (u > t && u < pb) v -= M[(jb + u) * ld + jb + t] * z[u];
           z[t] = v * M[(jb + t) * ld + jb + t];
         }
@@ -320,12 +320,12 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
         const int i = lane + 32 * c;
         if (i >= jb && i < jb + pb) {
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
+          for (int t = 0; t < kRcSB; ++t)
             if (i == jb + t) y[c] = z[t];
         } else if (i < jb) {
           double v = y[c];
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
+          for (int t = 0; t < kRcSB; ++t)
             if (t < pb) v -= M[(jb + t) * ld + i] * z[t];
           y[c] = v;
         }

@@ -437,7 +437,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
   h->cpart_n = 0;
   if (c.nu == 1.0 && !c.pos_code && k <= kRcMaxK) {
     // ridge closed form (v2): every CTA factorises, 8 right-hand sides per CTA
-    const int k4 = (k + 3) & ~3;
+    const int k4 = (k + kRcSB - 1) & ~(kRcSB - 1);
     const size_t smem = ((size_t)((k4 + 31) / 32 <= kRcInvKPL ? 2 : 1) * k4 * (k4 + 1) + (size_t)8 * k4) *
                         sizeof(double);
     const int g = want_cpart ? (int)ceil_div(m, 8) : (int)std::min<int64_t>(ceil_div(m, 8), 4 * h->nsm);
@@ -447,7 +447,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     }
     double* cp = want_cpart ? h->cpart : nullptr;
     const void* fn = nullptr;
-    switch (((k + 3) & ~3) / 32 + (((k + 3) & ~3) % 32 != 0)) {
+    switch ((k4 + 31) / 32) {
       case 1: fn = (const void*)k_ridge_codes<1>; break;
       case 2: fn = (const void*)k_ridge_codes<2>; break;
       case 3: fn = (const void*)k_ridge_codes<3>; break;
