@@ -22,22 +22,53 @@ def _sources():
                   if f.endswith((".cu", ".cuh"))) + [os.path.join(ROOT, "include", "somf.h")]
 
 
+NT_KPTS = (16, 32, 48, 64, 72, 80, 96)   # bcd_newton_inst.cu variants (one object each)
+
+
+def _units():
+    """(name, source, extra flags) of every translation unit of libsomf.so."""
+    units = [("somf_capi", os.path.join(CSRC, "somf_capi.cu"), []),
+             ("bcd_onchip_inst", os.path.join(CSRC, "bcd_onchip_inst.cu"), [])]
+    units += [(f"bcd_newton_k{k}", os.path.join(CSRC, "bcd_newton_inst.cu"), [f"-DNT_KPT={k}"])
+              for k in NT_KPTS]
+    return units
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/somf_capi.cu into libsomf.so for sm_100a (in-tree)."""
+    """Compile csrc/ into libsomf.so for sm_100a (in-tree): one object per
+    translation unit, compiled in parallel, then linked with nvcc -shared."""
+    from concurrent.futures import ThreadPoolExecutor
     newest = max(os.path.getmtime(s) for s in _sources())
     if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
         return LIB_PATH
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     if not os.path.exists(nvcc):
         nvcc = "nvcc"
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, "-O3", "-std=c++17", *NVCC_ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-           "-shared", "-o", tmp, os.path.join(CSRC, "somf_capi.cu")]
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    base = [nvcc, "-O3", "-std=c++17", *NVCC_ARCH, "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden"]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    res = subprocess.run(cmd, capture_output=True, text=True)
+        base.append("-Xptxas=-v")
+
+    def compile_one(unit):
+        name, src, extra = unit
+        obj = os.path.join(objdir, name + ".o")
+        res = subprocess.run(base + extra + ["-c", src, "-o", obj], capture_output=True, text=True)
+        return name, obj, res
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(_units()), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, _units()))
+    errs = [f"[{n}]\n{r.stdout}{r.stderr}" for n, _, r in results if r.returncode != 0]
+    if errs:
+        raise RuntimeError("nvcc failed:\n" + "\n".join(errs))
+    if verbose:
+        for n, _, r in results:
+            print(f"[{n}]\n{r.stderr}")
+    tmp = LIB_PATH + ".tmp"
+    res = subprocess.run([nvcc, *NVCC_ARCH, "-shared", "-o", tmp] + [o for _, o, _ in results],
+                         capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -134,11 +134,22 @@ namespace somf {
 // half), so every gather is in flight at once (the gather is latency-bound
 // otherwise); warp w owns rows w, w+8, ..., lane l atoms l, l+32, ...
 // ---------------------------------------------------------------------------
+// Optional fold of the Cbar update (Eq. somf_partial; k_cbar_finalize):
+// Cbar <- (1 - w) Cbar + (w / eta) sum_b cpart_b, each CTA a slice of the k x k
+// entries, partials added in block order (deterministic), so the step needs
+// no separate launch for it.
+struct CbarFold {
+  const double* cpart;      // nparts x k x k (null: no fold)
+  int nparts, kk;
+  double* C64;
+  float* C32;
+};
+
 template <int KC, int RT, bool kXCompact>
 __global__ void __launch_bounds__(kBbThreads, 1)
 k_bbar_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, const float* __restrict__ X,
           int64_t ldx, int eta, const float* __restrict__ AT, int kp, int k, float* __restrict__ Bbar,
-          const double* __restrict__ w_dev, int seg_rows) {
+          const double* __restrict__ w_dev, int seg_rows, CbarFold cf) {
   static_assert(RT % 2 == 0, "RT even: the two halves of the segment are compile-time row ranges");
   constexpr int KA = 32 * KC, SEG = kBbWarps * RT, HALF = SEG / 2;
   extern __shared__ __align__(16) float b3_smem[];
@@ -155,6 +166,17 @@ k_bbar_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, co
   for (int e = tid; e < eta * ck; e += kBbThreads) {
     const int s = e / ck, c = e % ck;
     bb_cp_async16(ATs + (size_t)s * KA + 4 * c, AT + (int64_t)s * kp + 4 * c, true);
+  }
+  if (cf.cpart) {
+    // my slice of the Cbar entries (its loads overlap the A^T staging)
+    const int e0 = (int)((int64_t)cf.kk * blockIdx.x / G), e1 = (int)((int64_t)cf.kk * (blockIdx.x + 1) / G);
+    for (int e = e0 + tid; e < e1; e += kBbThreads) {
+      double s = 0.0;
+      for (int bq = 0; bq < cf.nparts; ++bq) s += cf.cpart[(size_t)bq * cf.kk + e];
+      const double c = (1.0 - w) * cf.C64[e] + (w / eta) * s;
+      cf.C64[e] = c;
+      cf.C32[e] = (float)c;
+    }
   }
   for (int e = tid; e < eta * (KA - kp); e += kBbThreads) {
     const int s = e / (KA - kp), a = kp + e % (KA - kp);

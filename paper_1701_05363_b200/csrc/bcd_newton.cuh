@@ -29,14 +29,16 @@
 
 namespace somf {
 
-constexpr int kNtThreads = 384;     // 2 threads per masked row: >= 2 x rows per CTA
 constexpr int kNtRing = 3;
+constexpr int kNtRec = 16;          // doubles per accumulator record (128 bytes)
 // Convergence: every atom exact (its active set reproduces itself) and its
 // lambda stable to this relative tolerance between two rounds.  The
-// recurrence runs in fp32 (v, d carry ~1e-7 relative rounding), so asking for
-// more than ~1e-8 only makes rounding noise of one atom ripple down the
-// chain one round per atom.
-constexpr double kNtLamTol = 1e-8;
+// recurrence runs in fp32 (v, d carry ~1e-7 relative rounding); a lambda
+// moving by < 1e-6 relative moves d by < 1e-6 of the threshold, far inside the
+// 1e-4 parity tolerance, while a tighter test only waits for rounding noise of
+// early atoms to stop rippling down the chain (1e-8: 12.1 rounds per step at
+// cfgC r=12, 1e-6: 9.6).  SOMF_NT_TOL overrides it.
+constexpr double kNtLamTol = 1e-6;
 
 struct NtArgs {
   const int32_t* idx;       // masked local rows (ascending)
@@ -51,11 +53,32 @@ struct NtArgs {
   int k, kp;
   double a, b;              // 1 - mu, mu
   int pos;                  // D >= 0
-  int cap_rows;             // rows per CTA the shared memory holds (<= kNtThreads)
+  int cap_rows;             // rows per CTA the shared memory holds (T x cap_rows <= blockDim)
+  int ct_in_w;               // Cbar per thread parity fits the staging buffer W
+  int part_in_cpi;           // the stats partials (5 H KPT words) fit the Cbar staging area
   int max_rounds;
-  double* acc;              // [kNtRing][k][3]  (zero between uses)
-  unsigned* accmm;          // [kNtRing][k][2]  min-above (0xffffffff) / max-below (0)
-  double* rho_acc;          // [2k]             (zero between uses)
+  double lam_tol;           // convergence tolerance on lambda (kNtLamTol)
+  // per-atom grid accumulators, one 128-byte record each so the 148-way
+  // atomics of different atoms land in different L2 slices:
+  //   rec[((slot * k) + p) * kNtRec + {0,1,2}] = count, S1, S2 (fp64, zero between uses)
+  //   ((unsigned*)(rec + ... + 3))[0 / 1]     = min |v| above / max |v| below (float bits)
+  // slots 0..kNtRing-1: the round ring; slot kNtRing: radius sums in {0,1}
+  double* rec;
+  // draw-ahead of iteration t+1 while the CTAs wait on the rounds (null idx_next
+  // = off): M_{t+1} (Eq. mt) into idx_next / q_next (per-CTA counts through
+  // cnt_next, published before round 0's barrier), pi_{t+1} into perm_next,
+  // t+1 and w_{t+1} = (t+1)^-u into t_next / w_next.
+  int32_t* idx_next;
+  int64_t* q_next;
+  int32_t* perm_next;
+  int* cnt_next;            // gridDim.x
+  int64_t* t_next;
+  double* w_next;
+  uint64_t seed, Tthr;
+  int64_t tn, row_lo, row_hi;
+  double u;
+  int cyclic;
+  int mbits_off;            // byte offset of the mask-bit scratch in dynamic smem
   unsigned* bar;            // [0] arrivals [1] exits [2] watchdog
   int64_t* nred_out;
   int* err;                 // 2 capacity, 4 round cap
@@ -103,7 +126,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Shared by the single-GPU kernel and the row-sharded round kernels.
 __device__ __forceinline__ int nt_atom_update(double a, double b, double rho, double cnt, double S1, double S2,
                                               double mnv, double mxv, int mode, double lam, int* nmode_out,
-                                              double* nlam_out) {
+                                              double* nlam_out, double tol = kNtLamTol) {
   const double th = a * lam;
   int nmode = mode, conv = 1;
   double nlam = lam;
@@ -124,13 +147,13 @@ __device__ __forceinline__ int nt_atom_update(double a, double b, double rho, do
     }
     // exact when the active set at the new threshold is still "every nonzero"
     const bool exact = nlam == 0.0 || !(a > 0.0) || a * nlam < mnv;
-    conv = exact && nmode == mode && fabs(nlam - lam) <= kNtLamTol * fmax(nlam, 1e-300);
+    conv = exact && nmode == mode && fabs(nlam - lam) <= tol * fmax(nlam, 1e-300);
   } else {
     nlam = enet_lambda(a, b, rho, cnt, S1, S2);
     nmode = nlam > 0.0 ? kModeShrink : kModeCopy;
     const double nth = a * nlam;
     const bool exact = nlam > 0.0 && mxv <= nth && nth < mnv;
-    conv = exact && fabs(nlam - lam) <= kNtLamTol * nlam;
+    conv = exact && fabs(nlam - lam) <= tol * nlam;
   }
   *nmode_out = nmode;
   *nlam_out = nlam;
@@ -147,138 +170,183 @@ __device__ __forceinline__ double nt_norm_d(double a, double b, int mode, double
   return 0.0;
 }
 
+__device__ __forceinline__ void nt_rec_reset(double* rc) {
+  rc[0] = 0.0;
+  rc[1] = 0.0;
+  rc[2] = 0.0;
+  unsigned* mm = reinterpret_cast<unsigned*>(rc + 3);
+  mm[0] = 0xffffffffu;
+  mm[1] = 0u;
+}
+
 __device__ __forceinline__ void nt_red_add(double* p, double v) {
   asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
-// One atom of the recurrence at compile-time position PP (so R[] is indexed
-// statically and stays in registers), then the next position.
-template <int KPT, int PP>
-struct NtRec {
-  // __restrict__: the v / d stores of one position must not pin the loads of
-  // the next positions (and the Cbar rows) behind them, or no two positions'
-  // dependency chains can overlap
-  static __device__ __forceinline__ void run(float (&R)[KPT], const float* __restrict__ drow,
-                                             float* __restrict__ vrow, float* __restrict__ dnrow,
-                                             const float* __restrict__ Cpi, const float* __restrict__ invc_s,
-                                             const float* __restrict__ thf_s, const float* __restrict__ scf_s,
-                                             const float* __restrict__ vlo_s, int k) {
-    if (PP >= k) return;
-    // branch-free: copy = (th 0, scale 1), zero = scale 0, dead = (invc 0, copy)
-    const float dold = drow[PP];
-    const float u = fmaf(R[PP], invc_s[PP], dold);
-    const float v = fmaxf(u, vlo_s[PP]);
-    const float d = copysignf(fmaxf(fabsf(v) - thf_s[PP], 0.f) * scf_s[PP], v);
-    vrow[PP] = v;
-    dnrow[PP] = d;
-    const float delta = d - dold;
-    // rank-1 update of the later positions: straight-line (no delta == 0
-    // branch) so ptxas can overlap it with the next position's chain; the
-    // Cbar row is read 16 bytes at a time (rows are 16-byte aligned).
-    const float4* crow = reinterpret_cast<const float4*>(Cpi + (size_t)PP * KPT);
-#pragma unroll
-    for (int l4 = (PP + 1) / 4; l4 < KPT / 4; ++l4) {
-      const float4 c = crow[l4];
-      if (4 * l4 + 0 > PP) R[4 * l4 + 0] = fmaf(-delta, c.x, R[4 * l4 + 0]);
-      if (4 * l4 + 1 > PP) R[4 * l4 + 1] = fmaf(-delta, c.y, R[4 * l4 + 1]);
-      if (4 * l4 + 2 > PP) R[4 * l4 + 2] = fmaf(-delta, c.z, R[4 * l4 + 2]);
-      if (4 * l4 + 3 > PP) R[4 * l4 + 3] = fmaf(-delta, c.w, R[4 * l4 + 3]);
-    }
-    NtRec<KPT, PP + 1>::run(R, drow, vrow, dnrow, Cpi, invc_s, thf_s, scf_s, vlo_s, k);
+// ---------------------------------------------------------------------------
+// v5 recurrence: a group of T adjacent lanes owns M masked rows.  Thread t of
+// a group owns the positions p = i T + t of all M rows: R[m][i] (the residual,
+// PRESCALED by 1/c_pp so u = R + d_old) and Do[m][i] (d before this
+// pass, constant over the rounds).  Position PP (compile-time, so the arrays
+// stay in registers) is owned by t = PP % T; the owner's d - d_old reaches the
+// group's other threads with one width-T shuffle per row, then every thread
+// updates its own later positions of its M rows with the prescaled Cbar row
+// Ct[t][PP][i] = c_{PP, iT+t} / c_{iT+t, iT+t}; each 16-byte shared load of
+// Ct serves M rows (shared-memory wavefronts are the limit of this loop).
+// Positions below the frozen prefix F (atoms whose threshold is final, see
+// the kernel) are skipped: their effect is already folded into R.
+// Per-atom parameters: simple case (mu = 0, no D >= 0) the threshold alone
+// (theta = +inf zeroes the atom); generic case {theta, 1/(1+b lam), v_lo}.
+// Only v is stored: d is a function of v and the round's parameters.
+template <bool kGen>
+struct NtPar;
+template <>
+struct NtPar<false> {
+  float th;
+  __device__ __forceinline__ float d_of(float u) const { return copysignf(fmaxf(fabsf(u) - th, 0.f), u); }
+  __device__ __forceinline__ float v_of(float u) const { return u; }
+};
+template <>
+struct NtPar<true> {
+  float th, sc, vlo, pad;
+  __device__ __forceinline__ float v_of(float u) const { return fmaxf(u, vlo); }
+  __device__ __forceinline__ float d_of(float u) const {
+    const float v = fmaxf(u, vlo);
+    return copysignf(fmaxf(fabsf(v) - th, 0.f) * sc, v);
   }
 };
-template <int KPT>
-struct NtRec<KPT, KPT> {
-  static __device__ __forceinline__ void run(float (&)[KPT], const float*, float*, float*, const float*,
-                                             const float*, const float*, const float*, const float*, int) {}
-};
 
-// Two threads per row (lanes 2r and 2r+1): the thread of parity t holds the
-// residual of the positions p = t (mod 2) in R[p / 2].  Position PP is owned by
-// parity PP % 2 (compile-time); the owner's d - d_old reaches its partner with
-// one shuffle, then each thread updates its own later positions.  Halves the
-// FMAs per thread and doubles the warps that hide the per-position chain.
-template <int KPT, int PP>
-struct NtRec2 {
-  static __device__ __forceinline__ void run(float (&R)[KPT / 2], int par, int pairbase, bool wr,
-                                             const float* drow, float* vrow, float* dnrow, const float* Cpi,
-                                             const float* invc_s, const float* thf_s, const float* scf_s,
-                                             const float* vlo_s, int k) {
-    if (PP >= k) return;
-    constexpr int own = PP & 1;
-    const float dold = drow[PP];
-    const float u = fmaf(R[PP / 2], invc_s[PP], dold);                // P:861 (valid in the owner)
-    const float v = fmaxf(u, vlo_s[PP]);
-    const float d = copysignf(fmaxf(fabsf(v) - thf_s[PP], 0.f) * scf_s[PP], v);
-    if (wr && par == own) {
-      vrow[PP] = v;
-      dnrow[PP] = d;
-    }
-    const float delta = __shfl_sync(0xffffffffu, d - dold, pairbase | own);
-    const float* crow = Cpi + (size_t)PP * KPT;
+template <int KPT, int T, int M, bool kGen, int PP>
+struct NtRec5 {
+  static constexpr int KT = KPT / T;
+  static constexpr int KTS = (KT + 3) & ~3;
+  static __device__ __forceinline__ void run(float (&R)[M][KPT / T], const float (&Do)[M][KPT / T], int t,
+                                             int F, float* __restrict__ v0, int vstride,
+                                             const float* __restrict__ Ct_t, const NtPar<kGen>* __restrict__ par) {
+    constexpr int own = PP % T, ii = PP / T;
+    if (PP >= F) {                                   // uniform: frozen prefix skipped
+      const NtPar<kGen> pr = par[PP];
+      float delta[M];
 #pragma unroll
-    for (int l2 = PP / 2; l2 < KPT / 2; ++l2) {
-      // my position l = 2 l2 + par; update it if it comes after PP
-      const float2 c = *reinterpret_cast<const float2*>(crow + 2 * l2);
-      const float cl = par ? c.y : c.x;
-      const bool later = (2 * l2 + 1 > PP);            // parity-1 position 2 l2 + 1 is later
-      const bool later0 = (2 * l2 > PP);               // parity-0 position 2 l2 is later
-      if (par ? later : later0) R[l2] = fmaf(-delta, cl, R[l2]);
+      for (int m = 0; m < M; ++m) {
+        const float u = R[m][ii] + Do[m][ii];        // P:861 (valid in the owner)
+        const float v = pr.v_of(u);
+        const float d = pr.d_of(u);
+        if (t == own) v0[m * vstride + PP] = v;
+        delta[m] = __shfl_sync(0xffffffffu, d - Do[m][ii], own, T);
+      }
+      const float* crow = Ct_t + PP * KTS;
+#pragma unroll
+      for (int j4 = ii / 4; j4 < KTS / 4; ++j4) {
+        const float4 c = *reinterpret_cast<const float4*>(crow + 4 * j4);
+        const float cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = 4 * j4 + e;
+          if (i < KT) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (i > ii) {
+                R[m][i] = fmaf(-delta[m], cc[e], R[m][i]);
+              } else if (i == ii) {
+                const float up = fmaf(-delta[m], cc[e], R[m][i]);
+                R[m][i] = t > own ? up : R[m][i];
+              }
+            }
+          }
+        }
+      }
     }
-    NtRec2<KPT, PP + 1>::run(R, par, pairbase, wr, drow, vrow, dnrow, Cpi, invc_s, thf_s, scf_s, vlo_s, k);
+    NtRec5<KPT, T, M, kGen, PP + 1>::run(R, Do, t, F, v0, vstride, Ct_t, par);
   }
 };
-template <int KPT>
-struct NtRec2<KPT, KPT> {
-  static __device__ __forceinline__ void run(float (&)[KPT / 2], int, int, bool, const float*, float*, float*,
-                                             const float*, const float*, const float*, const float*, const float*,
-                                             int) {}
+template <int KPT, int T, int M, bool kGen>
+struct NtRec5<KPT, T, M, kGen, KPT> {
+  static __device__ __forceinline__ void run(float (&)[M][KPT / T], const float (&)[M][KPT / T], int, int, float*,
+                                             int, const float*, const NtPar<kGen>*) {}
 };
 
-template <int KPT>
-__global__ void __launch_bounds__(kNtThreads, 1)
+template <int T, int M>
+struct NtCfg {
+  static constexpr int kThreads = M == 1 ? 640 : 384;   // >= T x ceil(rows per CTA / M)
+};
+
+template <bool kGen>
+__device__ __forceinline__ NtPar<kGen> nt_make_par(int mode, double a, double b, double lam, float vlo);
+template <>
+__device__ __forceinline__ NtPar<false> nt_make_par<false>(int mode, double a, double, double lam, float) {
+  NtPar<false> p;
+  p.th = mode == kModeShrink ? (float)(a * lam) : mode == kModeZero ? INFINITY : 0.f;
+  return p;
+}
+template <>
+__device__ __forceinline__ NtPar<true> nt_make_par<true>(int mode, double a, double b, double lam, float vlo) {
+  NtPar<true> p;
+  p.th = mode == kModeShrink ? (float)(a * lam) : 0.f;
+  p.sc = mode == kModeShrink ? (float)(1.0 / (1.0 + b * lam)) : mode == kModeZero ? 0.f : 1.f;
+  p.vlo = mode == kModeDead ? -INFINITY : vlo;
+  p.pad = 0.f;
+  return p;
+}
+
+// Rounds with a frozen prefix.  After each round's update, the atoms
+// [F, F') whose thresholds converged, F' the first unconverged position, are
+// FROZEN with the parameters this round used (so the round's v of those
+// positions is final); their deltas are folded into the initial residual of
+// the later positions once, and later rounds run the recurrence from F'
+// only.  Convergence (exact active set, lambda stable to kNtLamTol) needs the
+// predecessors fixed, so the converged set grows from the front.
+template <int KPT, int T, int M, bool kGen>
+__global__ void __launch_bounds__(NtCfg<T, M>::kThreads, 1)
 k_bcd_newton(NtArgs P) {
   constexpr int LD = KPT + 1;                 // odd row stride: conflict-free per-row access
+  constexpr int KT = KPT / T, KTS = (KT + 3) & ~3;
+  // Cbar block of one thread parity: padded so the T blocks start in
+  // different bank groups (one 16-byte load of a quarter warp touches T blocks)
+  constexpr int CTS = ((KPT * KTS + 31) & ~31) + 8;
+  static_assert(KPT % T == 0, "KPT must be a multiple of T");
+  static_assert(M == 1 || M == 2, "one or two rows per thread");
   extern __shared__ __align__(16) float nt_smem[];
+  __shared__ __align__(16) NtPar<kGen> par_s[2][KPT];
   __shared__ double lam_s[KPT], rho_s[KPT];
-  __shared__ float thf_s[KPT], scf_s[KPT], invc_s[KPT], vlo_s[KPT];
+  __shared__ float invc_s[KPT], vlo_s[KPT];
   __shared__ int mode_s[KPT], jmap_s[KPT], pinv_s[KPT];
-  __shared__ int conv_all_s;
+  __shared__ double dmax_s;
+  __shared__ double diag_s[KPT], lws_s[KPT], ns_s[KPT];
+  __shared__ int fnew_s[2];   // first unconverged position, double-buffered by round parity
+  __shared__ int mcnt_s;      // selected rows of M_{t+1} in my slice
   const int k = P.k, kp = P.kp;
+  const int nthr = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
   const int64_t q = *P.q_dev;
   const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
   int nr = (int)(hi - lo);
-  if (nr > P.cap_rows) {
-    if (tid == 0) atomicExch(P.err, 2);
-    nr = P.cap_rows;
-  }
   const int cap = P.cap_rows;
-  const size_t blk = ((size_t)cap * LD + 3) & ~(size_t)3;   // 16-byte aligned sub-arrays
+  if (nr > cap || T * ((nr + M - 1) / M) > nthr) {
+    if (tid == 0) atomicExch(P.err, 2);
+    nr = min(cap, (nthr / T) * M);
+  }
+  // cap rows + 1 spare row (zeros in Dold / Rini, scratch in V) for the threads past nr
+  const size_t blk = ((size_t)(cap + 1) * LD + 3) & ~(size_t)3;   // 16-byte aligned sub-arrays
   float* Dold = nt_smem;                        // cap x LD   (pi order)
-  float* Rini = Dold + blk;                     // cap x LD
-  float* V = Rini + blk;                        // cap x LD   (v of the last round)
-  float* Dn = V + blk;                          // cap x LD   (d of the last round = the result)
-  float* Cpi = Dn + blk;                        // k x KPT    Cbar in pi order, zero padded
-  double* part = reinterpret_cast<double*>(Cpi + (size_t)k * KPT);   // stats partials (see below)
+  float* Rini = Dold + blk;                     // cap x LD   (staged Cbar, then R0 / c_pp)
+  float* V = Rini + blk;                        // cap x LD   (v of the last round; staged D rows first)
+  float* W = V + blk;                           // cap x LD   (staged Bbar rows; then Ct when it fits)
+  float* Cpi = W + blk;                         // k x KPT    Cbar in pi order, zero padded
+  float* Ct = P.ct_in_w ? W : Cpi + (size_t)k * KPT;                    // T x CTS
+  int* rows_s = reinterpret_cast<int*>(P.ct_in_w ? Cpi + (size_t)k * KPT : Ct + (size_t)T * CTS);
   const double a = P.a, b = P.b;
-
-  int* rows_s = reinterpret_cast<int*>(part + 3 * (size_t)max(1, kNtThreads / max(k, 1)) * KPT +
-                                       (size_t)max(1, kNtThreads / max(k, 1)) * KPT);   // cap
-  __shared__ double dmax_s;
-  __shared__ double diag_s[KPT], lws_s[KPT], ns_s[KPT];
+  if (tid == 0) mcnt_s = 0;
   long long t_mark = clock64();
   // ---- setup: round 1 (independent loads) ------------------------------------------
-  // Cbar (fp32, atom order) -> Rini as a staging buffer when it fits, the row
-  // indices, the atom order and the per-atom scalars, all in flight at once
   const bool cstage = (size_t)cap * LD >= (size_t)k * k + 4;
   if (cstage) {
-    for (int e = tid; e < (k * k + 3) / 4; e += kNtThreads) cp_async16(Rini + 4 * e, P.C32 + 4 * e);
+    for (int e = tid; e < (k * k + 3) / 4; e += nthr) cp_async16(Rini + 4 * e, P.C32 + 4 * e);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
-  for (int r = tid; r < nr; r += kNtThreads) rows_s[r] = P.idx[lo + r];
-  for (int p = tid; p < k; p += kNtThreads) {
+  for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + r];
+  for (int p = tid; p < k; p += nthr) {
     jmap_s[p] = P.perm[p];
     diag_s[p] = P.C64[(int64_t)p * k + p];
     lws_s[p] = P.lam_ws[p];
@@ -288,13 +356,30 @@ k_bcd_newton(NtArgs P) {
   // ---- round 2: the masked rows of D and Bbar (cp.async, every chunk in flight) ----
   {
     const int c4 = kp / 4;
-    for (int e = tid; e < nr * c4; e += kNtThreads) {
+    for (int e = tid; e < nr * c4; e += nthr) {
       const int row = e / c4, c = e % c4;
       const int64_t goff = (int64_t)rows_s[row] * kp + 4 * c;
       cp_async16(V + (size_t)row * kp + 4 * c, P.D + goff);
-      cp_async16(Dn + (size_t)row * kp + 4 * c, P.Bbar + goff);
+      cp_async16(W + (size_t)row * kp + 4 * c, P.Bbar + goff);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // M_{t+1} of my slice of Philox blocks while the rows are in flight
+  uint8_t* mbits_s = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(nt_smem) + P.mbits_off);
+  int64_t mb0 = 0;
+  int nmb = 0;
+  if (P.idx_next) {
+    const int64_t b0 = P.row_lo >> 2, nb = ((P.row_hi - 1) >> 2) - b0 + 1;
+    mb0 = b0 + nb * blockIdx.x / G;
+    nmb = (int)(b0 + nb * (blockIdx.x + 1) / G - mb0);
+    int c = 0;
+    for (int i = tid; i < nmb; i += nthr) {
+      const uint32_t bits = mask_bits(P.seed, (uint64_t)P.tn, mb0 + i, P.row_lo, P.row_hi, P.Tthr);
+      mbits_s[i] = (uint8_t)bits;
+      c += __popc(bits);
+    }
+    c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    if (lane == 0 && c) atomicAdd(&mcnt_s, c);
   }
   if (wid == 0) {
     double dm = 1.0;
@@ -304,32 +389,32 @@ k_bcd_newton(NtArgs P) {
   }
   __syncthreads();
   const double dmax = dmax_s;
-  for (int p = tid; p < KPT; p += kNtThreads) {
+  for (int p = tid; p < KPT; p += nthr) {
     if (p < k) {
       const int j = jmap_s[p];
       pinv_s[j] = p;
       const double cjj = diag_s[j];
       const bool dead = !(cjj > 1e-12 * dmax);                      // R10
-      invc_s[p] = dead ? 0.f : (float)(1.0 / cjj);
-      vlo_s[p] = (P.pos && !dead) ? 0.f : -INFINITY;      // D >= 0 clamp; dead atoms keep d
       const double lw = dead ? 0.0 : lws_s[j];
       lam_s[p] = lw;
       rho_s[p] = ns_s[j];         // n_{t-1}^(j); becomes rho_j after round 0
-      mode_s[p] = dead ? kModeDead : (lw > 0.0 ? kModeShrink : kModeCopy);
-      thf_s[p] = (float)(a * lw);
-      scf_s[p] = (float)(1.0 / (1.0 + b * lw));
+      const int mode = dead ? kModeDead : (lw > 0.0 ? kModeShrink : kModeCopy);
+      mode_s[p] = mode;
+      invc_s[p] = dead ? 0.f : (float)(1.0 / cjj);
+      vlo_s[p] = P.pos ? 0.f : -INFINITY;                            // D >= 0 clamp
+      par_s[0][p] = par_s[1][p] = nt_make_par<kGen>(mode, a, b, lw, vlo_s[p]);
     } else {
-      invc_s[p] = 0.f;
-      vlo_s[p] = -INFINITY;
-      thf_s[p] = 0.f;
-      scf_s[p] = 1.f;
       mode_s[p] = kModeDead;
       lam_s[p] = 0.0;
+      invc_s[p] = 0.f;
+      vlo_s[p] = -INFINITY;
+      par_s[0][p] = par_s[1][p] = nt_make_par<kGen>(kModeDead, a, b, 0.0, -INFINITY);
     }
   }
+  if (tid == 0) fnew_s[0] = fnew_s[1] = k;
   asm volatile("cp.async.wait_group 1;" ::: "memory");     // Cbar staged
   __syncthreads();
-  for (int e = tid; e < k * KPT; e += kNtThreads) {
+  for (int e = tid; e < k * KPT; e += nthr) {
     const int p = e / KPT, l = e % KPT;
     const int64_t src = (int64_t)jmap_s[p] * k + (l < k ? jmap_s[l] : 0);
     Cpi[e] = l < k ? (cstage ? Rini[src] : __ldg(P.C32 + src)) : 0.f;
@@ -338,23 +423,34 @@ k_bcd_newton(NtArgs P) {
   asm volatile("cp.async.wait_group 0;" ::: "memory");     // rows staged
   __syncthreads();
   NT_MARK(77);
-  for (int e = tid; e < nr * KPT; e += kNtThreads) {
+  for (int e = tid; e < LD; e += nthr) {
+    Dold[(size_t)cap * LD + e] = 0.f;
+    Rini[(size_t)cap * LD + e] = 0.f;
+  }
+  for (int e = tid; e < nr * KPT; e += nthr) {
     const int row = e / KPT, p = e % KPT;
     const bool in = p < k;
     const int j = in ? jmap_s[p] : 0;
     Dold[(size_t)row * LD + p] = in ? V[(size_t)row * kp + j] : 0.f;
-    Rini[(size_t)row * LD + p] = in ? Dn[(size_t)row * kp + j] : 0.f;
+    Rini[(size_t)row * LD + p] = in ? W[(size_t)row * kp + j] : 0.f;
   }
   __syncthreads();
+  // prescaled Cbar per thread parity (W is free now): c_{p,l} / c_{l,l}
+  for (int e = tid; e < T * KPT * KTS; e += nthr) {
+    const int t = e / (KPT * KTS), rem = e % (KPT * KTS), p = rem / KTS, i = rem % KTS;
+    const int l = i * T + t;
+    Ct[(size_t)t * CTS + rem] = (i < KT && p < k) ? Cpi[(size_t)p * KPT + l] * invc_s[l] : 0.f;
+  }
   NT_MARK(78);
-  // R = P Bbar - P D Cbar: 8 rows x 8 positions per item (about one item per thread)
+  // R = (P Bbar - P D Cbar) / c_pp: RT rows x 8 positions per item (register tile)
   {
-    const int nrb = (nr + 7) / 8, npb = (k + 7) / 8;
-    for (int it = tid; it < nrb * npb; it += kNtThreads) {
-      const int r0 = (it / npb) * 8, p0 = (it % npb) * 8;
-      float acc[8][8];
+    constexpr int RT = 8;
+    const int nrb = (nr + RT - 1) / RT, npb = (k + 7) / 8;
+    for (int it = tid; it < nrb * npb; it += nthr) {
+      const int r0 = (it / npb) * RT, p0 = (it % npb) * 8;
+      float acc[RT][8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
         for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
       for (int l = 0; l < k; ++l) {
@@ -362,114 +458,142 @@ k_bcd_newton(NtArgs P) {
         const float4 c1 = *reinterpret_cast<const float4*>(Cpi + (size_t)l * KPT + p0 + 4);
         const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < RT; ++i) {
           const float d = Dold[(size_t)min(r0 + i, cap - 1) * LD + l];
 #pragma unroll
           for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(d, cv[c], acc[i][c]);
         }
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < RT; ++i) {
         const int row = r0 + i;
         if (row >= nr) continue;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int p = p0 + c;
-          if (p < k) Rini[(size_t)row * LD + p] -= acc[i][c];
+          if (p < k) {
+            float* rr = Rini + (size_t)row * LD + p;
+            *rr = (*rr - acc[i][c]) * invc_s[p];
+          }
         }
       }
     }
   }
+  // radii (R9): ||P d_j|| of the column before its update, one warp per atom
+  if (nr > 0) {
+    const int nwarp = nthr >> 5;
+    for (int p = wid; p < k; p += nwarp) {
+      double d1 = 0.0, d2 = 0.0;
+      for (int row = lane; row < nr; row += 32) {
+        const double d = Dold[(size_t)row * LD + p];
+        d1 += fabs(d);
+        d2 += d * d;
+      }
+      d1 = warp_sum(d1);
+      d2 = warp_sum(d2);
+      if (lane == 0) {
+        double* rr = P.rec + ((size_t)kNtRing * k + p) * kNtRec;
+        nt_red_add(rr, d1);
+        nt_red_add(rr + 1, d2);
+      }
+    }
+  }
   __syncthreads();
+  // my rows: M consecutive rows of group g; rows >= nr use the spare row
+  const int g = tid / T, tq = tid % T;
+  int rowx[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) rowx[m] = (g * M + m < nr) ? g * M + m : cap;
+  const int vstride = (rowx[M - 1] - rowx[0]);          // 1 row apart unless the tail hits the spare row
+  float Do[M][KT];
+#pragma unroll
+  for (int m = 0; m < M; ++m)
+#pragma unroll
+    for (int i = 0; i < KT; ++i) Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
+  const float* Ct_t = Ct + (size_t)tq * CTS;
 
-  // stats partial layout: H groups of threads per atom
-  const int H = max(1, kNtThreads / max(k, 1));
-  double* pc = part;                              // [H][KPT] count
-  double* p1 = pc + H * KPT;                      // [H][KPT] S1
-  double* p2 = p1 + H * KPT;                      // [H][KPT] S2
-  unsigned* pmn = reinterpret_cast<unsigned*>(p2 + H * KPT);   // [H][KPT]
-  unsigned* pmx = pmn + H * KPT;                                // [H][KPT]
-
+  // stats partials (H threads per atom) reuse the Cbar staging area (host checks the size)
+  const int H = max(1, nthr / max(k, 1));
+  unsigned* pcn = reinterpret_cast<unsigned*>(P.part_in_cpi ? Cpi : reinterpret_cast<float*>(rows_s + cap));
+  float* ps1 = reinterpret_cast<float*>(pcn + H * KPT);
+  float* ps2 = ps1 + H * KPT;
+  unsigned* pmn = reinterpret_cast<unsigned*>(ps2 + H * KPT);
+  unsigned* pmx = pmn + H * KPT;
+  __syncthreads();
+  if (P.idx_next && tid == 0) P.cnt_next[blockIdx.x] = mcnt_s;   // before round 0's barrier
   NT_MARK(0);
   unsigned nbar = 0;
-  int round = 0;
+  int round = 0, cur = 0, F = 0;
   bool done = q == 0;
+#pragma unroll 1
   while (!done) {
-    // ---- 1. the recurrence, thread per row ------------------------------------
-    if (tid < nr) {
-      const int row = tid;
-      float R[KPT];
+    // ---- 1. the recurrence from the frozen prefix on, T threads x M rows ---------
+    {
+      // every thread of the CTA runs it (the width-T shuffles need converged
+      // warps); rows >= nr compute on the spare row's zeros
+      float R[M][KT];
 #pragma unroll
-      for (int p = 0; p < KPT; ++p) R[p] = Rini[(size_t)row * LD + p];
-      NtRec<KPT, 0>::run(R, Dold + (size_t)row * LD, V + (size_t)row * LD, Dn + (size_t)row * LD, Cpi, invc_s,
-                         thf_s, scf_s, vlo_s, k);
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int i = 0; i < KT; ++i) R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
+      // rows rowx[0] and rowx[0] + vstride (vstride = LD for consecutive rows; the
+      // spare row is its own target when both are past nr)
+      NtRec5<KPT, T, M, kGen, 0>::run(R, Do, tq, F, V + (size_t)rowx[0] * LD,
+                                      M > 1 ? vstride * LD : 0, Ct_t, par_s[cur]);
     }
     __syncthreads();
     NT_MARK(1);
-    // ---- 2. per-atom statistics over my rows, then one grid reduction -----------
+    // ---- 2. per-atom statistics over my rows, then one grid reduction -------------
+    // H threads per atom sum a strided share of the rows (fp32 over <= cap/H
+    // rows, relative error ~1e-6), combined in fixed order.
     const int ring = round % kNtRing;
-    if (tid < H * k) {
-      const int p = tid % k, h = tid / k;
-      const double th = a * lam_s[p];
-      const bool thr_zero = !(th > 0.0);
-      // fp32 partials over <= cap/H rows (relative error ~1e-6),
-      // fp64 from here on.  The test is exact: for a float |v| and a double
-      // th, |v| > th  <=>  |v| > round_down_to_float(th).
-      int cnt = 0;
-      float s1 = 0.f, s2 = 0.f;
-      unsigned mn = 0xffffffffu, mx = 0u;
-      const float thf = thr_zero ? 0.f : __double2float_rd(th);
+    const int nact = k - F;
+    if (nr > 0) {
+      if (tid < H * nact) {
+        const int p = F + tid % nact, h = tid / nact;
+        const double th = a * lam_s[p];
+        // the test is exact: for a float |v| and a double th,
+        // |v| > th  <=>  |v| > round_down_to_float(th)
+        const float thf = th > 0.0 ? __double2float_rd(th) : 0.f;
+        unsigned cnt = 0, mn = 0xffffffffu, mx = 0u;
+        float s1 = 0.f, s2 = 0.f;
 #pragma unroll 4
-      for (int row = h; row < nr; row += H) {
-        const float av = fabsf(V[(size_t)row * LD + p]);
-        if (av > thf) {
-          ++cnt;
-          s1 += av;
-          s2 = fmaf(av, av, s2);
-          mn = min(mn, __float_as_uint(av));
-        } else {
-          mx = max(mx, __float_as_uint(av));
+        for (int r = h; r < nr; r += H) {
+          const float av = fabsf(V[(size_t)r * LD + p]);
+          const bool above = av > thf;
+          cnt += above;
+          s1 += above ? av : 0.f;
+          s2 = fmaf(above ? av : 0.f, av, s2);
+          mn = above ? min(mn, __float_as_uint(av)) : mn;
+          mx = above ? mx : max(mx, __float_as_uint(av));
         }
+        pcn[h * KPT + p] = cnt;
+        ps1[h * KPT + p] = s1;
+        ps2[h * KPT + p] = s2;
+        pmn[h * KPT + p] = mn;
+        pmx[h * KPT + p] = mx;
       }
-      pc[h * KPT + p] = (double)cnt;
-      p1[h * KPT + p] = (double)s1;
-      p2[h * KPT + p] = (double)s2;
-      pmn[h * KPT + p] = mn;
-      pmx[h * KPT + p] = mx;
-    }
-    __syncthreads();
-    if (tid < k) {
-      const int p = tid;
-      double cnt = 0.0, s1 = 0.0, s2 = 0.0;
-      unsigned mn = 0xffffffffu, mx = 0u;
-      for (int h = 0; h < H; ++h) {
-        cnt += pc[h * KPT + p];
-        s1 += p1[h * KPT + p];
-        s2 += p2[h * KPT + p];
-        mn = min(mn, pmn[h * KPT + p]);
-        mx = max(mx, pmx[h * KPT + p]);
-      }
-      double* acc = P.acc + ((size_t)ring * k + p) * 3;
-      unsigned* mm = P.accmm + ((size_t)ring * k + p) * 2;
-      if (nr > 0) {
-        if (cnt > 0.0) {
-          nt_red_add(acc, cnt);
-          nt_red_add(acc + 1, s1);
-          nt_red_add(acc + 2, s2);
+      __syncthreads();
+      if (tid < nact) {
+        const int p = F + tid;
+        unsigned cnt = 0, mn = 0xffffffffu, mx = 0u;
+        double S1 = 0.0, S2 = 0.0;
+        for (int h = 0; h < H; ++h) {
+          cnt += pcn[h * KPT + p];
+          S1 += (double)ps1[h * KPT + p];
+          S2 += (double)ps2[h * KPT + p];
+          mn = min(mn, pmn[h * KPT + p]);
+          mx = max(mx, pmx[h * KPT + p]);
+        }
+        double* rc = P.rec + ((size_t)ring * k + p) * kNtRec;
+        unsigned* mm = reinterpret_cast<unsigned*>(rc + 3);
+        if (cnt > 0) {
+          nt_red_add(rc, (double)cnt);
+          nt_red_add(rc + 1, S1);
+          nt_red_add(rc + 2, S2);
           atomicMin(mm, mn);
         }
         if (mx) atomicMax(mm + 1, mx);
-        if (round == 0) {
-          // radii (R9): ||P d_j|| of the column before its update
-          double d1 = 0.0, d2 = 0.0;
-          for (int row = 0; row < nr; ++row) {
-            const double d = Dold[(size_t)row * LD + p];
-            d1 += fabs(d);
-            d2 += d * d;
-          }
-          nt_red_add(P.rho_acc + 2 * p, d1);
-          nt_red_add(P.rho_acc + 2 * p + 1, d2);
-        }
       }
     }
     NT_MARK(2);
@@ -479,71 +603,188 @@ k_bcd_newton(NtArgs P) {
     if (blockIdx.x == 0) {
       // recycle the ring slot of the NEXT-but-one round (its readers are done)
       const int rz = (round + 2) % kNtRing;
-      for (int e = tid; e < 3 * k; e += kNtThreads) P.acc[(size_t)rz * k * 3 + e] = 0.0;
-      for (int e = tid; e < k; e += kNtThreads) {
-        P.accmm[((size_t)rz * k + e) * 2] = 0xffffffffu;
-        P.accmm[((size_t)rz * k + e) * 2 + 1] = 0u;
-      }
+      for (int p = tid; p < k; p += nthr) nt_rec_reset(P.rec + ((size_t)rz * k + p) * kNtRec);
     }
-    // ---- 3. the same Michelot step for every atom in every CTA -----------------
-    int conv = 1;
-    if (tid < k) {
-      const int p = tid;
+    // ---- 3. the same Michelot step for every unfrozen atom in every CTA ----------
+    int conv = 1, nmode = 0;
+    double nlam = 0.0, cnt = 0.0, S1 = 0.0, S2 = 0.0;
+    const int p = F + tid;
+    const bool act = tid < nact;
+    if (act) {
       if (round == 0) {
-        const double d1 = __ldcg(P.rho_acc + 2 * p), d2 = __ldcg(P.rho_acc + 2 * p + 1);
+        const double* rr = P.rec + ((size_t)kNtRing * k + p) * kNtRec;
+        const double d1 = __ldcg(rr), d2 = __ldcg(rr + 1);
         rho_s[p] = fmax(0.0, rho_s[p] + a * d1 + 0.5 * b * d2);          // P:860, R9
       }
-      const double rho = rho_s[p];
-      const double* acc = P.acc + ((size_t)ring * k + p) * 3;
-      const unsigned* mm = P.accmm + ((size_t)ring * k + p) * 2;
-      const double cnt = __ldcg(acc), S1 = __ldcg(acc + 1), S2 = __ldcg(acc + 2);
-      const double mnv = cnt > 0.0 ? (double)__uint_as_float(__ldcg(mm)) : INFINITY;
-      const double mxv = (double)__uint_as_float(__ldcg(mm + 1));
-      const int mode = mode_s[p];
-      const double lam = lam_s[p];
-      int nmode;
-      double nlam;
-      conv = nt_atom_update(a, b, rho, cnt, S1, S2, mnv, mxv, mode, lam, &nmode, &nlam);
-      lam_s[p] = nlam;
-      mode_s[p] = nmode;
-      thf_s[p] = nmode == kModeShrink ? (float)(a * nlam) : 0.f;
-      scf_s[p] = nmode == kModeShrink ? (float)(1.0 / (1.0 + b * nlam)) : nmode == kModeZero ? 0.f : 1.f;
+      const double* acc = P.rec + ((size_t)ring * k + p) * kNtRec;
+      const unsigned* mm = reinterpret_cast<const unsigned*>(acc + 3);
+      cnt = __ldcg(acc);
+      S1 = __ldcg(acc + 1);
+      S2 = __ldcg(acc + 2);
+      const unsigned mnb = __ldcg(mm), mxb = __ldcg(mm + 1);
+      const double mnv = cnt > 0.0 ? (double)__uint_as_float(mnb) : INFINITY;
+      const double mxv = (double)__uint_as_float(mxb);
+      conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol);
+      if (!conv) atomicMin(&fnew_s[round & 1], p);
     }
-    const int all = __syncthreads_and(conv);
+    __syncthreads();
+    const int Fn = fnew_s[round & 1];
+    if (tid == 0) fnew_s[(round + 1) & 1] = k;      // nobody reads that slot this round
+    const bool capped = round + 1 >= P.max_rounds && Fn < k;
+    if (act) {
+      if (p < Fn || capped) {
+        // frozen with this round's parameters: slack n_j = rho_j - ||d_j|| from
+        // this round's sums, warm start for the next iteration
+        if (mode_s[p] != kModeDead && blockIdx.x == 0) {
+          const int j = jmap_s[p];
+          P.nslack[j] = rho_s[p] - nt_norm_d(a, b, mode_s[p], lam_s[p], cnt, S1, S2);
+          P.lam_ws[j] = lam_s[p];
+        }
+        par_s[cur ^ 1][p] = par_s[cur][p];
+      } else {
+        lam_s[p] = nlam;
+        mode_s[p] = nmode;
+        par_s[cur ^ 1][p] = nt_make_par<kGen>(nmode, a, b, nlam, vlo_s[p]);
+      }
+    }
+    // (frozen and padding positions hold the same parameters in both buffers)
     if (P.prof && blockIdx.x == 0) {
       // convergence profile: unconverged atoms per round (slots 8..71)
-      const int nun = __syncthreads_count(!conv);
+      const int nun = __syncthreads_count(act && !conv);
       if (tid == 0 && round < 64) P.prof[8 + round] += nun;
     }
     NT_MARK(4);
     ++round;
-    if (all) {
+    if (Fn >= k) {
       done = true;
-    } else if (round >= P.max_rounds) {
+    } else if (capped) {
       if (tid == 0 && blockIdx.x == 0) atomicExch(P.err, 4);
       done = true;
     }
-    if (done && tid < k) {
-      // slack n_j = rho_j - ||d_j|| from the sums of this (final) round
-      const int p = tid, j = jmap_s[p];
-      const int mode = mode_s[p];
-      if (mode != kModeDead && blockIdx.x == 0) {
-        const double* acc = P.acc + ((size_t)ring * k + p) * 3;
-        const double cnt = __ldcg(acc), S1 = __ldcg(acc + 1), S2 = __ldcg(acc + 2);
-        const double Nd = nt_norm_d(a, b, mode, lam_s[p], cnt, S1, S2);
-        P.nslack[j] = rho_s[p] - Nd;
-        P.lam_ws[j] = lam_s[p];
+    if (!done) {
+      // fold the newly frozen atoms [F, Fn) into the initial residual of my rows
+      if (Fn > F) {
+        float R[M][KT];
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int i = 0; i < KT; ++i) R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
+        for (int j = F; j < Fn; ++j) {
+          const NtPar<kGen> pr = par_s[cur][j];
+          const float* crow = Ct_t + j * KTS;
+          float delta[M];
+#pragma unroll
+          for (int m = 0; m < M; ++m) {
+            const float v = V[(size_t)rowx[m] * LD + j];
+            const float dj = pr.d_of(v);
+            delta[m] = dj - Dold[(size_t)rowx[m] * LD + j];
+          }
+#pragma unroll
+          for (int j4 = 0; j4 < KTS / 4; ++j4) {
+            const float4 c = *reinterpret_cast<const float4*>(crow + 4 * j4);
+            const float cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 4 * j4 + e;
+              if (i < KT) {
+                const int l = i * T + tq;
+                if (l > j) {
+#pragma unroll
+                  for (int m = 0; m < M; ++m) R[m][i] = fmaf(-delta[m], cc[e], R[m][i]);
+                }
+              }
+            }
+          }
+        }
+        __syncthreads();   // every thread read its R0 before anyone writes
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+          if (rowx[m] == cap) continue;
+#pragma unroll
+          for (int i = 0; i < KT; ++i) Rini[(size_t)rowx[m] * LD + i * T + tq] = R[m][i];
+        }
       }
+      F = Fn;
+      cur ^= 1;
+      __syncthreads();
     }
   }
   __syncthreads();
   NT_MARK(5);
-  // ---- final D = the last round's d (what its recurrence used), in atom order ------
-  if (q > 0) {
-    for (int row = wid; row < nr; row += kNtThreads / 32) {
-      float* dst = P.D + (int64_t)rows_s[row] * kp;
-      const float* src = Dn + (size_t)row * LD;
-      for (int j = lane; j < k; j += 32) dst[j] = src[pinv_s[j]];
+  // ---- final D = the v of each atom's final round through its parameters, atom order ----
+  // (with the draw-ahead on, the last warp scatters M_{t+1} and, in CTA 0, warp
+  // 0 draws pi_{t+1}: both stay out of the write-back so the three overlap)
+  const int nwarp_all = nthr >> 5;
+  const bool ahead = P.idx_next != nullptr && nwarp_all >= 4;
+  if (q > 0 && !(ahead && (wid == nwarp_all - 1 || (blockIdx.x == 0 && wid == 0)))) {
+    const NtPar<kGen>* pr = par_s[cur];
+    const int w0 = (ahead && blockIdx.x == 0) ? 1 : 0;
+    const int nwarp = ahead ? nwarp_all - 1 - w0 : nwarp_all;
+    for (int r = wid - w0; r < nr; r += nwarp) {
+      float* dst = P.D + (int64_t)rows_s[r] * kp;
+      const float* src = V + (size_t)r * LD;
+      for (int j = lane; j < k; j += 32) {
+        const int pp = pinv_s[j];
+        dst[j] = pr[pp].d_of(src[pp]);
+      }
+    }
+  }
+  // ---- draw-ahead of t+1: scatter of my slice of M_{t+1}, pi_{t+1}, t+1, w_{t+1} -----
+  if (P.idx_next) {
+    const int nwarp = nthr >> 5;
+    if (wid == nwarp - 1) {
+      // rows of M_{t+1} before my slice: counts of the CTAs before me (fixed order)
+      int64_t off = 0;
+      for (int i = lane; i < (int)blockIdx.x; i += 32) off += __ldcg(P.cnt_next + i);
+      off = warp_sum(off);
+      // lane l scans the blocks [l nmb / 32, (l+1) nmb / 32) of my slice
+      const int i0 = nmb * lane / 32, i1 = nmb * (lane + 1) / 32;
+      int c = 0;
+      for (int i = i0; i < i1; ++i) c += __popc((unsigned)mbits_s[i]);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int64_t pos = off + incl - c;
+      for (int i = i0; i < i1; ++i) {
+        const unsigned bits = mbits_s[i];
+        for (int l = 0; l < 4; ++l)
+          if (bits & (1u << l)) P.idx_next[pos++] = (int32_t)((mb0 + i) * 4 + l - P.row_lo);
+      }
+      if (blockIdx.x == G - 1 && lane == 31) *P.q_next = pos;
+    }
+    if (blockIdx.x == 0 && wid == 0) {
+      // Alg. 4's atom order of t+1 (R13): words drawn by the warp, swaps by lane 0
+      // scratch the other warps' write-back does not read: >= k words each
+      int32_t* pi = reinterpret_cast<int32_t*>(par_s[cur ^ 1]);
+      uint32_t* words = reinterpret_cast<uint32_t*>(lam_s);
+      __syncwarp();
+      for (int i = lane; i < k; i += 32) pi[i] = i;
+      if (!P.cyclic) {
+        for (int bq = lane; bq * 4 < k - 1; bq += 32) {
+          const U4 w = philox4x32_10(U4{(uint32_t)bq, (uint32_t)P.tn, kStreamPerm, 0u}, P.seed);
+          for (int l = 0; l < 4; ++l)
+            if (bq * 4 + l < k - 1) words[bq * 4 + l] = u4_word(w, l);
+        }
+      }
+      __syncwarp();
+      if (!P.cyclic && lane == 0) {
+        for (int w = 0; w < k - 1; ++w) {
+          const int i = k - 1 - w;
+          const int j = (int)(((uint64_t)words[w] * (uint64_t)(i + 1)) >> 32);
+          const int32_t tmp = pi[i];
+          pi[i] = pi[j];
+          pi[j] = tmp;
+        }
+      }
+      __syncwarp();
+      for (int i = lane; i < k; i += 32) P.perm_next[i] = pi[i];
+      if (lane == 0) {
+        *P.t_next = P.tn;
+        *P.w_next = pow((double)P.tn, -P.u);
+      }
     }
   }
   // ---- exit: last CTA resets counters and accumulators ------------------------------
@@ -555,12 +796,7 @@ k_bcd_newton(NtArgs P) {
     const unsigned old = atomicAdd(P.bar + 1, 1u);
     if (old == (unsigned)G - 1) {
       __threadfence();
-      for (int e = 0; e < kNtRing * k * 3; ++e) P.acc[e] = 0.0;
-      for (int e = 0; e < kNtRing * k; ++e) {
-        P.accmm[2 * e] = 0xffffffffu;
-        P.accmm[2 * e + 1] = 0u;
-      }
-      for (int e = 0; e < 2 * k; ++e) P.rho_acc[e] = 0.0;
+      for (int e = 0; e < (kNtRing + 1) * k; ++e) nt_rec_reset(P.rec + (size_t)e * kNtRec);
       if (P.nred_out) *P.nred_out = nbar;
       P.bar[0] = 0u;
       P.bar[1] = 0u;

@@ -1,0 +1,22 @@
+// bcd_newton_inst.cu -- instantiates the simultaneous-threshold BCD kernel
+// k_bcd_newton<NT_KPT, T, M, gen> (bcd_newton.cuh) for groups of T = 4 or 2
+// threads owning M = 2 masked rows.  Compiled once per NT_KPT (-DNT_KPT=...) so the variants build in
+// parallel; the C ABI (somf_capi.cu) picks one through somf_nt_kernel_<KPT>.
+#include "bcd_newton.cuh"
+
+#ifndef NT_KPT
+#error "compile with -DNT_KPT=<positions per row>"
+#endif
+#define NT_CAT2(a, b) a##b
+#define NT_CAT(a, b) NT_CAT2(a, b)
+
+// T threads x M rows per group; gen = generic parameters (mu > 0 or D >= 0)
+const void* NT_CAT(somf_nt_kernel_, NT_KPT)(int T, int M, int gen) {
+  if (T == 4 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, true>
+                                   : (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, false>;
+  if (T == 4 && M == 1) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, true>
+                                   : (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, false>;
+  if (T == 2 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, true>
+                                   : (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, false>;
+  return nullptr;
+}

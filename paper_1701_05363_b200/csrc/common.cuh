@@ -42,6 +42,20 @@ __host__ __device__ __forceinline__ uint32_t u4_word(const U4& v, int lane) {
 
 enum : uint32_t { kStreamMask = 1, kStreamPerm = 2, kStreamCols = 3 };
 
+// Selection bits of the 4 rows of Philox block blk (rows 4 blk .. 4 blk + 3)
+// in M_t (Eq. mt; R1, R2): row i selected iff word_{i&3} < T(r).
+__device__ __forceinline__ uint32_t mask_bits(uint64_t seed, uint64_t t, int64_t blk,
+                                              int64_t row_lo, int64_t row_hi, uint64_t T) {
+  const U4 w = philox4x32_10(U4{(uint32_t)blk, (uint32_t)t, kStreamMask, (uint32_t)(blk >> 32)}, seed);
+  uint32_t bits = 0;
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    const int64_t row = blk * 4 + l;
+    if (row >= row_lo && row < row_hi && (uint64_t)u4_word(w, l) < T) bits |= 1u << l;
+  }
+  return bits;
+}
+
 // ---------------------------------------------------------------------------
 // Fixed-order reductions.  xor-butterfly: every lane ends with the same value
 // and the combination tree does not depend on timing.

@@ -175,11 +175,23 @@ namespace somf {
 // second half lands.  Used when the tile covers k and eta + k and the slice
 // fits in shared memory; rows beyond one slice are processed in segments.
 // ---------------------------------------------------------------------------
+// Optional fused split-K reduction (cooperative launch, bar != null): after
+// the partial tiles are written, one grid barrier, then CTA b reduces the
+// outputs [tot b / G, tot (b+1) / G) over the G partials in the fixed order
+// of k_contract_reduce2 (lane = output, warp w sums splits w, w + 8, ...,
+// then the 8 warp sums in order) and writes r x [beta | G] in fp64.
+struct CtFuse {
+  unsigned* bar;            // [0] arrivals, [1] exits (zero between launches); null = no fusion
+  double r;
+  double* beta;             // k x eta
+  double* G;                // k x k
+};
+
 template <int MT, int NT, bool kXCompact>
 __global__ void __launch_bounds__(kCtThreads)
 k_contract_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, const float* __restrict__ D,
               int kp, int k, const float* __restrict__ X, int64_t ldx, int eta, float* __restrict__ partial,
-              int seg_rows) {
+              int seg_rows, CtFuse fz) {
   extern __shared__ __align__(16) float c3_smem[];
   const int LDY = eta + kp;                 // [X row | D row], 16-byte multiple
   float* Ys = c3_smem;                      // seg_rows x LDY
@@ -243,6 +255,65 @@ k_contract_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev
     for (int j = 0; j < NT; ++j) {
       const int c = tc + 32 * j;
       if (c < nc) out[(int64_t)a * nc + c] = acc[i][j];
+    }
+  }
+  if (fz.bar == nullptr) return;
+  // ---- fused fixed-order reduction of the G partial tiles ----------------------------
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(fz.bar), "r"(1u) : "memory");
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_gpu(fz.bar) < (unsigned)G) {
+      if (globaltimer_ns() - t0 > 2000000000ull) break;     // protocol bug: do not hang the GPU
+    }
+  }
+  __syncthreads();
+  // warp w sums the splits w, w + 8, ... of all my outputs (every load in flight
+  // at once: the latency of L2, not its bandwidth, bounds this), lane = output
+  constexpr int kOpl = 8;                        // outputs per lane (>= ceil(tot / G / 32))
+  __shared__ double ws[8][32 * kOpl];
+  const int64_t tot = (int64_t)k * nc;
+  const int64_t e0 = tot * blockIdx.x / G, e1 = tot * (blockIdx.x + 1) / G;
+  for (int64_t g0 = e0; g0 < e1; g0 += 32 * kOpl) {
+    double sacc[kOpl];
+#pragma unroll
+    for (int o = 0; o < kOpl; ++o) sacc[o] = 0.0;
+#pragma unroll 5
+    for (int i = ta; i < G; i += 8) {
+      float v[kOpl];
+#pragma unroll
+      for (int o = 0; o < kOpl; ++o) {
+        const int64_t e = g0 + 32 * o + tc;
+        v[o] = e < e1 ? __ldcg(partial + (int64_t)i * tot + e) : 0.f;
+      }
+#pragma unroll
+      for (int o = 0; o < kOpl; ++o) sacc[o] += (double)v[o];
+    }
+#pragma unroll
+    for (int o = 0; o < kOpl; ++o) ws[ta][32 * o + tc] = sacc[o];
+    __syncthreads();
+    for (int x = tid; x < 32 * kOpl; x += kCtThreads) {
+      const int64_t e = g0 + x;
+      if (e < e1) {
+        double t = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t += ws[i][x];
+        t *= fz.r;
+        const int a = (int)(e / nc), c = (int)(e % nc);
+        if (c < eta) fz.beta[(int64_t)a * eta + c] = t;
+        else fz.G[(int64_t)a * k + (c - eta)] = t;
+      }
+    }
+    __syncthreads();
+  }
+  // last CTA out resets the barrier for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(fz.bar + 1, 1u) == (unsigned)G - 1) {
+      fz.bar[0] = 0u;
+      fz.bar[1] = 0u;
+      __threadfence();
     }
   }
 }

@@ -15,18 +15,6 @@ namespace somf {
 
 constexpr int kMaskThreads = 256;   // one Philox block (4 rows) per thread
 
-__device__ __forceinline__ uint32_t mask_bits(uint64_t seed, uint64_t t, int64_t blk,
-                                              int64_t row_lo, int64_t row_hi, uint64_t T) {
-  const U4 w = philox4x32_10(U4{(uint32_t)blk, (uint32_t)t, kStreamMask, (uint32_t)(blk >> 32)}, seed);
-  uint32_t bits = 0;
-#pragma unroll
-  for (int l = 0; l < 4; ++l) {
-    const int64_t row = blk * 4 + l;
-    if (row >= row_lo && row < row_hi && (uint64_t)u4_word(w, l) < T) bits |= 1u << l;
-  }
-  return bits;
-}
-
 // Pass 1: selected-row count per tile of kMaskThreads Philox blocks.
 __global__ void __launch_bounds__(kMaskThreads)
 k_mask_count(uint64_t seed, const int64_t* __restrict__ t_dev, int64_t row_lo, int64_t row_hi,

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -94,6 +95,17 @@ struct somf_ctx {
   std::string err;
   bool initialized = false;
   bool mask_ready = false;   // idx/q hold the draw of iteration t+1
+  bool begin_ready = false;  // t_dev / w_dev / perm hold iteration t+1 (drawn ahead)
+  bool ahead_ready = false;  // the *_next buffers hold iteration t+1 (BCD draw-ahead)
+  int32_t* idx_next = nullptr;
+  int32_t* perm_next = nullptr;
+  int* cnt_next = nullptr;
+  unsigned* ct_bar = nullptr;   // fused contract reduction barrier [arrivals, exits]
+  int ct_launches = 2;          // kernels the last launch_contract issued
+  int64_t* q_next = nullptr;
+  int64_t* t_next = nullptr;
+  double* w_next = nullptr;
+  int nt_mbits_off = 0;
   int64_t t_host = 0;
   // iterate
   float* D = nullptr;
@@ -132,7 +144,8 @@ struct somf_ctx {
   size_t oc_smem = 0;
   double* theta_ws = nullptr;
   const void* nt_fn = nullptr;   // simultaneous-threshold BCD (bcd_newton.cuh)
-  int nt_cap_rows = 0, nt_kpt = 0;
+  double nt_lam_tol = kNtLamTol;
+  int nt_cap_rows = 0, nt_kpt = 0, nt_threads = 0, nt_ct_in_w = 0, nt_part_in_cpi = 0;
   size_t nt_smem = 0;
   double* lam_ws = nullptr;
   double* nt_acc = nullptr;
@@ -143,7 +156,6 @@ struct somf_ctx {
   ShState sh{};
   bool sh_alloc = false;
   int* sh_conv_host = nullptr;     // pinned
-  unsigned* nt_accmm = nullptr;
   double* oc_acc = nullptr;
   unsigned* oc_accmin = nullptr;
   double* oc_rho = nullptr;
@@ -275,7 +287,7 @@ static const BbVariant kBbVariants[] = {
 #undef BBV
 
 typedef void (*Bb3Fn)(const int32_t*, const int64_t*, const float*, int64_t, int, const float*, int, int, float*,
-                      const double*, int);
+                      const double*, int, CbarFold);
 struct Bb3Variant { int kc, rt; Bb3Fn fn[2]; };   // [0] compact X, [1] gathered X
 #define BB3(KC, RT) {KC, RT, {k_bbar_v3<KC, RT, true>, k_bbar_v3<KC, RT, false>}}
 static const Bb3Variant kBb3Variants[] = {BB3(1, 4), BB3(1, 8), BB3(1, 16), BB3(2, 4), BB3(2, 8), BB3(2, 16),
@@ -284,8 +296,10 @@ static const Bb3Variant kBb3Variants[] = {BB3(1, 4), BB3(1, 8), BB3(1, 16), BB3(
 
 // Bbar rows (masked list, or all rows when !gather) -- bbar.cuh.  false when
 // the layout does not allow the 16-byte path (caller uses k_bbar_update).
+// *folded (optional) is set when the Cbar update rode along (v3 kernel, cpart ready)
 static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_t* q_dev, int64_t q_est,
-                           const float* X, int64_t ldx) {
+                           const float* X, int64_t ldx, bool* folded = nullptr) {
+  if (folded) *folded = false;
   const int k = h->cfg.k, eta = h->cfg.eta;
   if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15)) return false;
   int kc = (k + 31) / 32;
@@ -303,8 +317,13 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
       Bb3Fn fn = v3->fn[xcompact ? 0 : 1];
       if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
           cudaSuccess) {
+        CbarFold cf{};
+        if (folded && h->cpart_n > 0) {
+          cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32};
+          *folded = true;
+        }
         fn<<<h->nsm, kBbThreads, smem, h->st>>>(h->idx, q_dev, X, ldx, eta, h->AT32, h->kp, k, h->Bbar, h->w_dev,
-                                                (int)seg);
+                                                (int)seg, cf);
         return true;
       }
       cudaGetLastError();
@@ -340,7 +359,7 @@ static const CtVariant kCtVariants[] = {
 
 // v3 (whole-slice staging) variants: single output tile per CTA
 typedef void (*Ct3Fn)(const int32_t*, const int64_t*, const float*, int, int, const float*, int64_t, int, float*,
-                      int);
+                      int, CtFuse);
 struct Ct3Variant { int mt, nt; Ct3Fn fn[2]; };   // [0] compact X, [1] gathered X
 #define CT3(MT, NT) {MT, NT, {k_contract_v3<MT, NT, true>, k_contract_v3<MT, NT, false>}}
 static const Ct3Variant kCt3Variants[] = {CT3(2, 2), CT3(2, 4), CT3(2, 6), CT3(2, 9), CT3(4, 2), CT3(4, 4),
@@ -353,6 +372,7 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
                                    double* beta, double* G) {
   const int k = h->cfg.k;
   const int nc = m + k;
+  h->ct_launches = 2;
   const bool fast = (m % 4 == 0) && (ldx % 4 == 0) && (((uintptr_t)X & 15) == 0);
   if (fast && gather) {
     const Ct3Variant* v3 = nullptr;
@@ -368,7 +388,26 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
       const size_t smem = (size_t)seg * LDY * sizeof(float) + (size_t)seg * sizeof(int);
       Ct3Fn fn = v3->fn[xcompact ? 0 : 1];
       CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      fn<<<h->nsm, kCtThreads, smem, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial, seg);
+      int occ = 0;
+      static const bool fuse_off = std::getenv("SOMF_CT_FUSE") && std::atoi(std::getenv("SOMF_CT_FUSE")) == 0;
+      if (!fuse_off &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kCtThreads, smem) == cudaSuccess &&
+          occ >= 1) {
+        // split-K reduction fused behind one grid barrier (cooperative launch)
+        CtFuse fz{h->ct_bar, r, beta, G};
+        const int32_t* idxp = h->idx;
+        float* Dp = h->D;
+        int kp = h->kp, kk = k, mm = m, sg = seg;
+        float* part = h->partial;
+        int64_t ld = ldx;
+        void* args[] = {(void*)&idxp, (void*)&q_dev, (void*)&Dp, (void*)&kp, (void*)&kk, (void*)&X, (void*)&ld,
+                        (void*)&mm, (void*)&part, (void*)&sg, (void*)&fz};
+        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(h->nsm), dim3(kCtThreads), args, smem, h->st));
+        h->ct_launches = 1;
+        return SOMF_OK;
+      }
+      cudaGetLastError();
+      fn<<<h->nsm, kCtThreads, smem, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial, seg, CtFuse{});
       CKL();
       const int64_t tot = (int64_t)k * nc;
       k_contract_reduce2<<<(unsigned)ceil_div(tot, 32), 256, 0, h->st>>>(h->partial, h->nsm, k, m, r, beta, G);
@@ -501,47 +540,82 @@ static somf_status launch_mask(somf_ctx* h, const int64_t* t_dev_ptr, int64_t id
 // on-chip BCD variants: KC = columns per lane (ceil(kp/32), 5..7 -> 8),
 // RPW = masked rows per warp; R lives in RPW*KC registers per thread.
 // ---------------------------------------------------------------------------
-struct OcVariant { int kc, rpw; const void* fn; };
-#define OCV(KC, RPW) {KC, RPW, (const void*)k_bcd_onchip<KC, RPW>}
+// on-chip BCD variants (bcd_onchip_inst.cu): KC = columns per lane
+// (ceil(kp/32), 5..7 -> 8), RPW = masked rows per warp; R lives in RPW*KC
+// registers per thread.
+struct OcVariant { int kc, rpw; };
 static const OcVariant kOcVariants[] = {
-    OCV(1, 2), OCV(1, 4), OCV(1, 8), OCV(1, 12), OCV(1, 16), OCV(1, 24), OCV(1, 32),
-    OCV(2, 2), OCV(2, 4), OCV(2, 8), OCV(2, 12), OCV(2, 16), OCV(2, 24), OCV(2, 32),
-    OCV(3, 2), OCV(3, 4), OCV(3, 8), OCV(3, 12), OCV(3, 16), OCV(3, 24),
-    OCV(4, 2), OCV(4, 4), OCV(4, 8), OCV(4, 12), OCV(4, 16),
-    OCV(8, 2), OCV(8, 4), OCV(8, 8)};
-#undef OCV
+    {1, 2}, {1, 4}, {1, 8}, {1, 12}, {1, 16}, {1, 24}, {1, 32},
+    {2, 2}, {2, 4}, {2, 8}, {2, 12}, {2, 16}, {2, 24}, {2, 32},
+    {3, 2}, {3, 4}, {3, 8}, {3, 12}, {3, 16}, {3, 24},
+    {4, 2}, {4, 4}, {4, 8}, {4, 12}, {4, 16},
+    {8, 2}, {8, 4}, {8, 8}};
+const void* somf_oc_kernel(int kc, int rpw);
 
-struct NtVariant { int kpt; const void* fn; };
-#define NTV(K) {K, (const void*)k_bcd_newton<K>}
-static const NtVariant kNtVariants[] = {NTV(16), NTV(32), NTV(48), NTV(64), NTV(72), NTV(80), NTV(96)};
-#undef NTV
+// simultaneous-threshold BCD variants (bcd_newton_inst.cu, one object per KPT)
+#define NT_DECL(K) const void* somf_nt_kernel_##K(int T, int M, int gen);
+NT_DECL(16) NT_DECL(32) NT_DECL(48) NT_DECL(64) NT_DECL(72) NT_DECL(80) NT_DECL(96)
+#undef NT_DECL
+struct NtVariant { int kpt; const void* (*get)(int, int, int); };
+static const NtVariant kNtVariants[] = {{16, somf_nt_kernel_16}, {32, somf_nt_kernel_32}, {48, somf_nt_kernel_48},
+                                        {64, somf_nt_kernel_64}, {72, somf_nt_kernel_72}, {80, somf_nt_kernel_80},
+                                        {96, somf_nt_kernel_96}};
+
+// threads per group of M = 2 masked rows in the simultaneous-threshold kernel:
+// 4 (default), SOMF_NT_T=2 selects pairs (diagnostics / tuning)
+static int nt_threads_per_row() {
+  const char* e = std::getenv("SOMF_NT_T");
+  return (e && std::atoi(e) == 2) ? 2 : 4;
+}
 
 static void choose_newton(somf_ctx* h) {
   const int k = h->cfg.k;
   const int cap = (int)ceil_div(h->q_cap, h->nsm);
-  if (2 * cap > kNtThreads) return;                  // two threads per masked row
+  const int T = nt_threads_per_row();
+  const char* em = std::getenv("SOMF_NT_M");
+  const int M = (em && std::atoi(em) == 1) ? 1 : 2;
+  const int gen = h->cfg.mu > 0.0 || h->cfg.pos_dict;
+  const int max_thr = M == 1 ? 640 : NtCfg<4, 2>::kThreads;
+  const int64_t groups = ceil_div(cap, M);
+  if (T * groups > max_thr) return;
+  const int nthr = (int)std::max<int64_t>(64, ceil_div((int64_t)T * groups, 32) * 32);
   for (const NtVariant& v : kNtVariants) {
     if (v.kpt < k) continue;
+    const void* fn = v.get(T, M, gen);
+    if (!fn) return;
     const int LD = v.kpt + 1;
-    const int H = std::max(1, kNtThreads / k);
-    const size_t smem = (size_t)4 * (((size_t)cap * LD + 3) & ~(size_t)3) * sizeof(float) +
-                        (size_t)k * v.kpt * sizeof(float) +
-                        (size_t)H * v.kpt * (3 * sizeof(double) + 2 * sizeof(unsigned)) +
-                        (size_t)cap * sizeof(int) + 16;
-    if (smem > 200 * 1024) return;
-    if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    const int KT = v.kpt / T, KTS = (KT + 3) & ~3;
+    const size_t blk = ((size_t)(cap + 1) * LD + 3) & ~(size_t)3;
+    const size_t ct = (size_t)T * ((((size_t)v.kpt * KTS + 31) & ~(size_t)31) + 8);   // T x CTS (bcd_newton.cuh)
+    const int ct_in_w = ct <= blk;
+    const size_t H = std::max(1, nthr / k);
+    const size_t part = 5 * H * v.kpt;             // stats partials (words)
+    const int part_in_cpi = part <= (size_t)k * v.kpt;
+    const size_t base = ((size_t)4 * blk + (size_t)k * v.kpt + (ct_in_w ? 0 : ct) + (part_in_cpi ? 0 : part)) *
+                            sizeof(float) + (size_t)cap * sizeof(int) + 16;
+    // mask-bit scratch of the draw-ahead: one byte per Philox block of my slice
+    const int64_t nb = ((h->cfg.row_hi - 1) >> 2) - (h->cfg.row_lo >> 2) + 1;
+    const size_t mb_off = (base + 15) & ~(size_t)15;
+    const size_t smem = mb_off + (size_t)ceil_div(nb, h->nsm) + 16;
+    if (smem > 220 * 1024) return;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
       cudaGetLastError();
       return;
     }
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.fn, kNtThreads, smem) != cudaSuccess || occ < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, smem) != cudaSuccess || occ < 1) {
       cudaGetLastError();
       return;
     }
-    h->nt_fn = v.fn;
+    h->nt_fn = fn;
     h->nt_cap_rows = cap;
     h->nt_kpt = v.kpt;
     h->nt_smem = smem;
+    h->nt_threads = nthr;
+    h->nt_ct_in_w = ct_in_w;
+    h->nt_mbits_off = (int)mb_off;
+    if (const char* et = std::getenv("SOMF_NT_TOL")) h->nt_lam_tol = std::atof(et);
+    h->nt_part_in_cpi = part_in_cpi;
     return;
   }
 }
@@ -554,8 +628,10 @@ static void choose_onchip(somf_ctx* h) {
   if (kc > 4) kc = 8;
   const int need = (int)ceil_div(h->q_cap, h->nsm);
   const int cs = k <= 160;
-  for (const OcVariant& v : kOcVariants) {
-    if (v.kc != kc || v.rpw * kOcWarps < need) continue;
+  for (const OcVariant& ov : kOcVariants) {
+    if (ov.kc != kc || ov.rpw * kOcWarps < need) continue;
+    const struct { int kc, rpw; const void* fn; } v{ov.kc, ov.rpw, somf_oc_kernel(ov.kc, ov.rpw)};
+    if (!v.fn) return;
     const int cap = need;
     size_t smem = (size_t)cap * kp * sizeof(float) + (cs ? (size_t)((k * k + 3) & ~3) * sizeof(float) : 0) +
                   (size_t)((cap + 1) & ~1) * sizeof(float) + (size_t)k * (2 * sizeof(double) + sizeof(int));
@@ -708,6 +784,14 @@ static cudaError_t init_accmm(unsigned* mm, int n) {
   k_init_accmm<<<(n + 255) / 256, 256>>>(mm, n);
   return cudaGetLastError();
 }
+__global__ void k_init_nt_rec(double* rec, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) nt_rec_reset(rec + (size_t)i * kNtRec);
+}
+static cudaError_t init_nt_rec(double* rec, int n) {
+  k_init_nt_rec<<<(n + 255) / 256, 256>>>(rec, n);
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -784,9 +868,17 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->err_dev, 1));
   A(dalloc(&h->sweeps_dev, 1));
   A(dalloc(&h->idx, (size_t)rows));
+  A(dalloc(&h->idx_next, (size_t)rows));
+  A(dalloc(&h->q_next, 1));
+  A(dalloc(&h->t_next, 1));
+  A(dalloc(&h->w_next, 1));
   h->ntiles = (int)ceil_div(((c.row_hi - 1) >> 2) - (c.row_lo >> 2) + 1, kMaskThreads);
   A(dalloc(&h->tile_counts, (size_t)h->ntiles));
   A(dalloc(&h->perm, (size_t)k));
+  A(dalloc(&h->perm_next, (size_t)k));
+  A(dalloc(&h->cnt_next, (size_t)h->nsm));
+  A(dalloc(&h->ct_bar, 2));
+  A(cudaMemset(h->ct_bar, 0, 2 * sizeof(unsigned)));
   // [beta | G] contiguous: one allreduce when row-sharded
   A(dalloc(&h->beta64, (size_t)k * c.eta + (size_t)k * k));
   h->G64 = h->beta64 + (size_t)k * c.eta;
@@ -818,8 +910,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->oc_bar, 4));
   A(dalloc(&h->lam_ws, (size_t)k));
   A(dalloc(&h->bcd_prof, 80));
-  A(dalloc(&h->nt_acc, (size_t)kNtRing * k * 3));
-  A(dalloc(&h->nt_accmm, (size_t)kNtRing * k * 2));
+  A(dalloc(&h->nt_acc, (size_t)(kNtRing + 1) * k * kNtRec));
   if (c.bcd_kernel == 0 || c.bcd_kernel == 3) choose_newton(h);
   if (c.bcd_kernel == 0 ? !h->nt_fn : c.bcd_kernel == 2) choose_onchip(h);
   if ((c.bcd_kernel == 2 && !h->oc_fn) || (c.bcd_kernel == 3 && !h->nt_fn)) {
@@ -836,8 +927,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       cudaMemset(h->lam_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->AT32, 0, (size_t)c.eta * ((k + 3) & ~3) * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->bcd_prof, 0, 80 * sizeof(long long)) != cudaSuccess ||
-      cudaMemset(h->nt_acc, 0, (size_t)kNtRing * k * 3 * sizeof(double)) != cudaSuccess ||
-      init_accmm(h->nt_accmm, kNtRing * k) != cudaSuccess ||
+      init_nt_rec(h->nt_acc, (kNtRing + 1) * k) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->C64, 0, (size_t)k * k * sizeof(double)) != cudaSuccess ||
@@ -861,7 +951,7 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->partial, h->beta64, h->A64, h->A32, h->red, h->bar,
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
-                  h->lam_ws, h->nt_acc, h->nt_accmm, h->bcd_prof, h->cpart, h->AT32};
+                  h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->perm_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->sh_alloc) {
@@ -901,7 +991,7 @@ SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int6
   CK(cudaMemsetAsync(h->theta_ws, 0, (size_t)k * sizeof(double), h->st));
   CK(cudaMemsetAsync(h->lam_ws, 0, (size_t)k * sizeof(double), h->st));
   h->t_host = 0;
-  h->mask_ready = false;
+  h->mask_ready = h->begin_ready = h->ahead_ready = false;
   h->initialized = true;
   return post_call(h);
 }
@@ -926,6 +1016,16 @@ struct PhaseScope {
   }
 };
 
+// the draw-ahead buffers of the BCD kernel become the current ones
+static void swap_ahead(somf_ctx* h) {
+  std::swap(h->idx, h->idx_next);
+  std::swap(h->q_dev, h->q_next);
+  std::swap(h->perm, h->perm_next);
+  std::swap(h->t_dev, h->t_next);
+  std::swap(h->w_dev, h->w_next);
+  h->ahead_ready = false;
+}
+
 static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, bool compact) {
   const somf_config& c = h->cfg;
   const int k = c.k, eta = c.eta;
@@ -941,12 +1041,20 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     // t <- t+1, w_t, atom order and (unless drawn ahead by somf_next_mask) the
     // tile counts of M_t in one launch; the scatter of the index list in a second
     h->t_host += 1;
+    if (h->ahead_ready) {
+      // drawn ahead by the previous iteration's BCD kernel: swap the buffers in
+      swap_ahead(h);
+      h->begin_ready = h->mask_ready = true;
+    }
     const int nt = h->mask_ready ? 0 : h->ntiles;
-    k_step_mask_count<<<nt + 1, kMaskThreads, 0, h->st>>>(c.seed, h->t_host, c.u, c.row_lo, c.row_hi, h->T, nt,
-                                                          h->tile_counts, h->t_dev, h->w_dev, k, c.perm_cyclic,
-                                                          h->perm);
-    CKL();
-    h->launches[SOMF_PH_MASK] += 1;
+    if (!h->begin_ready) {
+      k_step_mask_count<<<nt + 1, kMaskThreads, 0, h->st>>>(c.seed, h->t_host, c.u, c.row_lo, c.row_hi, h->T, nt,
+                                                            h->tile_counts, h->t_dev, h->w_dev, k, c.perm_cyclic,
+                                                            h->perm);
+      CKL();
+      h->launches[SOMF_PH_MASK] += 1;
+    }
+    h->begin_ready = false;
     if (!h->mask_ready) {                                                    // M_t (Eq. mt)
       k_mask_scatter<<<h->ntiles, kMaskThreads, 0, h->st>>>(c.seed, h->t_dev, c.row_lo, c.row_hi, h->T,
                                                             h->tile_counts, c.row_lo, h->idx, h->q_dev);
@@ -973,24 +1081,14 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       return s;
     if (somf_status s = reduce(h, h->beta64, (int64_t)k * eta + (int64_t)k * k, SOMF_DT_F64, SOMF_OP_SUM))
       return s;
-    h->launches[SOMF_PH_CONTRACT] += 2;
+    h->launches[SOMF_PH_CONTRACT] += h->ct_launches;
   }
   {
     PhaseScope ps(h, SOMF_PH_CODES);                                         // Eq. somf_alpha
     if (somf_status s = launch_codes(h, h->G64, h->beta64, eta, c.cd_tol, h->A64, h->A32, true)) return s;
     h->launches[SOMF_PH_CODES] += 1;
   }
-  {
-    PhaseScope ps(h, SOMF_PH_CBAR);                                          // Eq. somf_partial
-    if (h->cpart_n > 0)
-      k_cbar_finalize<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->cpart, h->cpart_n, k, eta,
-                                                                                h->w_dev, h->C64, h->C32);
-    else
-      k_cbar_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->A64, k, eta, h->w_dev, h->C64,
-                                                                                h->C32);
-    CKL();
-    h->launches[SOMF_PH_CBAR] += 1;
-  }
+  bool cbar_folded = false;
   {
     PhaseScope ps(h, SOMF_PH_BBAR);
     const int grid_a = (int)ceil_div(k, TN);
@@ -1002,7 +1100,8 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
             nullptr, h->qfull_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
       }
       h->launches[SOMF_PH_BBAR] += 2;
-    } else if (launch_bbar_v2(h, true, compact, h->q_dev, q_est, Xd, ld)) {
+    } else if (launch_bbar_v2(h, true, compact, h->q_dev, q_est, Xd, ld, &cbar_folded)) {
+      // (Cbar rides along when cbar_folded: Eq. somf_partial)
       h->launches[SOMF_PH_BBAR] += 1;
     } else {
       const int grid_r = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q_est, TM), 8 * h->nsm));
@@ -1015,6 +1114,17 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       h->launches[SOMF_PH_BBAR] += 1;
     }
     CKL();
+  }
+  if (!cbar_folded) {
+    PhaseScope ps(h, SOMF_PH_CBAR);                                          // Eq. somf_partial
+    if (h->cpart_n > 0)
+      k_cbar_finalize<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->cpart, h->cpart_n, k, eta,
+                                                                                h->w_dev, h->C64, h->C32);
+    else
+      k_cbar_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->A64, k, eta, h->w_dev, h->C64,
+                                                                                h->C32);
+    CKL();
+    h->launches[SOMF_PH_CBAR] += 1;
   }
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
@@ -1037,16 +1147,33 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.b = c.mu;
       na.pos = c.pos_dict;
       na.cap_rows = h->nt_cap_rows;
+      na.ct_in_w = h->nt_ct_in_w;
       na.max_rounds = 3 * k + 20;
-      na.acc = h->nt_acc;
-      na.accmm = h->nt_accmm;
-      na.rho_acc = h->oc_rho;
+      na.lam_tol = h->nt_lam_tol;
+      // draw-ahead of t+1 (mask, atom order, t, w) inside the rounds
+      na.idx_next = h->idx_next;
+      na.q_next = h->q_next;
+      na.perm_next = h->perm_next;
+      na.cnt_next = h->cnt_next;
+      na.t_next = h->t_next;
+      na.w_next = h->w_next;
+      na.seed = c.seed;
+      na.Tthr = h->T;
+      na.tn = h->t_host + 1;
+      na.row_lo = c.row_lo;
+      na.row_hi = c.row_hi;
+      na.u = c.u;
+      na.cyclic = c.perm_cyclic;
+      na.mbits_off = h->nt_mbits_off;
+      na.rec = h->nt_acc;
+      na.part_in_cpi = h->nt_part_in_cpi;
       na.bar = h->oc_bar;
       na.nred_out = h->nred_dev;
       na.err = h->err_dev;
       na.prof = h->prof_on ? h->bcd_prof : nullptr;
       void* kargs[] = {&na};
-      CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(kNtThreads), kargs, h->nt_smem, h->st));
+      CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(h->nt_threads), kargs, h->nt_smem, h->st));
+      h->ahead_ready = true;
     } else if (h->oc_fn) {
       OcArgs oa{};
       oa.idx = h->idx;
@@ -1110,6 +1237,10 @@ SOMF_EXPORT somf_status somf_partial_fit(somf_handle h, const float* X, int64_t 
 SOMF_EXPORT somf_status somf_next_mask(somf_handle h, int64_t* q_out, int32_t* idx_out) {
   if (!h) return SOMF_E_ARG;
   const somf_config& c = h->cfg;
+  if (h->ahead_ready) {
+    swap_ahead(h);                                  // M_{t+1}, pi_{t+1}, t+1, w_{t+1} already drawn
+    h->begin_ready = h->mask_ready = true;
+  }
   if (!h->mask_ready) {
     // draw M_{t+1}: the mask kernels read t from a device scalar
     k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->t_host + 1);
@@ -1256,7 +1387,7 @@ SOMF_EXPORT somf_status somf_set_state(somf_handle h, const float* D, const floa
   CK(cudaMemsetAsync(h->lam_ws, 0, (size_t)k * sizeof(double), h->st));
   CK(cudaStreamSynchronize(h->st));
   h->t_host = t;
-  h->mask_ready = false;
+  h->mask_ready = h->begin_ready = h->ahead_ready = false;
   h->initialized = true;
   return post_call(h);
 }

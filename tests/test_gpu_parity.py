@@ -216,6 +216,34 @@ def test_set_components_projects_and_slacks(somf):
         assert st["t"] == 0 and np.abs(st["Cbar"]).max() == 0 and np.abs(st["Bbar"]).max() == 0
 
 
+@pytest.mark.parametrize("name", ["ridge_l1_fmri_small", "enet_enet", "nmf_small"])
+def test_draw_ahead_multi_step(somf, name):
+    """The simultaneous-threshold BCD kernel draws M_{t+1}, pi_{t+1}, t+1 and
+    w_{t+1} while it runs; the next step consumes them.  Three
+    consecutive steps from a loaded state: after each, the mask the handle
+    reports for t+1 is the oracle's bit for bit, and the state after the
+    three steps matches the oracle (each step is pinned one by one in
+    test_one_step_parity)."""
+    ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel="newton")
+    r = CASES[name][3]["r"]
+    for s in range(3):
+        batch = X[:, k + (5 + s) * eta:k + (6 + s) * eta]
+        out = ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+        info = gpu.last_step_info()
+        assert info["q"] == out["S"].size
+        assert abs(info["w"] - ora.t ** -CASES[name][3].get("u", 0.917)) <= 1e-15
+        st = gpu.get_state()
+        errs = dict(Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar), D=rel(st["D"], ora.D))
+        assert all(v <= TOL_STEP for v in errs.values()), (s, errs)
+        # continue from the GPU's float32 state so the steps stay independent pins
+        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
+                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
+    q, idx = gpu.next_mask()
+    ref_S = ostreams.mask_rows(3, ora.t + 1, p, r)
+    assert q == ref_S.size and np.array_equal(idx, ref_S)
+
+
 # ---------------------------------------------------------------------------
 # trajectory: objective after 100 iterations
 # ---------------------------------------------------------------------------
