@@ -419,13 +419,16 @@ def run_somf(args):
     if bcd_cyc["launches"]:
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
         roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
-                                         if ph not in ("launches", "unconverged_per_round", "ridge", "setup_split")}
+                                         if ph not in ("launches", "unconverged_per_round", "frozen_prefix_per_round", "ridge",
+                                                       "setup_split")}
         roof["ridge_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["ridge"].items()}
         roof["bcd_setup_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["setup_split"].items()}
         unc = [u / bcd_cyc["launches"] for u in bcd_cyc["unconverged_per_round"]]
         while unc and unc[-1] == 0:
             unc.pop()
         roof["bcd_unconverged_atoms_per_round"] = [round(u, 2) for u in unc]
+        roof["bcd_frozen_prefix_per_round"] = [round(f / bcd_cyc["launches"], 2)
+                                               for f in bcd_cyc["frozen_prefix_per_round"][:len(unc)]]
     sb = step_bytes(q, k, eta)
     step_roof = {"bytes_per_step": sb, "achieved_gbs": sb / (step_ms * 1e-3) / 1e9,
                  "frac_of_hbm": sb / (step_ms * 1e-3) / 1e9 / peaks["hbm"]}

@@ -30,15 +30,17 @@
 namespace somf {
 
 constexpr int kNtRing = 3;
+constexpr int kNtMaxK = 96;         // largest k of the simultaneous-threshold kernel
 constexpr int kNtRec = 16;          // doubles per accumulator record (128 bytes)
 // Convergence: every atom exact (its active set reproduces itself) and its
 // lambda stable to this relative tolerance between two rounds.  The
 // recurrence runs in fp32 (v, d carry ~1e-7 relative rounding); a lambda
-// moving by < 1e-6 relative moves d by < 1e-6 of the threshold, far inside the
-// 1e-4 parity tolerance, while a tighter test only waits for rounding noise of
-// early atoms to stop rippling down the chain (1e-8: 12.1 rounds per step at
-// cfgC r=12, 1e-6: 9.6).  SOMF_NT_TOL overrides it.
-constexpr double kNtLamTol = 1e-6;
+// moving by < 1e-5 relative moves d by < 1e-5 of the threshold, inside the 1e-4
+// parity tolerance (and the slack norms stay within 1e-5), while a tighter test
+// only waits for perturbations of earlier atoms to die out down the chain
+// (cfgC r=12: 1e-8 12.1 rounds per step, 1e-6 9.6, 1e-5 8.9; 1e-4 fails the
+// slack bound).  SOMF_NT_TOL overrides it.
+constexpr double kNtLamTol = 1e-5;
 
 struct NtArgs {
   const int32_t* idx;       // masked local rows (ascending)
@@ -49,7 +51,9 @@ struct NtArgs {
   const float* C32;         // k x k
   double* nslack;           // k (atom index)
   double* lam_ws;           // k (atom index): lambda of the previous pass
-  const int32_t* perm;      // k
+  const int32_t* perm;      // k (device; used when perm_v is not filled)
+  int32_t perm_v[kNtMaxK];  // pi_t by value (drawn on the host, R13), perm_by_value = 1
+  int perm_by_value;
   int k, kp;
   double a, b;              // 1 - mu, mu
   int pos;                  // D >= 0
@@ -66,11 +70,10 @@ struct NtArgs {
   double* rec;
   // draw-ahead of iteration t+1 while the CTAs wait on the rounds (null idx_next
   // = off): M_{t+1} (Eq. mt) into idx_next / q_next (per-CTA counts through
-  // cnt_next, published before round 0's barrier), pi_{t+1} into perm_next,
-  // t+1 and w_{t+1} = (t+1)^-u into t_next / w_next.
+  // cnt_next, published before round 0's barrier), t+1 and w_{t+1} = (t+1)^-u
+  // into t_next / w_next.  (pi_{t+1} is drawn on the host: perm_v.)
   int32_t* idx_next;
   int64_t* q_next;
-  int32_t* perm_next;
   int* cnt_next;            // gridDim.x
   int64_t* t_next;
   double* w_next;
@@ -193,8 +196,8 @@ __device__ __forceinline__ void nt_red_add(double* p, double v) {
 // updates its own later positions of its M rows with the prescaled Cbar row
 // Ct[t][PP][i] = c_{PP, iT+t} / c_{iT+t, iT+t}; each 16-byte shared load of
 // Ct serves M rows (shared-memory wavefronts are the limit of this loop).
-// Positions below the frozen prefix F (atoms whose threshold is final, see
-// the kernel) are skipped: their effect is already folded into R.
+// Straight-line code over the positions (no per-position branch), so the
+// scheduler can overlap one position's chain with the previous one's updates.
 // Per-atom parameters: simple case (mu = 0, no D >= 0) the threshold alone
 // (theta = +inf zeroes the atom); generic case {theta, 1/(1+b lam), v_lo}.
 // Only v is stored: d is a function of v and the round's parameters.
@@ -221,10 +224,10 @@ struct NtRec5 {
   static constexpr int KT = KPT / T;
   static constexpr int KTS = (KT + 3) & ~3;
   static __device__ __forceinline__ void run(float (&R)[M][KPT / T], const float (&Do)[M][KPT / T], int t,
-                                             int F, float* __restrict__ v0, int vstride,
+                                             float* __restrict__ v0, int vstride,
                                              const float* __restrict__ Ct_t, const NtPar<kGen>* __restrict__ par) {
     constexpr int own = PP % T, ii = PP / T;
-    if (PP >= F) {                                   // uniform: frozen prefix skipped
+    {
       const NtPar<kGen> pr = par[PP];
       float delta[M];
 #pragma unroll
@@ -257,13 +260,13 @@ struct NtRec5 {
         }
       }
     }
-    NtRec5<KPT, T, M, kGen, PP + 1>::run(R, Do, t, F, v0, vstride, Ct_t, par);
+    NtRec5<KPT, T, M, kGen, PP + 1>::run(R, Do, t, v0, vstride, Ct_t, par);
   }
 };
 template <int KPT, int T, int M, bool kGen>
 struct NtRec5<KPT, T, M, kGen, KPT> {
-  static __device__ __forceinline__ void run(float (&)[M][KPT / T], const float (&)[M][KPT / T], int, int, float*,
-                                             int, const float*, const NtPar<kGen>*) {}
+  static __device__ __forceinline__ void run(float (&)[M][KPT / T], const float (&)[M][KPT / T], int, float*, int,
+                                             const float*, const NtPar<kGen>*) {}
 };
 
 template <int T, int M>
@@ -289,13 +292,12 @@ __device__ __forceinline__ NtPar<true> nt_make_par<true>(int mode, double a, dou
   return p;
 }
 
-// Rounds with a frozen prefix.  After each round's update, the atoms
-// [F, F') whose thresholds converged, F' the first unconverged position, are
-// FROZEN with the parameters this round used (so the round's v of those
-// positions is final); their deltas are folded into the initial residual of
-// the later positions once, and later rounds run the recurrence from F'
-// only.  Convergence (exact active set, lambda stable to kNtLamTol) needs the
-// predecessors fixed, so the converged set grows from the front.
+// Rounds: every round runs the recurrence over all atoms with the current
+// thresholds; the iteration ends when every atom is exact and its lambda is
+// stable (then the round's v and parameters give Alg. 4's D).  (A frozen
+// prefix -- skipping converged leading atoms -- was measured not to help:
+// at cfgC the atoms converge out of order, the leading converged run stays
+// near 0 until the last rounds.)
 template <int KPT, int T, int M, bool kGen>
 __global__ void __launch_bounds__(NtCfg<T, M>::kThreads, 1)
 k_bcd_newton(NtArgs P) {
@@ -313,7 +315,6 @@ k_bcd_newton(NtArgs P) {
   __shared__ int mode_s[KPT], jmap_s[KPT], pinv_s[KPT];
   __shared__ double dmax_s;
   __shared__ double diag_s[KPT], lws_s[KPT], ns_s[KPT];
-  __shared__ int fnew_s[2];   // first unconverged position, double-buffered by round parity
   __shared__ int mcnt_s;      // selected rows of M_{t+1} in my slice
   const int k = P.k, kp = P.kp;
   const int nthr = blockDim.x;
@@ -347,7 +348,7 @@ k_bcd_newton(NtArgs P) {
   asm volatile("cp.async.commit_group;" ::: "memory");
   for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + r];
   for (int p = tid; p < k; p += nthr) {
-    jmap_s[p] = P.perm[p];
+    jmap_s[p] = P.perm_by_value ? P.perm_v[p] : P.perm[p];
     diag_s[p] = P.C64[(int64_t)p * k + p];
     lws_s[p] = P.lam_ws[p];
     ns_s[p] = P.nslack[p];
@@ -411,7 +412,6 @@ k_bcd_newton(NtArgs P) {
       par_s[0][p] = par_s[1][p] = nt_make_par<kGen>(kModeDead, a, b, 0.0, -INFINITY);
     }
   }
-  if (tid == 0) fnew_s[0] = fnew_s[1] = k;
   asm volatile("cp.async.wait_group 1;" ::: "memory");     // Cbar staged
   __syncthreads();
   for (int e = tid; e < k * KPT; e += nthr) {
@@ -523,7 +523,8 @@ k_bcd_newton(NtArgs P) {
   if (P.idx_next && tid == 0) P.cnt_next[blockIdx.x] = mcnt_s;   // before round 0's barrier
   NT_MARK(0);
   unsigned nbar = 0;
-  int round = 0, cur = 0, F = 0;
+  int round = 0, cur = 0;
+  constexpr int F = 0;          // (no frozen prefix: every round runs every atom)
   bool done = q == 0;
 #pragma unroll 1
   while (!done) {
@@ -538,7 +539,7 @@ k_bcd_newton(NtArgs P) {
         for (int i = 0; i < KT; ++i) R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
       // rows rowx[0] and rowx[0] + vstride (vstride = LD for consecutive rows; the
       // spare row is its own target when both are past nr)
-      NtRec5<KPT, T, M, kGen, 0>::run(R, Do, tq, F, V + (size_t)rowx[0] * LD,
+      NtRec5<KPT, T, M, kGen, 0>::run(R, Do, tq, V + (size_t)rowx[0] * LD,
                                       M > 1 ? vstride * LD : 0, Ct_t, par_s[cur]);
     }
     __syncthreads();
@@ -625,11 +626,10 @@ k_bcd_newton(NtArgs P) {
       const double mnv = cnt > 0.0 ? (double)__uint_as_float(mnb) : INFINITY;
       const double mxv = (double)__uint_as_float(mxb);
       conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol);
-      if (!conv) atomicMin(&fnew_s[round & 1], p);
     }
-    __syncthreads();
-    const int Fn = fnew_s[round & 1];
-    if (tid == 0) fnew_s[(round + 1) & 1] = k;      // nobody reads that slot this round
+    // every atom converged: the round's v and parameters are final (a frozen
+    // prefix was measured not to help: atoms converge out of order)
+    const int Fn = __syncthreads_and(conv) ? k : 0;
     const bool capped = round + 1 >= P.max_rounds && Fn < k;
     if (act) {
       if (p < Fn || capped) {
@@ -651,7 +651,7 @@ k_bcd_newton(NtArgs P) {
     if (P.prof && blockIdx.x == 0) {
       // convergence profile: unconverged atoms per round (slots 8..71)
       const int nun = __syncthreads_count(act && !conv);
-      if (tid == 0 && round < 64) P.prof[8 + round] += nun;
+      if (tid == 0 && round < 64) P.prof[8 + round] += nun + ((long long)F << 16);   // (F << 16) + unconverged
     }
     NT_MARK(4);
     ++round;
@@ -661,66 +661,19 @@ k_bcd_newton(NtArgs P) {
       if (tid == 0 && blockIdx.x == 0) atomicExch(P.err, 4);
       done = true;
     }
-    if (!done) {
-      // fold the newly frozen atoms [F, Fn) into the initial residual of my rows
-      if (Fn > F) {
-        float R[M][KT];
-#pragma unroll
-        for (int m = 0; m < M; ++m)
-#pragma unroll
-          for (int i = 0; i < KT; ++i) R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
-        for (int j = F; j < Fn; ++j) {
-          const NtPar<kGen> pr = par_s[cur][j];
-          const float* crow = Ct_t + j * KTS;
-          float delta[M];
-#pragma unroll
-          for (int m = 0; m < M; ++m) {
-            const float v = V[(size_t)rowx[m] * LD + j];
-            const float dj = pr.d_of(v);
-            delta[m] = dj - Dold[(size_t)rowx[m] * LD + j];
-          }
-#pragma unroll
-          for (int j4 = 0; j4 < KTS / 4; ++j4) {
-            const float4 c = *reinterpret_cast<const float4*>(crow + 4 * j4);
-            const float cc[4] = {c.x, c.y, c.z, c.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int i = 4 * j4 + e;
-              if (i < KT) {
-                const int l = i * T + tq;
-                if (l > j) {
-#pragma unroll
-                  for (int m = 0; m < M; ++m) R[m][i] = fmaf(-delta[m], cc[e], R[m][i]);
-                }
-              }
-            }
-          }
-        }
-        __syncthreads();   // every thread read its R0 before anyone writes
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-          if (rowx[m] == cap) continue;
-#pragma unroll
-          for (int i = 0; i < KT; ++i) Rini[(size_t)rowx[m] * LD + i * T + tq] = R[m][i];
-        }
-      }
-      F = Fn;
-      cur ^= 1;
-      __syncthreads();
-    }
+    if (!done) cur ^= 1;
   }
   __syncthreads();
   NT_MARK(5);
   // ---- final D = the v of each atom's final round through its parameters, atom order ----
-  // (with the draw-ahead on, the last warp scatters M_{t+1} and, in CTA 0, warp
-  // 0 draws pi_{t+1}: both stay out of the write-back so the three overlap)
+  // (with the draw-ahead on, the last warp scatters M_{t+1} and stays out of
+  // the write-back so the two overlap)
   const int nwarp_all = nthr >> 5;
   const bool ahead = P.idx_next != nullptr && nwarp_all >= 4;
-  if (q > 0 && !(ahead && (wid == nwarp_all - 1 || (blockIdx.x == 0 && wid == 0)))) {
+  if (q > 0 && !(ahead && wid == nwarp_all - 1)) {
     const NtPar<kGen>* pr = par_s[cur];
-    const int w0 = (ahead && blockIdx.x == 0) ? 1 : 0;
-    const int nwarp = ahead ? nwarp_all - 1 - w0 : nwarp_all;
-    for (int r = wid - w0; r < nr; r += nwarp) {
+    const int nwarp = ahead ? nwarp_all - 1 : nwarp_all;
+    for (int r = wid; r < nr; r += nwarp) {
       float* dst = P.D + (int64_t)rows_s[r] * kp;
       const float* src = V + (size_t)r * LD;
       for (int j = lane; j < k; j += 32) {
@@ -729,7 +682,7 @@ k_bcd_newton(NtArgs P) {
       }
     }
   }
-  // ---- draw-ahead of t+1: scatter of my slice of M_{t+1}, pi_{t+1}, t+1, w_{t+1} -----
+  // ---- draw-ahead of t+1: scatter of my slice of M_{t+1}, t+1, w_{t+1} ------------------
   if (P.idx_next) {
     const int nwarp = nthr >> 5;
     if (wid == nwarp - 1) {
@@ -755,36 +708,9 @@ k_bcd_newton(NtArgs P) {
       }
       if (blockIdx.x == G - 1 && lane == 31) *P.q_next = pos;
     }
-    if (blockIdx.x == 0 && wid == 0) {
-      // Alg. 4's atom order of t+1 (R13): words drawn by the warp, swaps by lane 0
-      // scratch the other warps' write-back does not read: >= k words each
-      int32_t* pi = reinterpret_cast<int32_t*>(par_s[cur ^ 1]);
-      uint32_t* words = reinterpret_cast<uint32_t*>(lam_s);
-      __syncwarp();
-      for (int i = lane; i < k; i += 32) pi[i] = i;
-      if (!P.cyclic) {
-        for (int bq = lane; bq * 4 < k - 1; bq += 32) {
-          const U4 w = philox4x32_10(U4{(uint32_t)bq, (uint32_t)P.tn, kStreamPerm, 0u}, P.seed);
-          for (int l = 0; l < 4; ++l)
-            if (bq * 4 + l < k - 1) words[bq * 4 + l] = u4_word(w, l);
-        }
-      }
-      __syncwarp();
-      if (!P.cyclic && lane == 0) {
-        for (int w = 0; w < k - 1; ++w) {
-          const int i = k - 1 - w;
-          const int j = (int)(((uint64_t)words[w] * (uint64_t)(i + 1)) >> 32);
-          const int32_t tmp = pi[i];
-          pi[i] = pi[j];
-          pi[j] = tmp;
-        }
-      }
-      __syncwarp();
-      for (int i = lane; i < k; i += 32) P.perm_next[i] = pi[i];
-      if (lane == 0) {
-        *P.t_next = P.tn;
-        *P.w_next = pow((double)P.tn, -P.u);
-      }
+    if (blockIdx.x == 0 && wid == 0 && lane == 0) {
+      *P.t_next = P.tn;
+      *P.w_next = pow((double)P.tn, -P.u);
     }
   }
   // ---- exit: last CTA resets counters and accumulators ------------------------------

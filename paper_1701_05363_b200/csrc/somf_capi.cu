@@ -98,7 +98,6 @@ struct somf_ctx {
   bool begin_ready = false;  // t_dev / w_dev / perm hold iteration t+1 (drawn ahead)
   bool ahead_ready = false;  // the *_next buffers hold iteration t+1 (BCD draw-ahead)
   int32_t* idx_next = nullptr;
-  int32_t* perm_next = nullptr;
   int* cnt_next = nullptr;
   unsigned* ct_bar = nullptr;   // fused contract reduction barrier [arrivals, exits]
   int ct_launches = 2;          // kernels the last launch_contract issued
@@ -875,7 +874,6 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   h->ntiles = (int)ceil_div(((c.row_hi - 1) >> 2) - (c.row_lo >> 2) + 1, kMaskThreads);
   A(dalloc(&h->tile_counts, (size_t)h->ntiles));
   A(dalloc(&h->perm, (size_t)k));
-  A(dalloc(&h->perm_next, (size_t)k));
   A(dalloc(&h->cnt_next, (size_t)h->nsm));
   A(dalloc(&h->ct_bar, 2));
   A(cudaMemset(h->ct_bar, 0, 2 * sizeof(unsigned)));
@@ -951,7 +949,7 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->partial, h->beta64, h->A64, h->A32, h->red, h->bar,
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
-                  h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->perm_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32};
+                  h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->sh_alloc) {
@@ -1016,11 +1014,25 @@ struct PhaseScope {
   }
 };
 
+// Alg. 4's atom order pi_t on the host (R13): Fisher-Yates from the top with
+// j = floor(word_w (i+1) / 2^32), word w of Philox((w>>2, t, 2, 0)) -- the
+// arithmetic of atom_perm_cta (mask.cuh), bit for bit.
+static void host_atom_perm(uint64_t seed, uint64_t t, int k, int cyclic, int32_t* pi) {
+  for (int i = 0; i < k; ++i) pi[i] = i;
+  if (cyclic) return;
+  for (int w = 0; w < k - 1; ++w) {
+    const U4 x = philox4x32_10(U4{(uint32_t)(w >> 2), (uint32_t)t, kStreamPerm, 0u}, seed);
+    const uint32_t word = u4_word(x, w & 3);
+    const int i = k - 1 - w;
+    const int j = (int)(((uint64_t)word * (uint64_t)(i + 1)) >> 32);
+    std::swap(pi[i], pi[j]);
+  }
+}
+
 // the draw-ahead buffers of the BCD kernel become the current ones
 static void swap_ahead(somf_ctx* h) {
   std::swap(h->idx, h->idx_next);
   std::swap(h->q_dev, h->q_next);
-  std::swap(h->perm, h->perm_next);
   std::swap(h->t_dev, h->t_next);
   std::swap(h->w_dev, h->w_next);
   h->ahead_ready = false;
@@ -1141,6 +1153,9 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.nslack = h->nslack;
       na.lam_ws = h->lam_ws;
       na.perm = h->perm;
+      // pi_t drawn on the host (same Philox words and swaps as atom_perm_cta, R13)
+      host_atom_perm(c.seed, (uint64_t)h->t_host, k, c.perm_cyclic, na.perm_v);
+      na.perm_by_value = 1;
       na.k = k;
       na.kp = h->kp;
       na.a = 1.0 - c.mu;
@@ -1153,7 +1168,6 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       // draw-ahead of t+1 (mask, atom order, t, w) inside the rounds
       na.idx_next = h->idx_next;
       na.q_next = h->q_next;
-      na.perm_next = h->perm_next;
       na.cnt_next = h->cnt_next;
       na.t_next = h->t_next;
       na.w_next = h->w_next;
