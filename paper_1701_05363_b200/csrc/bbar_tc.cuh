@@ -1,0 +1,210 @@
+// bbar_tc.cuh -- (a3) masked-row surrogate aggregation on the tensor cores:
+//   P_t Bbar <- (1 - w) P_t Bbar + (w / eta) X_M A^T      (Eq. somf_partial
+//   P:602, masked rows only (north star), batch mean R4)
+// as one tcgen05 GEMM per tile of 128 masked rows: D[rows x k] = X_M[rows x eta]
+// . A[k x eta]^T, fp32 accumulator in TMEM.  fp32 operands are split into two
+// bf16 terms (x = hi + lo, |x - hi - lo| <= 2^-17 |x|) and three products
+// hi.hi + hi.lo + lo.hi are accumulated (bf16x3: per-product error ~2^-16,
+// DESIGN.md §5), kind::f16, K = 16 per instruction.
+//
+// One CTA per SM owns ~q / #SMs masked rows (tiles of 128).  Staging: the
+// codes (B operand, N = k rounded up to 16) once per CTA, the masked X rows
+// (A operand, M = 128) per tile, both written split and in the K-major
+// SWIZZLE_NONE core-matrix layout of tc_common.cuh; the old Bbar rows by
+// cp.async.  Thread 0 issues the 3 x ceil(eta/16) MMAs, commits to an
+// mbarrier; the epilogue (warp w: TMEM lanes 32 (w % 4) .., column half w / 4)
+// reads the accumulator and writes keep * Bbar_old + add * acc.
+// Optionally folds the Cbar update (CbarFold, as k_bbar_v3).
+#pragma once
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "bbar.cuh"
+
+namespace somf {
+
+constexpr int kBtThreads = 256;
+constexpr int kBtM = 128;
+
+struct BtArgs {
+  const int32_t* idx;       // masked local rows (ascending): the Bbar rows
+  int xcompact;             // X holds only the masked rows (row m of X = m-th masked row)
+  const int64_t* q_dev;
+  const float* X;           // rows x ldx (or q x ldx when compact)
+  int64_t ldx;
+  int eta, k, kp;
+  const float* A;           // codes k x eta (fp32, row-major)
+  float* Bbar;              // rows x kp
+  const double* w_dev;
+  int np;                   // N: k rounded up to 16
+  int ep;                   // eta rounded up to 16
+  CbarFold cf;
+};
+
+__device__ __forceinline__ void bt_split(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+// one 16-byte K chunk (8 values) of one operand row: split and store hi / lo
+__device__ __forceinline__ void bt_store_chunk(const float (&v)[8], uint8_t* hi_base, uint8_t* lo_base,
+                                               uint32_t off) {
+  __align__(16) __nv_bfloat16 h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) bt_split(v[i], h[i], l[i]);
+  *reinterpret_cast<uint4*>(hi_base + off) = *reinterpret_cast<const uint4*>(h);
+  *reinterpret_cast<uint4*>(lo_base + off) = *reinterpret_cast<const uint4*>(l);
+}
+
+// 8 consecutive floats of a row of length len starting at s (zeros past len)
+__device__ __forceinline__ void bt_load8(const float* row, int s, int len, bool streaming, float (&v)[8]) {
+  if (s + 8 <= len && ((reinterpret_cast<uintptr_t>(row + s) & 15) == 0)) {
+    const float4 a = streaming ? __ldcs(reinterpret_cast<const float4*>(row + s))
+                               : __ldg(reinterpret_cast<const float4*>(row + s));
+    const float4 b = streaming ? __ldcs(reinterpret_cast<const float4*>(row + s + 4))
+                               : __ldg(reinterpret_cast<const float4*>(row + s + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = s + i < len ? row[s + i] : 0.f;
+  }
+}
+
+// byte offset of element (row, kk) in a K-major SWIZZLE_NONE bf16 operand with
+// LBO = 128 (K chunks adjacent) and SBO = 128 * nch (8-row groups)
+__device__ __forceinline__ uint32_t bt_off(int row, int kk, int nch) {
+  return (uint32_t)((row >> 3) * 128 * nch + (kk >> 3) * 128 + (row & 7) * 16 + (kk & 7) * 2);
+}
+
+__global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
+  extern __shared__ __align__(128) uint8_t bt_smem[];
+  __shared__ uint32_t tmem_s;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ int grow[kBtM];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int eta = P.eta, k = P.k, kp = P.kp, np = P.np, ep = P.ep, nch = ep / 8;
+  const int G = gridDim.x;
+  const int64_t q = *P.q_dev;
+  const double w = *P.w_dev;
+  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
+  const size_t a_bytes = (size_t)kBtM * ep * 2, b_bytes = (size_t)np * ep * 2;
+  uint8_t* Ahi = bt_smem;
+  uint8_t* Alo = Ahi + a_bytes;
+  uint8_t* Bhi = Alo + a_bytes;
+  uint8_t* Blo = Bhi + b_bytes;
+  float* Bold = reinterpret_cast<float*>(Blo + b_bytes);        // 128 x kp
+  if (P.cf.cpart) {
+    // my slice of the Cbar entries (Eq. somf_partial)
+    const int e0 = (int)((int64_t)P.cf.kk * blockIdx.x / G), e1 = (int)((int64_t)P.cf.kk * (blockIdx.x + 1) / G);
+    for (int e = e0 + tid; e < e1; e += kBtThreads) {
+      double s = 0.0;
+      for (int bq = 0; bq < P.cf.nparts; ++bq) s += P.cf.cpart[(size_t)bq * P.cf.kk + e];
+      const double c = (1.0 - w) * P.cf.C64[e] + (w / eta) * s;
+      P.cf.C64[e] = c;
+      P.cf.C32[e] = (float)c;
+    }
+  }
+  if (hi <= lo) return;
+  if (wid == 0) tc_alloc(&tmem_s, np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256);
+  if (tid == 0) mbar_init(&mbar, 1);
+  // ---- B = codes (N = np x K = ep), split, once per CTA ------------------------------
+  for (int e = tid; e < np * nch; e += kBtThreads) {
+    const int n = e % np, c = e / np;              // n fastest: conflict-free 16-byte stores
+    float v[8];
+    if (n < k) bt_load8(P.A + (int64_t)n * eta, 8 * c, eta, false, v);
+    else
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    bt_store_chunk(v, Bhi, Blo, bt_off(n, 8 * c, nch));
+  }
+  const uint32_t idesc = tc_idesc_bf16(kBtM, np);
+  uint32_t phase = 0;
+  for (int64_t t0 = lo; t0 < hi; t0 += kBtM) {
+    const int n = (int)(hi - t0 < (int64_t)kBtM ? hi - t0 : (int64_t)kBtM);
+    __syncthreads();                                   // previous tile's epilogue done with smem
+    for (int r = tid; r < kBtM; r += kBtThreads) grow[r] = r < n ? P.idx[t0 + r] : 0;
+    __syncthreads();
+    // old Bbar rows of the tile (async; consumed by the epilogue)
+    for (int e = tid; e < n * (kp / 4); e += kBtThreads) {
+      const int r = e / (kp / 4), c = e % (kp / 4);
+      const unsigned d = smem_u32(Bold + (size_t)r * kp + 4 * c);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d),
+                   "l"(P.Bbar + (int64_t)grow[r] * kp + 4 * c)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // A = masked X rows (M = 128 x K = ep), split; rows fastest (conflict-free
+    // 16-byte stores), U chunks of every thread in flight before the stores
+    {
+      constexpr int U = 4;
+      for (int e0 = tid; e0 < kBtM * nch; e0 += kBtThreads * U) {
+        float v[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kBtThreads;
+          const int r = e % kBtM, c = e / kBtM;
+          if (e < kBtM * nch && r < n) {
+            const int64_t xr = P.xcompact ? t0 + r : (int64_t)grow[r];
+            bt_load8(P.X + xr * P.ldx, 8 * c, eta, true, v[u]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int e = e0 + u * kBtThreads;
+          if (e < kBtM * nch) bt_store_chunk(v[u], Ahi, Alo, bt_off(e % kBtM, 8 * (e / kBtM), nch));
+        }
+      }
+    }
+    tc_fence_smem_to_async();
+    tc_sync_before();
+    __syncthreads();
+    tc_sync_after();
+    const uint32_t tmem = tmem_s;
+    if (tid == 0) {
+      // D = Ahi Bhi^T + Ahi Blo^T + Alo Bhi^T over K = ep (2 chunks of 8 per instruction)
+      const uint32_t sbo_a = 128u * nch, sbo_b = 128u * nch;
+      for (int ks = 0; ks < ep / 16; ++ks) {
+        const size_t ko = (size_t)ks * 256;
+        const uint64_t ah = tc_sdesc(Ahi + ko, 128, sbo_a), al = tc_sdesc(Alo + ko, 128, sbo_a);
+        const uint64_t bh = tc_sdesc(Bhi + ko, 128, sbo_b), bl = tc_sdesc(Blo + ko, 128, sbo_b);
+        tc_mma_bf16(tmem, ah, bh, idesc, ks > 0);
+        tc_mma_bf16(tmem, ah, bl, idesc, true);
+        tc_mma_bf16(tmem, al, bh, idesc, true);
+      }
+      tc_commit(&mbar);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    __syncthreads();                                   // Bold rows of every thread landed
+    tc_sync_after();
+    // ---- epilogue: warp w reads lanes 32 (w % 4) .. (rows), column half w / 4 ----
+    {
+      const int row = 32 * (wid & 3) + lane;
+      const int nck = np / 16, c0 = (wid >> 2) * ((nck + 1) / 2), c1 = min(nck, c0 + (nck + 1) / 2);
+      for (int cc = c0; cc < c1; ++cc) {
+        float v[16];
+        tc_ld16(tmem + ((uint32_t)(32 * (wid & 3)) << 16) + 16 * cc, v);
+        if (row < n) {
+          float* brow = P.Bbar + (int64_t)grow[row] * kp;
+          const float* bo = Bold + (size_t)row * kp;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int a = 16 * cc + j;
+            if (a < k) brow[a] = fmaf(keep, bo[a], add * v[j]);
+          }
+        }
+      }
+    }
+    tc_sync_before();
+  }
+  __syncthreads();
+  if (wid == 0) tc_dealloc(tmem_s, np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256);
+}
+
+}  // namespace somf

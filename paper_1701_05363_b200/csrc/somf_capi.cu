@@ -34,6 +34,7 @@
 #include "bcd_onchip.cuh"
 #include "bcd_newton.cuh"
 #include "bcd_shard.cuh"
+#include "bbar_tc.cuh"
 
 using namespace somf;
 
@@ -301,6 +302,36 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
   if (folded) *folded = false;
   const int k = h->cfg.k, eta = h->cfg.eta;
   if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15)) return false;
+  static const bool tc_off = std::getenv("SOMF_BBAR_TC") && std::atoi(std::getenv("SOMF_BBAR_TC")) == 0;
+  if (gather && !tc_off && k <= 256) {
+    // tensor cores (bbar_tc.cuh): bf16x3 tcgen05 GEMM per 128 masked rows
+    BtArgs a{};
+    a.np = (k + 15) & ~15;
+    a.ep = (eta + 15) & ~15;
+    const size_t smem = (size_t)2 * (kBtM + a.np) * a.ep * 2 + (size_t)kBtM * h->kp * sizeof(float);
+    if (smem <= 220 * 1024 &&
+        cudaFuncSetAttribute((const void*)k_bbar_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+            cudaSuccess) {
+      a.idx = h->idx;
+      a.xcompact = xcompact;
+      a.q_dev = q_dev;
+      a.X = X;
+      a.ldx = ldx;
+      a.eta = eta;
+      a.k = k;
+      a.kp = h->kp;
+      a.A = h->A32;
+      a.Bbar = h->Bbar;
+      a.w_dev = h->w_dev;
+      if (folded && h->cpart_n > 0) {
+        a.cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32};
+        *folded = true;
+      }
+      k_bbar_tc<<<h->nsm, kBtThreads, smem, h->st>>>(a);
+      return true;
+    }
+    cudaGetLastError();
+  }
   int kc = (k + 31) / 32;
   if (kc > 4) kc = 8;
   const int64_t per = ceil_div(std::max<int64_t>(q_est, 1), h->nsm);
