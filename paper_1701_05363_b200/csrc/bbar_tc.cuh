@@ -191,12 +191,18 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
         float v[16];
         tc_ld16(tmem + ((uint32_t)(32 * (wid & 3)) << 16) + 16 * cc, v);
         if (row < n) {
+          // 16-byte stores up to kp (padding columns stay 0: zero codes, zero old values)
           float* brow = P.Bbar + (int64_t)grow[row] * kp;
           const float* bo = Bold + (size_t)row * kp;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int a = 16 * cc + j;
-            if (a < k) brow[a] = fmaf(keep, bo[a], add * v[j]);
+          for (int j4 = 0; j4 < 4; ++j4) {
+            const int a0 = 16 * cc + 4 * j4;
+            if (a0 + 4 <= kp) {
+              const float4 o = *reinterpret_cast<const float4*>(bo + a0);
+              *reinterpret_cast<float4*>(brow + a0) =
+                  make_float4(fmaf(keep, o.x, add * v[4 * j4]), fmaf(keep, o.y, add * v[4 * j4 + 1]),
+                              fmaf(keep, o.z, add * v[4 * j4 + 2]), fmaf(keep, o.w, add * v[4 * j4 + 3]));
+            }
           }
         }
       }

@@ -187,6 +187,115 @@ struct CtFuse {
   double* G;                // k x k
 };
 
+// Fused fixed-order split-K reduction (CtFuse): grid barrier, then CTA b
+// reduces the outputs [tot b / G, tot (b+1) / G) over the G partial tiles.
+// Partial tile layout: k rows of ncp columns; column c < eta is beta[:, c],
+// column ep + j (j < k) is G[:, j], other columns are padding.  Order: warp w
+// sums the splits w, w + 8, ... ascending (fp64), then the 8 warp sums in
+// order -- the same bits for any timing.
+__device__ __forceinline__ void ct_store_out(const CtFuse& fz, int64_t e, double t, int k, int eta, int ncp,
+                                             int ep) {
+  const int a = (int)(e / ncp), c = (int)(e % ncp);
+  t *= fz.r;
+  if (c < eta) fz.beta[(int64_t)a * eta + c] = t;
+  else if (c >= ep && c - ep < k) fz.G[(int64_t)a * k + (c - ep)] = t;
+}
+
+// scratch: >= 16 KB of shared memory the caller no longer needs
+__device__ __forceinline__ void ct_fused_reduce(const float* __restrict__ partial, int k, int eta, int ncp, int ep,
+                                                const CtFuse& fz, double* scratch) {
+  const int tid = threadIdx.x, ta = tid >> 5, tc = tid & 31;
+  const int G = gridDim.x;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(fz.bar), "r"(1u) : "memory");
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_gpu(fz.bar) < (unsigned)G) {
+      if (globaltimer_ns() - t0 > 2000000000ull) break;     // protocol bug: do not hang the GPU
+    }
+  }
+  __syncthreads();
+  const int64_t tot = (int64_t)k * ncp;
+  if ((ncp & 3) == 0) {
+    // lane = 4 consecutive outputs (16-byte loads), every split's load in flight
+    double (*ws4)[32][4] = reinterpret_cast<double (*)[32][4]>(scratch);     // [8][32][4]
+    const int64_t t4 = tot / 4;
+    const int64_t e0 = t4 * blockIdx.x / G, e1 = t4 * (blockIdx.x + 1) / G;
+    for (int64_t g0 = e0; g0 < e1; g0 += 32) {
+      const int64_t e = g0 + tc;
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      if (e < e1) {
+        const float4* p4 = reinterpret_cast<const float4*>(partial) + e;
+#pragma unroll 8
+        for (int i = ta; i < G; i += 8) {
+          const float4 v = __ldcg(p4 + (int64_t)i * t4);
+          s[0] += (double)v.x;
+          s[1] += (double)v.y;
+          s[2] += (double)v.z;
+          s[3] += (double)v.w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ws4[ta][tc][j] = s[j];
+      __syncthreads();
+      if (tid < 128) {
+        const int l = tid >> 2, j = tid & 3;
+        const int64_t ee = g0 + l;
+        if (ee < e1) {
+          double t = 0.0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) t += ws4[w][l][j];
+          ct_store_out(fz, 4 * ee + j, t, k, eta, ncp, ep);
+        }
+      }
+      __syncthreads();
+    }
+  } else {
+    constexpr int kOpl = 8;                      // outputs per lane (>= ceil(tot / G / 32))
+    double (*ws)[32 * kOpl] = reinterpret_cast<double (*)[32 * kOpl]>(scratch);   // [8][32 kOpl]
+    const int64_t e0 = tot * blockIdx.x / G, e1 = tot * (blockIdx.x + 1) / G;
+    for (int64_t g0 = e0; g0 < e1; g0 += 32 * kOpl) {
+      double sacc[kOpl];
+#pragma unroll
+      for (int o = 0; o < kOpl; ++o) sacc[o] = 0.0;
+#pragma unroll 5
+      for (int i = ta; i < G; i += 8) {
+        float v[kOpl];
+#pragma unroll
+        for (int o = 0; o < kOpl; ++o) {
+          const int64_t e = g0 + 32 * o + tc;
+          v[o] = e < e1 ? __ldcg(partial + (int64_t)i * tot + e) : 0.f;
+        }
+#pragma unroll
+        for (int o = 0; o < kOpl; ++o) sacc[o] += (double)v[o];
+      }
+#pragma unroll
+      for (int o = 0; o < kOpl; ++o) ws[ta][32 * o + tc] = sacc[o];
+      __syncthreads();
+      for (int x = tid; x < 32 * kOpl; x += kCtThreads) {
+        const int64_t e = g0 + x;
+        if (e < e1) {
+          double t = 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) t += ws[i][x];
+          ct_store_out(fz, e, t, k, eta, ncp, ep);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // last CTA out resets the barrier for the next launch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(fz.bar + 1, 1u) == (unsigned)G - 1) {
+      fz.bar[0] = 0u;
+      fz.bar[1] = 0u;
+      __threadfence();
+    }
+  }
+}
+
 template <int MT, int NT, bool kXCompact>
 __global__ void __launch_bounds__(kCtThreads)
 k_contract_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, const float* __restrict__ D,
@@ -258,64 +367,7 @@ k_contract_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev
     }
   }
   if (fz.bar == nullptr) return;
-  // ---- fused fixed-order reduction of the G partial tiles ----------------------------
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(fz.bar), "r"(1u) : "memory");
-    const uint64_t t0 = globaltimer_ns();
-    while (ld_acquire_gpu(fz.bar) < (unsigned)G) {
-      if (globaltimer_ns() - t0 > 2000000000ull) break;     // protocol bug: do not hang the GPU
-    }
-  }
-  __syncthreads();
-  // warp w sums the splits w, w + 8, ... of all my outputs (every load in flight
-  // at once: the latency of L2, not its bandwidth, bounds this), lane = output
-  constexpr int kOpl = 8;                        // outputs per lane (>= ceil(tot / G / 32))
-  __shared__ double ws[8][32 * kOpl];
-  const int64_t tot = (int64_t)k * nc;
-  const int64_t e0 = tot * blockIdx.x / G, e1 = tot * (blockIdx.x + 1) / G;
-  for (int64_t g0 = e0; g0 < e1; g0 += 32 * kOpl) {
-    double sacc[kOpl];
-#pragma unroll
-    for (int o = 0; o < kOpl; ++o) sacc[o] = 0.0;
-#pragma unroll 5
-    for (int i = ta; i < G; i += 8) {
-      float v[kOpl];
-#pragma unroll
-      for (int o = 0; o < kOpl; ++o) {
-        const int64_t e = g0 + 32 * o + tc;
-        v[o] = e < e1 ? __ldcg(partial + (int64_t)i * tot + e) : 0.f;
-      }
-#pragma unroll
-      for (int o = 0; o < kOpl; ++o) sacc[o] += (double)v[o];
-    }
-#pragma unroll
-    for (int o = 0; o < kOpl; ++o) ws[ta][32 * o + tc] = sacc[o];
-    __syncthreads();
-    for (int x = tid; x < 32 * kOpl; x += kCtThreads) {
-      const int64_t e = g0 + x;
-      if (e < e1) {
-        double t = 0.0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) t += ws[i][x];
-        t *= fz.r;
-        const int a = (int)(e / nc), c = (int)(e % nc);
-        if (c < eta) fz.beta[(int64_t)a * eta + c] = t;
-        else fz.G[(int64_t)a * k + (c - eta)] = t;
-      }
-    }
-    __syncthreads();
-  }
-  // last CTA out resets the barrier for the next launch
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(fz.bar + 1, 1u) == (unsigned)G - 1) {
-      fz.bar[0] = 0u;
-      fz.bar[1] = 0u;
-      __threadfence();
-    }
-  }
+  ct_fused_reduce(partial, k, eta, eta + k, eta, fz, reinterpret_cast<double*>(c3_smem));
 }
 
 }  // namespace somf

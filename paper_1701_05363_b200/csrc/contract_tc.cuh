@@ -1,0 +1,213 @@
+// contract_tc.cuh -- (a1) the masked code step on the tensor cores:
+//   beta = r D_M^T X_M (k x eta),  G = r D_M^T D_M (k x k)      (Eq. a)
+// Every CTA owns ~q / #SMs masked rows and computes the partial
+// [beta | G] = D_S^T [X_S | D_S] of its rows as two tcgen05 GEMMs sharing the
+// A operand: M = atoms (k <= 128, padded to 128), K = masked rows (tiles of
+// 128), N = eta (padded to 16; two instructions when > 256) and N = k (padded
+// to 16).  3xTF32: fp32 operands are split x = hi + lo (hi exact in tf32) and
+// hi.hi + hi.lo + lo.hi are accumulated in fp32 in TMEM, kind::tf32 (bf16x3
+// was measured too coarse for the ridge solve at cfgC: alpha off by 2.5e-3).
+// Rows arrive by 16-byte cp.async, all 128 rows of a chunk in flight at once
+// ([X row | D row] raw rows, one commit group per 32-row tile); each tile is
+// transposed and split in shared memory into the K-major operands (a 16-byte
+// K chunk = 4 rows of one atom / column) as soon as it lands.  The partial tiles are written in fp32 and
+// reduced in fixed order behind one grid barrier (ct_fused_reduce,
+// cooperative launch) into r [beta | G] in fp64.
+#pragma once
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "tc_common.cuh"
+#include "contract.cuh"
+#include "bbar_tc.cuh"
+
+namespace somf {
+
+constexpr int kTcM = 128;           // atoms per accumulator (k <= 128)
+constexpr int kTcK = 32;            // masked rows per tile (K of one tile)
+
+struct CtTcArgs {
+  const int32_t* idx;
+  const int64_t* q_dev;
+  const float* D;           // rows x kp
+  int kp, k;
+  const float* X;           // rows x ldx (or q x ldx when compact)
+  int64_t ldx;
+  int eta, xcompact;
+  int ep;                   // eta rounded up to 16
+  int kn;                   // k rounded up to 16 (N of the G product)
+  float* partial;           // G x k x (ep + kn): [beta | pad | G | pad] rows
+  CtFuse fz;
+};
+
+// fp32 -> (hi, lo) for 3xTF32: hi = x with the 13 low mantissa bits cleared
+// (exactly representable in tf32), lo = x - hi (exact in fp32)
+__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
+}
+
+// byte offset of (row mn, k) in a K-major SWIZZLE_NONE tf32 operand of one
+// tile: 16-byte chunks of 4 k, LBO = 128 (chunks adjacent), SBO = 128 kTcK / 4
+__device__ __forceinline__ uint32_t tf_off(int mn, int kk) {
+  return (uint32_t)((mn >> 3) * 128 * (kTcK / 4) + (kk >> 2) * 128 + (mn & 7) * 16 + (kk & 3) * 4);
+}
+
+// cp.async.wait_group with a runtime count (0..3)
+__device__ __forceinline__ void cp_async_wait_upto(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+  }
+}
+
+constexpr int kTcChunk = 128;       // masked rows whose raw data is resident at once (4 tiles)
+
+__global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
+  extern __shared__ __align__(128) uint8_t ctc_smem[];
+  __shared__ uint32_t tmem_s;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ int grow[kTcChunk];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int k = P.k, kp = P.kp, eta = P.eta, ep = P.ep, kn = P.kn;
+  const int LDR = ep + kp;                            // raw row: [X row (ep) | D row (kp)]
+  const int G = gridDim.x;
+  const int64_t q = *P.q_dev;
+  const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
+  const size_t a_bytes = (size_t)kTcM * kTcK * 4, x_bytes = (size_t)ep * kTcK * 4;
+  uint8_t* Ahi = ctc_smem;                            // atoms x rows (K-major tf32)
+  uint8_t* Alo = Ahi + a_bytes;
+  uint8_t* Xhi = Alo + a_bytes;                       // X columns x rows
+  uint8_t* Xlo = Xhi + x_bytes;
+  float* raw = reinterpret_cast<float*>(Xlo + x_bytes);          // kTcChunk x LDR (fp32 rows)
+  // TMEM: columns [0, ep) beta, [ep, ep + kn) G
+  const uint32_t ncols = (ep + kn) <= 256 ? 256 : 512;
+  if (wid == 0) tc_alloc(&tmem_s, ncols);
+  if (tid == 0) mbar_init(&mbar, 1);
+  uint32_t phase = 0;
+  int issued = 0;                                     // MMA batches committed (one per tile)
+  const int cx = eta / 4, cd = kp / 4, cr = cx + cd;  // 16-byte chunks of a raw row (eta % 4 == 0)
+  for (int64_t c0 = lo; c0 < hi; c0 += kTcChunk) {
+    const int nrow = (int)(hi - c0 < (int64_t)kTcChunk ? hi - c0 : (int64_t)kTcChunk);
+    const int ntile = (nrow + kTcK - 1) / kTcK;
+    if (issued > 0) {                                 // the previous chunk's MMAs read raw-derived operands
+      mbar_wait(&mbar, phase);
+      phase ^= 1;
+      issued = 0;
+    }
+    __syncthreads();
+    for (int r = tid; r < kTcChunk; r += kCtThreads) grow[r] = r < nrow ? P.idx[c0 + r] : -1;
+    __syncthreads();
+    // every row of the chunk in flight at once: one commit group per tile
+    for (int j = 0; j < ntile; ++j) {
+      const int r0 = j * kTcK, r1 = min(nrow, r0 + kTcK);
+      for (int e = tid; e < (r1 - r0) * cr; e += kCtThreads) {
+        const int r = r0 + e / cr, c = e % cr;
+        const int64_t g = grow[r];
+        const float* src =
+            c < cx ? P.X + (P.xcompact ? c0 + r : g) * P.ldx + 4 * c : P.D + g * kp + 4 * (c - cx);
+        float* dst = raw + (size_t)r * LDR + (c < cx ? 4 * c : ep + 4 * (c - cx));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int j = 0; j < ntile; ++j) {
+      cp_async_wait_upto(ntile - 1 - j);
+      if (issued > 0) {                               // tile j-1's MMAs have read the operand buffers
+        mbar_wait(&mbar, phase);
+        phase ^= 1;
+        issued = 0;
+      }
+      __syncthreads();
+      // ---- transpose + split tile j into K-major tf32 hi / lo operands ----
+      // thread -> one operand row m (atom, or X column), all kTcK / 4 chunks
+      for (int m = tid; m < kTcM + ep; m += kCtThreads) {
+        const bool isA = m < kTcM;
+        const int col = isA ? ep + m : m - kTcM;     // column of the raw row
+        const bool valid = isA ? m < k : col < eta;
+        float v[kTcK];
+#pragma unroll
+        for (int r = 0; r < kTcK; ++r) {
+          const int rr = j * kTcK + r;
+          v[r] = (valid && rr < nrow) ? raw[(size_t)rr * LDR + col] : 0.f;
+        }
+        uint8_t* hb = isA ? Ahi : Xhi;
+        uint8_t* lb = isA ? Alo : Xlo;
+        const int mm = isA ? m : m - kTcM;
+#pragma unroll
+        for (int c = 0; c < kTcK / 4; ++c) {
+          float4 h, l;
+          tf32_split(v[4 * c + 0], h.x, l.x);
+          tf32_split(v[4 * c + 1], h.y, l.y);
+          tf32_split(v[4 * c + 2], h.z, l.z);
+          tf32_split(v[4 * c + 3], h.w, l.w);
+          const uint32_t off = tf_off(mm, 4 * c);
+          *reinterpret_cast<float4*>(hb + off) = h;
+          *reinterpret_cast<float4*>(lb + off) = l;
+        }
+      }
+      tc_fence_smem_to_async();
+      tc_sync_before();
+      __syncthreads();
+      tc_sync_after();
+      const uint32_t tmem = tmem_s;
+      if (tid == 0) {
+        const uint32_t sbo = 128u * (kTcK / 4);
+        const bool first = (c0 == lo && j == 0);
+        for (int ks = 0; ks < kTcK / 8; ++ks) {
+          const size_t ko = (size_t)ks * 256;
+          const uint64_t ah = tc_sdesc(Ahi + ko, 128, sbo), al = tc_sdesc(Alo + ko, 128, sbo);
+          const bool acc0 = !first || ks > 0;
+          // beta: N = ep in pieces of <= 256 (multiples of 16)
+          for (int n0 = 0; n0 < ep; n0 += 256) {
+            const int nn = ep - n0 < 256 ? ep - n0 : 256;
+            const uint32_t id = tc_idesc_tf32(kTcM, nn);
+            const uint64_t xh = tc_sdesc(Xhi + (size_t)n0 * 16 * (kTcK / 4) + ko, 128, sbo);
+            const uint64_t xl = tc_sdesc(Xlo + (size_t)n0 * 16 * (kTcK / 4) + ko, 128, sbo);
+            tc_mma_tf32(tmem + n0, ah, xh, id, acc0);
+            tc_mma_tf32(tmem + n0, ah, xl, id, true);
+            tc_mma_tf32(tmem + n0, al, xh, id, true);
+          }
+          // G: B = the same D rows (the A operand), N = kn
+          const uint32_t idg = tc_idesc_tf32(kTcM, kn);
+          tc_mma_tf32(tmem + ep, ah, ah, idg, acc0);
+          tc_mma_tf32(tmem + ep, ah, al, idg, true);
+          tc_mma_tf32(tmem + ep, al, ah, idg, true);
+        }
+        tc_commit(&mbar);
+      }
+      issued = 1;
+    }
+  }
+  const int ntile_all = hi > lo ? 1 : 0;
+  if (issued > 0) {
+    mbar_wait(&mbar, phase);
+    tc_sync_after();
+  }
+  // ---- epilogue: partial tile [beta | pad | G | pad] of my rows (fp32), lane = atom ----
+  const int ncp = ep + kn;
+  float* out = P.partial + (int64_t)blockIdx.x * k * ncp;
+  if (ntile_all > 0) {
+    const int a = 32 * (wid & 3) + lane;
+    const uint32_t tl = tmem_s + ((uint32_t)(32 * (wid & 3)) << 16);
+    const int nchunk = ncp / 16;
+    for (int cc = wid >> 2; cc < nchunk; cc += 2) {
+      float v[16];
+      tc_ld16(tl + 16 * cc, v);
+      if (a < k) {
+        float4* o4 = reinterpret_cast<float4*>(out + (int64_t)a * ncp + 16 * cc);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+  } else {
+    for (int e = tid; e < k * ncp; e += kCtThreads) out[e] = 0.f;
+  }
+  tc_sync_before();
+  __syncthreads();
+  if (wid == 0) tc_dealloc(tmem_s, ncols);
+  ct_fused_reduce(P.partial, k, eta, ep + kn, ep, P.fz, reinterpret_cast<double*>(ctc_smem));
+}
+
+}  // namespace somf

@@ -35,6 +35,7 @@
 #include "bcd_newton.cuh"
 #include "bcd_shard.cuh"
 #include "bbar_tc.cuh"
+#include "contract_tc.cuh"
 
 using namespace somf;
 
@@ -403,6 +404,41 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
   const int k = h->cfg.k;
   const int nc = m + k;
   h->ct_launches = 2;
+  static const bool tc_off = std::getenv("SOMF_CT_TC") && std::atoi(std::getenv("SOMF_CT_TC")) == 0;
+  if (gather && !tc_off && k <= kTcM) {
+    // tensor cores (contract_tc.cuh): bf16x3 tcgen05 GEMMs + fused split-K reduction
+    CtTcArgs a{};
+    a.ep = (m + 15) & ~15;
+    a.kn = (k + 15) & ~15;
+    const size_t smem = (size_t)2 * (kTcM + a.ep) * kTcK * 4 + (size_t)kTcChunk * (a.ep + h->kp) * 4;
+    if (a.ep + a.kn <= 512 && smem <= 226 * 1024 && m % 4 == 0 &&
+        cudaFuncSetAttribute((const void*)k_contract_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+            cudaSuccess) {
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_contract_tc, kCtThreads, smem) ==
+              cudaSuccess && occ >= 1) {
+        somf_status s = ensure_partial(h, (size_t)h->nsm * k * (a.ep + a.kn));
+        if (s) return s;
+        a.idx = h->idx;
+        a.q_dev = q_dev;
+        a.D = h->D;
+        a.kp = h->kp;
+        a.k = k;
+        a.X = X;
+        a.ldx = ldx;
+        a.eta = m;
+        a.xcompact = xcompact;
+        a.partial = h->partial;
+        a.fz = CtFuse{h->ct_bar, r, beta, G};
+        void* args[] = {&a};
+        CK(cudaLaunchCooperativeKernel((const void*)k_contract_tc, dim3(h->nsm), dim3(kCtThreads), args, smem,
+                                       h->st));
+        h->ct_launches = 1;
+        return SOMF_OK;
+      }
+    }
+    cudaGetLastError();
+  }
   const bool fast = (m % 4 == 0) && (ldx % 4 == 0) && (((uintptr_t)X & 15) == 0);
   if (fast && gather) {
     const Ct3Variant* v3 = nullptr;
