@@ -36,6 +36,7 @@
 #include "bcd_shard.cuh"
 #include "bbar_tc.cuh"
 #include "contract_tc.cuh"
+#include "codes_mp.cuh"
 
 using namespace somf;
 
@@ -552,21 +553,42 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     }
     double* cp = want_cpart ? h->cpart : nullptr;
     const void* fn = nullptr;
-    switch ((k4 + 31) / 32) {
-      case 1: fn = (const void*)k_ridge_codes<1>; break;
-      case 2: fn = (const void*)k_ridge_codes<2>; break;
-      case 3: fn = (const void*)k_ridge_codes<3>; break;
-      case 4: fn = (const void*)k_ridge_codes<4>; break;
-      default: fn = (const void*)k_ridge_codes<5>; break;
+    size_t sm = smem;
+    // mixed precision (codes_mp.cuh: fp32 factor + substitutions, one fp64
+    // refinement) is opt-in, SOMF_RIDGE_MP=1: measured at cfgC it factors 25 %
+    // faster but its two substitution passes make the kernel slower (51.5 vs
+    // 49.4 us per step); the chain is latency-bound, not precision-bound
+    static const bool mp_on = std::getenv("SOMF_RIDGE_MP") && std::atoi(std::getenv("SOMF_RIDGE_MP")) == 1;
+    if (mp_on) {
+      sm = (size_t)8 * k4 * sizeof(double) + (size_t)k * (k + 1) * sizeof(double) +
+           (size_t)k4 * (k4 + 1) * sizeof(float);
+      static const int pw8 = std::getenv("SOMF_RIDGE_PW") && std::atoi(std::getenv("SOMF_RIDGE_PW")) == 8;
+#define RMP(N) (pw8 ? (const void*)k_ridge_mp<N, 8> : (const void*)k_ridge_mp<N, 4>)
+      switch ((k4 + 31) / 32) {
+        case 1: fn = RMP(1); break;
+        case 2: fn = RMP(2); break;
+        case 3: fn = RMP(3); break;
+        case 4: fn = RMP(4); break;
+        default: fn = RMP(5); break;
+      }
+#undef RMP
+    } else {
+      switch ((k4 + 31) / 32) {
+        case 1: fn = (const void*)k_ridge_codes<1>; break;
+        case 2: fn = (const void*)k_ridge_codes<2>; break;
+        case 3: fn = (const void*)k_ridge_codes<3>; break;
+        case 4: fn = (const void*)k_ridge_codes<4>; break;
+        default: fn = (const void*)k_ridge_codes<5>; break;
+      }
     }
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     double lam = c.lambda;
     long long* rprof = h->prof_on ? h->bcd_prof + 72 : nullptr;    // slots 72..75 (ridge phases)
     float* at = want_cpart ? h->AT32 : nullptr;
     int ldt = h->kp;
     void* args[] = {(void*)&G, (void*)&beta, (void*)&k, (void*)&m, (void*)&lam, (void*)&A64, (void*)&A32,
                     (void*)&at, (void*)&ldt, (void*)&cp, (void*)&h->err_dev, (void*)&rprof};
-    CK(cudaLaunchKernel(fn, dim3(g), dim3(kRcThreads), args, smem, h->st));
+    CK(cudaLaunchKernel(fn, dim3(g), dim3(kRcThreads), args, sm, h->st));
     return SOMF_OK;
   }
   const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
