@@ -415,6 +415,28 @@ def run_somf(args):
                 "frac": achieved / pk, "traffic": traffic, "kernel_phase": dom,
                 "peak_source": "guide: 148 SM x 64 FP64 lanes x 2 x sm_max_mhz"}
     roof["phase_ms_per_step"] = phase_ms
+    # every phase against its own bound: algorithmic bytes over
+    # HBM, the contractions' algorithmic flops over the tensor-core peak of the
+    # dtype they run in (3xTF32 / bf16x3 issue 3 products per flop counted once),
+    # the BCD also against the CUDA-core fp32 FMA peak (its recurrence pipe)
+    tf32_peak = peaks["bf16"] / 2.0          # guide: dense TF32 = 1/2 dense BF16
+    per = {}
+    for ph, pms in phase_ms.items():
+        if pms <= 0 or ph in ("stage", "mask", "cbar"):
+            continue
+        pb, pf, _ = phase_cost(ph, q, p, k, eta)
+        ent = {"ms": pms, "hbm_gbs": pb / (pms * 1e-3) / 1e9, "hbm_frac": pb / (pms * 1e-3) / 1e9 / peaks["hbm"]}
+        if ph == "contract":
+            ent.update(tensor_tflops=pf / (pms * 1e-3) / 1e12, tensor_peak=tf32_peak, tensor_dtype="tf32 (3xTF32)",
+                       tensor_frac=pf / (pms * 1e-3) / 1e12 / tf32_peak)
+        if ph == "bbar":
+            ent.update(tensor_tflops=pf / (pms * 1e-3) / 1e12, tensor_peak=peaks["bf16"], tensor_dtype="bf16 (bf16x3)",
+                       tensor_frac=pf / (pms * 1e-3) / 1e12 / peaks["bf16"])
+        if ph == "bcd":
+            fp32 = alu_peak_tflops(peaks["sm_max_mhz"], fp64=False)
+            ent.update(fma_tflops=pf / (pms * 1e-3) / 1e12, fma_peak=fp32, fma_frac=pf / (pms * 1e-3) / 1e12 / fp32)
+        per[ph] = ent
+    roof["phases"] = per
     roof["bcd_grid_reductions_per_step"] = info["bcd_reductions"]
     if bcd_cyc["launches"]:
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
