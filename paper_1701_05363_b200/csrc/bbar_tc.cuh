@@ -137,8 +137,9 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
     asm volatile("cp.async.commit_group;" ::: "memory");
     // A = masked X rows (M = 128 x K = ep), split; rows fastest (conflict-free
     // 16-byte stores), U chunks of every thread in flight before the stores
+    // (the gather is latency-bound: one round of loads, not several)
     {
-      constexpr int U = 4;
+      constexpr int U = 14;                         // every chunk of a thread in flight (eta <= 224)
       for (int e0 = tid; e0 < kBtM * nch; e0 += kBtThreads * U) {
         float v[U][8];
 #pragma unroll

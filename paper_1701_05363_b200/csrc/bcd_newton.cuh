@@ -444,7 +444,7 @@ k_bcd_newton(NtArgs P) {
   NT_MARK(78);
   // R = (P Bbar - P D Cbar) / c_pp: RT rows x 8 positions per item (register tile)
   {
-    constexpr int RT = 8;
+    constexpr int RT = 4;                 // ~2 items per thread at 288 threads
     const int nrb = (nr + RT - 1) / RT, npb = (k + 7) / 8;
     for (int it = tid; it < nrb * npb; it += nthr) {
       const int r0 = (it / npb) * RT, p0 = (it % npb) * 8;
