@@ -89,6 +89,60 @@ class FmriStreamGPU:
         return self._cols(self.k + b * self.eta, self.k + (b + 1) * self.eta)
 
 
+class HyperspectralStreamGPU:
+    """cfgB stand-in on the GPU (harness only): 16 x 16 pixels x
+    224 bands (p = 57,344, row = pixel * 224 + band); 256 |GP(RBF, l=20)|
+    spectra (drawn once as in synth.hyperspectral_patches); every column mixes
+    them with Dirichlet(0.5) abundances per pixel, 1 % Gaussian noise relative
+    to the column rms, then is centred and l2-normalised."""
+
+    def __init__(self, eta: int, seed: int, device, size: int = 16, bands: int = 224, n_end: int = 256):
+        import torch
+        rng = np.random.default_rng(seed)
+        bb = np.arange(bands, dtype=np.float64)
+        K = np.exp(-0.5 * ((bb[:, None] - bb[None, :]) / 20.0) ** 2)
+        L = np.linalg.cholesky(K + 1e-8 * np.eye(bands))
+        spectra = np.abs(L @ rng.standard_normal((bands, n_end))).T
+        self.spectra = torch.tensor(spectra, dtype=torch.float32, device=device)      # n_end x bands
+        self.npix, self.bands, self.eta, self.device = size * size, bands, eta, device
+        self.p = self.npix * bands
+        self.dir = torch.distributions.Dirichlet(torch.full((n_end,), 0.5, device=device))
+        self.g = torch.Generator(device=device)
+        self.g.manual_seed(seed + 1)
+        torch.manual_seed(seed + 2)
+
+    def batch(self, m: int | None = None):
+        import torch
+        m = m or self.eta
+        ab = self.dir.sample((m, self.npix))                         # m x npix x n_end
+        X = (ab @ self.spectra).reshape(m, self.p)                   # column s = row s here
+        rms = X.pow(2).mean(dim=1, keepdim=True).sqrt()
+        X = X + 0.01 * rms * torch.randn(X.shape, generator=self.g, device=self.device)
+        X = X - X.mean(dim=1, keepdim=True)
+        X = X / X.norm(dim=1, keepdim=True)
+        return X.t().contiguous()                                    # p x m
+
+
+class NmfStreamGPU:
+    """cfgD stand-in on the GPU: X = W* H* + |N(0, 0.01)|, W* 16,384 x 128 |N(0,1)|
+    at 30 % density (fixed), H* ~ Exp(1) per column."""
+
+    def __init__(self, eta: int, seed: int, device, p: int = 16384, k_true: int = 128):
+        import torch
+        self.g = torch.Generator(device=device)
+        self.g.manual_seed(seed)
+        W = torch.randn((p, k_true), generator=self.g, device=device).abs()
+        W *= (torch.rand((p, k_true), generator=self.g, device=device) < 0.3).float()
+        self.W, self.p, self.k_true, self.eta, self.device = W, p, k_true, eta, device
+
+    def batch(self, m: int | None = None):
+        import torch
+        m = m or self.eta
+        H = torch.empty((self.k_true, m), device=self.device).exponential_(1.0, generator=self.g)
+        N = (0.1 * torch.randn((self.p, m), generator=self.g, device=self.device)).abs()
+        return (self.W @ H + N).contiguous()
+
+
 def fmri_inputs_gpu(n_batches: int, eta: int, k: int, seed: int, device):
     """(list of p x eta float32 CUDA batches, D0 p x k) of FmriStreamGPU."""
     s = FmriStreamGPU(n_batches, eta, k, seed, device)
@@ -498,6 +552,43 @@ def run_somf(args):
                                      "bcd_grid_reductions": m3.last_step_info()["bcd_reductions"]}
             del m3
 
+    # --- the other BASELINE workloads (single GPU, secondary lines) -----------------
+    # cfgB hyperspectral (k = 256, lasso codes, l2-ball atoms) at r = 1/4/12 and
+    # cfgD NMF (k = 128, nonneg ridge CD codes, nonneg l2-ball atoms) at r = 8:
+    # 10 burn-in steps from the first k stream columns, then 5 timed steps
+    workloads = {}
+    if not args.no_sweep and world == 1:
+        specs = [("cfgB-hyperspectral", HyperspectralStreamGPU, 256, 256,
+                  dict(lam=0.1, nu=0.0, mu=1.0, pos_code=False, pos_dict=False), (1.0, 4.0, 12.0)),
+                 ("cfgD-nmf", NmfStreamGPU, 128, 512,
+                  dict(lam=0.05, nu=1.0, mu=1.0, pos_code=True, pos_dict=True), (8.0,))]
+        for name, gen_cls, kk, ee, kw, rs in specs:
+            gen = gen_cls(ee, seed=0, device=dev)
+            pool = [gen.batch() for _ in range(8)]
+            d0 = gen.batch(kk)
+            res = {}
+            for rr in rs:
+                m4 = somf_pkg.Somf(gen.p, kk, ee, r=rr, u=w["u"], seed=0, device=dev.index, stream=stream, **kw)
+                m4.set_components(d0)
+                for i in range(10):
+                    m4.partial_fit(pool[i % len(pool)])
+                torch.cuda.synchronize()
+                t4 = time_steps(m4, pool, 10, 5, flush, stream)
+                sm4 = sum(t4) / len(t4)
+                info4 = m4.last_step_info()
+                m4.profile_read()
+                m4.profile_enable(True)
+                time_steps(m4, pool, 15, 3, flush, stream)
+                pr4 = m4.profile_read()
+                m4.profile_enable(False)
+                res[f"r={int(rr)}"] = {"columns_per_s": ee / (sm4 * 1e-3), "ms_per_step": sm4,
+                                       "bcd_kernel": m4.bcd_variant,
+                                       "bcd_grid_reductions": info4["bcd_reductions"], "q": info4["q"],
+                                       "phase_ms_per_step": {ph: v / max(pr4["steps"], 1)
+                                                             for ph, v in pr4["ms"].items() if v > 0}}
+                del m4
+            workloads[name] = {"p": gen.p, "k": kk, "eta": ee, **{k_: v for k_, v in kw.items()}, "results": res}
+
     # --- CPU oracle baseline (rank 0, N = 1) ----------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -520,7 +611,7 @@ def run_somf(args):
                        "parallelism": "single" if world == 1 else f"row-sharded x{world} ({args.dist_backend} allreduce)"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / steps_prof,
-            "clocks": clk, "sweep": sweep, "wall_s_timed": t_wall}
+            "clocks": clk, "sweep": sweep, "workloads": workloads, "wall_s_timed": t_wall}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -121,13 +121,16 @@ k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m
   __syncthreads();
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
   for (int s = blockIdx.x * nw + wid; s < m; s += gridDim.x * nw) {
-    double alpha[KPL], g[KPL], den[KPL];
+    double alpha[KPL], g[KPL], den[KPL], rden[KPL];
+    int roff[KPL];                         // packed_off(row): row's packed segment
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
       const int row = lane + 32 * i;
       alpha[i] = 0.0;
       g[i] = row < k ? beta[(int64_t)row * m + s] : 0.0;
       den[i] = row < k ? (double)packed_get(Pk, row, row, k) + l2 : 1.0;
+      rden[i] = den[i] > 0.0 ? 1.0 / den[i] : 0.0;   // off the coordinate chain
+      roff[i] = packed_off(row < k ? row : 0, k);
     }
     int sweep = 0;
     for (; sweep < max_sweeps; ++sweep) {
@@ -143,18 +146,21 @@ k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m
             const double z = g[slot] + gjj * alpha[slot];
             double nv;
             if (!(den[slot] > 0.0)) nv = 0.0;                       // R12
-            else if (positive) nv = fmax(z - l1, 0.0) / den[slot];
-            else nv = copysign(fmax(fabs(z) - l1, 0.0), z) / den[slot];
+            else if (positive) nv = fmax(z - l1, 0.0) * rden[slot];
+            else nv = copysign(fmax(fabs(z) - l1, 0.0), z) * rden[slot];
             delta = nv - alpha[slot];
             alpha[slot] = nv;
           }
           delta = __shfl_sync(0xffffffffu, delta, ol);
           if (delta != 0.0) {
             maxd = fmax(maxd, fabs(delta));
+            const int joff = packed_off(j, k);
 #pragma unroll
             for (int i = 0; i < KPL; ++i) {
               const int row = lane + 32 * i;
-              if (row < k) g[i] -= (double)packed_get(Pk, row, j, k) * delta;
+              // G[row][j] from the packed upper triangle without index multiplies
+              const int a = row <= j ? roff[i] + (j - row) : joff + (row - j);
+              if (row < k) g[i] = fma(-(double)Pk[a], delta, g[i]);
             }
           }
         }
