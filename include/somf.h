@@ -99,7 +99,7 @@ typedef struct somf_config {
 } somf_config;
 
 /* Fills *cfg with defaults: u = 0.917, r = 1, nu = 1, mu = 0,
- * lambda = 0.1, b_mode = SOMF_B_MASKED, cd_tol = 1e-9, cd_max_sweeps = 4000,
+ * lambda = 0.1, b_mode = SOMF_B_MASKED, cd_tol = 1e-7, cd_max_sweeps = 4000,
  * seed = 0, row range [0, p), device 0, stream NULL, debug 0.  p, k, eta are
  * left 0 and must be set. */
 void somf_config_default(somf_config* cfg);

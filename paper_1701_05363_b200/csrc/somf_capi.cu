@@ -893,7 +893,7 @@ SOMF_EXPORT void somf_config_default(somf_config* c) {
   c->r = 1.0;
   c->u = 0.917;
   c->b_mode = SOMF_B_MASKED;
-  c->cd_tol = 1e-9;
+  c->cd_tol = 1e-7;
   c->cd_max_sweeps = 4000;
 }
 

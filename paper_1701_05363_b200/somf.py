@@ -83,7 +83,7 @@ class Somf:
     def __init__(self, p: int, k: int, eta: int, lam: float = 0.1, nu: float = 1.0,
                  pos_code: bool = False, mu: float = 0.0, pos_dict: bool = False,
                  r: float = 1.0, u: float = 0.917, b_mode: str = "masked",
-                 perm_cyclic: bool = False, cd_tol: float = 1e-9, cd_max_sweeps: int = 4000,
+                 perm_cyclic: bool = False, cd_tol: float = 1e-7, cd_max_sweeps: int = 4000,
                  seed: int = 0, row_lo: int = 0, row_hi: int = 0, device: int = 0,
                  stream=None, debug: bool = False, bcd_kernel: str = "auto"):
         L = lib()
