@@ -37,6 +37,7 @@
 #include "bbar_tc.cuh"
 #include "contract_tc.cuh"
 #include "codes_mp.cuh"
+#include "cd_as.cuh"
 
 using namespace somf;
 
@@ -594,6 +595,27 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
   const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
   const size_t smem = (size_t)k * (k + 1) / 2 * sizeof(float);
   const int kpl = (int)ceil_div(k, 32);
+  static const bool as_off = std::getenv("SOMF_CD_AS") && std::atoi(std::getenv("SOMF_CD_AS")) == 0;
+  const size_t smem_as = (size_t)(kAsThreads / 32) * cd_as_warp_bytes() + smem;
+  if (!as_off && k >= 32 && smem_as <= 220 * 1024) {
+    // CD with exact support jumps (cd_as.cuh), 4 columns per CTA
+    const int gas = (int)ceil_div(m, kAsThreads / 32);
+#define LAUNCH_AS(N)                                                                                  \
+  case N:                                                                                             \
+    CK(cudaFuncSetAttribute(k_cd_as<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_as));   \
+    k_cd_as<N><<<gas, kAsThreads, smem_as, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,           \
+                                                    c.cd_max_sweeps, A64, A32, h->sweeps_dev,         \
+                                                    want_cpart ? h->AT32 : nullptr, h->kp);           \
+    break;
+    switch (kpl) {
+      LAUNCH_AS(1) LAUNCH_AS(2) LAUNCH_AS(3) LAUNCH_AS(4)
+      LAUNCH_AS(5) LAUNCH_AS(6) LAUNCH_AS(7) LAUNCH_AS(8)
+      default: set_err(h, "k too large for the CD kernel"); return SOMF_E_ARG;
+    }
+#undef LAUNCH_AS
+    CKL();
+    return SOMF_OK;
+  }
 #define LAUNCH_CD(N)                                                                      \
   case N:                                                                                 \
     CK(cudaFuncSetAttribute(k_cd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
