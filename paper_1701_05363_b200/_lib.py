@@ -22,7 +22,7 @@ def _sources():
                   if f.endswith((".cu", ".cuh"))) + [os.path.join(ROOT, "include", "somf.h")]
 
 
-NT_KPTS = (16, 32, 48, 64, 72, 80, 96)   # bcd_newton_inst.cu variants (one object each)
+NT_KPTS = (16, 32, 48, 64, 72, 80, 96, 128)   # bcd_newton_inst.cu variants (one object each)
 
 
 def _units():

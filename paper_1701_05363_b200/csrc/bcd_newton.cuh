@@ -30,7 +30,7 @@
 namespace somf {
 
 constexpr int kNtRing = 3;
-constexpr int kNtMaxK = 96;         // largest k of the simultaneous-threshold kernel
+constexpr int kNtMaxK = 128;        // largest k of the simultaneous-threshold kernel
 constexpr int kNtRec = 16;          // doubles per accumulator record (128 bytes)
 // Convergence: every atom exact (its active set reproduces itself) and its
 // lambda stable to this relative tolerance between two rounds.  The

@@ -16,6 +16,8 @@ const void* NT_CAT(somf_nt_kernel_, NT_KPT)(int T, int M, int gen) {
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, false>;
   if (T == 4 && M == 1) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, true>
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, false>;
+  if (T == 8 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, true>
+                                   : (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, false>;
   if (T == 2 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, true>
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, false>;
   return nullptr;

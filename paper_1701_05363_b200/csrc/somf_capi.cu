@@ -664,12 +664,12 @@ const void* somf_oc_kernel(int kc, int rpw);
 
 // simultaneous-threshold BCD variants (bcd_newton_inst.cu, one object per KPT)
 #define NT_DECL(K) const void* somf_nt_kernel_##K(int T, int M, int gen);
-NT_DECL(16) NT_DECL(32) NT_DECL(48) NT_DECL(64) NT_DECL(72) NT_DECL(80) NT_DECL(96)
+NT_DECL(16) NT_DECL(32) NT_DECL(48) NT_DECL(64) NT_DECL(72) NT_DECL(80) NT_DECL(96) NT_DECL(128)
 #undef NT_DECL
 struct NtVariant { int kpt; const void* (*get)(int, int, int); };
 static const NtVariant kNtVariants[] = {{16, somf_nt_kernel_16}, {32, somf_nt_kernel_32}, {48, somf_nt_kernel_48},
                                         {64, somf_nt_kernel_64}, {72, somf_nt_kernel_72}, {80, somf_nt_kernel_80},
-                                        {96, somf_nt_kernel_96}};
+                                        {96, somf_nt_kernel_96}, {128, somf_nt_kernel_128}};
 
 // threads per group of M = 2 masked rows in the simultaneous-threshold kernel:
 // 4 (default), SOMF_NT_T=2 selects pairs (diagnostics / tuning)
@@ -687,16 +687,20 @@ static void choose_newton(somf_ctx* h) {
   const int gen = h->cfg.mu > 0.0 || h->cfg.pos_dict;
   const int max_thr = M == 1 ? 640 : NtCfg<4, 2>::kThreads;
   const int64_t groups = ceil_div(cap, M);
-  if (T * groups > max_thr) return;
-  const int nthr = (int)std::max<int64_t>(64, ceil_div((int64_t)T * groups, 32) * 32);
   for (const NtVariant& v : kNtVariants) {
     if (v.kpt < k) continue;
-    const void* fn = v.get(T, M, gen);
+    // KPT = 128: 8 threads per group keep the residual at 2 x 16 registers
+    const int Tv = (v.kpt > 96 && M == 2) ? 8 : T;
+    if (Tv * groups > max_thr) return;
+    // >= k threads: the per-atom statistics and threshold updates run one thread per atom
+    const int nthr = (int)std::max<int64_t>(ceil_div(std::max(64, k), 32) * 32, ceil_div((int64_t)Tv * groups, 32) * 32);
+    if (nthr > max_thr) return;
+    const void* fn = v.get(Tv, M, gen);
     if (!fn) return;
     const int LD = v.kpt + 1;
-    const int KT = v.kpt / T, KTS = (KT + 3) & ~3;
+    const int KT = v.kpt / Tv, KTS = (KT + 3) & ~3;
     const size_t blk = ((size_t)(cap + 1) * LD + 3) & ~(size_t)3;
-    const size_t ct = (size_t)T * ((((size_t)v.kpt * KTS + 31) & ~(size_t)31) + 8);   // T x CTS (bcd_newton.cuh)
+    const size_t ct = (size_t)Tv * ((((size_t)v.kpt * KTS + 31) & ~(size_t)31) + 8);   // T x CTS (bcd_newton.cuh)
     const int ct_in_w = ct <= blk;
     const size_t H = std::max(1, nthr / k);
     const size_t part = 5 * H * v.kpt;             // stats partials (words)

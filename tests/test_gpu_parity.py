@@ -104,6 +104,7 @@ CASES = {
     "enet_enet": (2500, 36, 40, dict(lam=0.05, nu=0.0, mu=0.5, r=4.0), "fmri"),
     "ridge_l2_r1": (700, 20, 30, dict(lam=0.2, nu=1.0, mu=1.0, r=1.0), "tiny"),
     "lasso_k256_ragged": (1520, 256, 33, dict(lam=0.05, nu=0.0, mu=1.0, r=3.0), "hyper"),
+    "nmf_k128": (2600, 128, 40, dict(lam=0.05, nu=1.0, pos_code=True, mu=1.0, pos_dict=True, r=8.0), "nmf"),
 }
 
 
@@ -136,8 +137,8 @@ def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
 @pytest.mark.parametrize("bcd_kernel", ["global", "onchip", "newton"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_one_step_parity(somf, name, bcd_kernel):
-    if bcd_kernel == "newton" and CASES[name][1] > 96:
-        pytest.skip("simultaneous-threshold kernel covers k <= 96")
+    if bcd_kernel == "newton" and CASES[name][1] > 128:
+        pytest.skip("simultaneous-threshold kernel covers k <= 128")
     ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel=bcd_kernel)
     assert gpu.bcd_variant == bcd_kernel
     batch = X[:, k + 5 * eta:k + 6 * eta]
