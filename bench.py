@@ -398,9 +398,9 @@ def run_somf(args):
     batches = [stream_gen.batch(args.burn_in + b)[lo:hi] for b in range(nb)]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
 
-    def make(rr, burn_in):
+    def make(rr, burn_in, b_mode="masked"):
         m = somf_pkg.Somf(p, k, eta, lam=w["lam"], nu=w["nu"], mu=w["mu"], pos_code=w["pos_code"],
-                          row_lo=lo, row_hi=hi,
+                          row_lo=lo, row_hi=hi, b_mode=b_mode,
                           pos_dict=w["pos_dict"], r=rr, u=w["u"], seed=0, device=dev.index, stream=stream)
         if world > 1:
             m.set_reducer(somf_pkg.dist_reducer())      # NCCL allreduce at every exchange point
@@ -551,6 +551,18 @@ def run_somf(args):
                                      "bcd_kernel": m3.bcd_variant,
                                      "bcd_grid_reductions": m3.last_step_info()["bcd_reductions"]}
             del m3
+        # mode F (Alg. 3 as printed): the rows outside M_t also update
+        # their Bbar, on a side stream beside the BCD
+        m3 = make(r, args.burn_in, b_mode="full")
+        for i in range(3):
+            m3.partial_fit(batches[i % nb])
+        torch.cuda.synchronize()
+        t3 = time_steps(m3, batches, 3, 5, flush, stream)
+        sm = sum(t3) / len(t3)
+        sweep[f"r={int(r)} b_mode=full"] = {"columns_per_s": eta / (sm * 1e-3), "ms_per_step": sm,
+                                             "bcd_kernel": m3.bcd_variant,
+                                             "bcd_grid_reductions": m3.last_step_info()["bcd_reductions"]}
+        del m3
 
     # --- the other BASELINE workloads (single GPU, secondary lines) -----------------
     # cfgB hyperspectral (k = 256, lasso codes, l2-ball atoms) at r = 1/4/12 and

@@ -27,7 +27,7 @@ constexpr int kBtThreads = 256;
 constexpr int kBtM = 128;
 
 struct BtArgs {
-  const int32_t* idx;       // masked local rows (ascending): the Bbar rows
+  const int32_t* idx;       // masked local rows (ascending): the Bbar rows; null = every row (mode F)
   int xcompact;             // X holds only the masked rows (row m of X = m-th masked row)
   const int64_t* q_dev;
   const float* X;           // rows x ldx (or q x ldx when compact)
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
   for (int64_t t0 = lo; t0 < hi; t0 += kBtM) {
     const int n = (int)(hi - t0 < (int64_t)kBtM ? hi - t0 : (int64_t)kBtM);
     __syncthreads();                                   // previous tile's epilogue done with smem
-    for (int r = tid; r < kBtM; r += kBtThreads) grow[r] = r < n ? P.idx[t0 + r] : 0;
+    for (int r = tid; r < kBtM; r += kBtThreads) grow[r] = r < n ? (P.idx ? P.idx[t0 + r] : (int)(t0 + r)) : 0;
     __syncthreads();
     // old Bbar rows of the tile (async; consumed by the epilogue)
     for (int e = tid; e < n * (kp / 4); e += kBtThreads) {

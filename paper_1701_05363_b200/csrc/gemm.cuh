@@ -171,6 +171,61 @@ k_bbar_update(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev
 }
 
 // ---------------------------------------------------------------------------
+// Mode F (Alg. 3 as printed): P_t^perp Bbar <- (1 - w)
+// P_t^perp Bbar + (w / eta) P_t^perp X A^T -- the rows OUTSIDE M_t, which the
+// BCD never reads, so this runs on a side stream concurrently with it.  Rows
+// in M_t are recognised from the Philox rule itself (R1), no index list; they
+// are skipped (the masked-row kernel updates them).  Small footprint (17 KB
+// shared, <= 64 registers) so CTAs fit next to the persistent BCD CTAs.
+__global__ void __launch_bounds__(kGemmThreads, 4)      // <= 64 registers: fits next to a BCD CTA
+k_bbar_comp(const float* __restrict__ X, int64_t ldx, int eta, const float* __restrict__ A, int k,
+            float* __restrict__ Bbar, int kp, const double* __restrict__ w_dev, int64_t rows, int64_t row_lo,
+            uint64_t seed, const int64_t* __restrict__ t_dev, uint64_t T) {
+  __shared__ __align__(16) float Xs[TK][TM + 4];   // [s][row]
+  __shared__ __align__(16) float As[TK][TN + 4];   // [s][atom]
+  const double w = *w_dev;
+  const uint64_t t = (uint64_t)*t_dev;
+  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+  const int a0 = blockIdx.y * TN;
+  for (int64_t m0 = (int64_t)blockIdx.x * TM; m0 < rows; m0 += (int64_t)gridDim.x * TM) {
+    float acc[4][4] = {};
+    for (int s0 = 0; s0 < eta; s0 += TK) {
+#pragma unroll
+      for (int pass = 0; pass < (TM * TK) / kGemmThreads; ++pass) {
+        const int e = pass * kGemmThreads + tid;
+        const int rr = e / TK, ss = e % TK;
+        const int64_t m = m0 + rr;
+        Xs[ss][rr] = (m < rows && s0 + ss < eta) ? X[m * ldx + s0 + ss] : 0.f;
+      }
+#pragma unroll
+      for (int pass = 0; pass < (TN * TK) / kGemmThreads; ++pass) {
+        const int e = pass * kGemmThreads + tid;
+        const int aa = e / TK, ss = e % TK;
+        As[ss][aa] = (a0 + aa < k && s0 + ss < eta) ? A[(int64_t)(a0 + aa) * eta + s0 + ss] : 0.f;
+      }
+      __syncthreads();
+      mma_tile_4x4(Xs, As, ty, tx, acc);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t m = m0 + ty * 4 + i;
+      if (m >= rows) continue;
+      const int64_t grow = row_lo + m;                                  // global row (R1 keys)
+      const uint32_t bits = mask_bits(seed, t, grow >> 2, grow & ~3, (grow & ~3) + 4, T);
+      if (bits & (1u << (grow & 3))) continue;                         // in M_t: masked kernel
+      float* brow = Bbar + m * kp;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int a = a0 + tx * 4 + j;
+        if (a < k) brow[a] = fmaf(keep, brow[a], add * acc[i][j]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // (a5) colsq[c] += sum_i (X[i][c] - sum_a D[i][a] A[a][c])^2 over local rows.
 // grid = (row tiles (persistent), ceil(m/TN)).  float64 atomics (objective
 // only; not on the per-iteration path).

@@ -96,6 +96,9 @@ struct somf_ctx {
   int kp = 0;                // k padded to a multiple of 4
   int dev = 0, nsm = 148;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;        // side stream: mode F complement rows beside the BCD
+  cudaEvent_t ev_codes = nullptr, ev_comp = nullptr;
+  bool comp_pending = false;
   std::string err;
   bool initialized = false;
   bool mask_ready = false;   // idx/q hold the draw of iteration t+1
@@ -300,13 +303,16 @@ static const Bb3Variant kBb3Variants[] = {BB3(1, 4), BB3(1, 8), BB3(1, 16), BB3(
 // Bbar rows (masked list, or all rows when !gather) -- bbar.cuh.  false when
 // the layout does not allow the 16-byte path (caller uses k_bbar_update).
 // *folded (optional) is set when the Cbar update rode along (v3 kernel, cpart ready)
+// all_rows: the tensor-core kernel over every row (mode F: the same update for
+// the rows in and outside M_t); returns false, launching nothing, if it does
+// not apply
 static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_t* q_dev, int64_t q_est,
-                           const float* X, int64_t ldx, bool* folded = nullptr) {
+                           const float* X, int64_t ldx, bool* folded = nullptr, bool all_rows = false) {
   if (folded) *folded = false;
   const int k = h->cfg.k, eta = h->cfg.eta;
   if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15)) return false;
   static const bool tc_off = std::getenv("SOMF_BBAR_TC") && std::atoi(std::getenv("SOMF_BBAR_TC")) == 0;
-  if (gather && !tc_off && k <= 256) {
+  if ((gather || all_rows) && !tc_off && k <= 256) {
     // tensor cores (bbar_tc.cuh): bf16x3 tcgen05 GEMM per 128 masked rows
     BtArgs a{};
     a.np = (k + 15) & ~15;
@@ -315,8 +321,8 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
     if (smem <= 220 * 1024 &&
         cudaFuncSetAttribute((const void*)k_bbar_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
             cudaSuccess) {
-      a.idx = h->idx;
-      a.xcompact = xcompact;
+      a.idx = all_rows ? nullptr : h->idx;
+      a.xcompact = all_rows ? 0 : xcompact;
       a.q_dev = q_dev;
       a.X = X;
       a.ldx = ldx;
@@ -335,6 +341,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
     }
     cudaGetLastError();
   }
+  if (all_rows) return false;
   int kc = (k + 31) / 32;
   if (kc > 4) kc = 8;
   const int64_t per = ceil_div(std::max<int64_t>(q_est, 1), h->nsm);
@@ -966,6 +973,12 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   h->T = (uint64_t)std::floor(4294967296.0 / c.r);   // R2
   auto fail = [&](somf_status s) { *out = h; return s; };
   if (cudaSetDevice(c.device) != cudaSuccess) { set_err(h, "cudaSetDevice failed"); return fail(SOMF_E_CUDA); }
+  if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_codes, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_comp, cudaEventDisableTiming) != cudaSuccess) {
+    set_err(h, "stream / event creation failed");
+    return fail(SOMF_E_CUDA);
+  }
   cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, c.device);
   const int k = c.k;
   const int64_t rows = h->rows;
@@ -1065,6 +1078,9 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
                   h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32};
+  if (h->st2) cudaStreamDestroy(h->st2);
+  if (h->ev_codes) cudaEventDestroy(h->ev_codes);
+  if (h->ev_comp) cudaEventDestroy(h->ev_comp);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->sh_alloc) {
@@ -1220,13 +1236,32 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     PhaseScope ps(h, SOMF_PH_BBAR);
     const int grid_a = (int)ceil_div(k, TN);
     if (c.b_mode == SOMF_B_FULL) {
+      // mode F (P:602 + P:612): every row gets the same update.  On the tensor
+      // cores in one launch over all rows when the bf16x3 kernel applies ...
       k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
-      if (!launch_bbar_v2(h, false, false, h->qfull_dev, h->rows, Xd, ld)) {
-        const int grid_r = (int)std::min<int64_t>(ceil_div(h->rows, TM), 8 * h->nsm);
-        k_bbar_update<false, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
-            nullptr, h->qfull_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+      if (launch_bbar_v2(h, false, false, h->qfull_dev, h->rows, Xd, ld, &cbar_folded, true)) {
+        h->launches[SOMF_PH_BBAR] += 2;
+      } else {
+        // ... else the rows in M_t first (the BCD reads them) and the rows
+        // outside M_t on the side stream beside the BCD (k_bbar_comp)
+        if (launch_bbar_v2(h, true, compact, h->q_dev, q_est, Xd, ld, &cbar_folded)) {
+          h->launches[SOMF_PH_BBAR] += 1;
+        } else {
+          const int grid_r = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(q_est, TM), 8 * h->nsm));
+          k_bbar_update<true, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
+              h->idx, h->q_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
+          h->launches[SOMF_PH_BBAR] += 1;
+        }
+        CK(cudaEventRecord(h->ev_codes, h->st));
+        CK(cudaStreamWaitEvent(h->st2, h->ev_codes, 0));
+        const int grid_c = (int)std::min<int64_t>(ceil_div(h->rows, TM), 2 * h->nsm);
+        k_bbar_comp<<<dim3(grid_c, grid_a), kGemmThreads, 0, h->st2>>>(Xd, ld, eta, h->A32, k, h->Bbar, h->kp,
+                                                                       h->w_dev, h->rows, c.row_lo, c.seed,
+                                                                       h->t_dev, h->T);
+        CK(cudaEventRecord(h->ev_comp, h->st2));
+        h->comp_pending = true;
+        h->launches[SOMF_PH_BBAR] += 1;
       }
-      h->launches[SOMF_PH_BBAR] += 2;
     } else if (launch_bbar_v2(h, true, compact, h->q_dev, q_est, Xd, ld, &cbar_folded)) {
       // (Cbar rides along when cbar_folded: Eq. somf_partial)
       h->launches[SOMF_PH_BBAR] += 1;
@@ -1353,6 +1388,11 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
                                    smem, h->st));
     }
     h->launches[SOMF_PH_BCD] += 1;
+  }
+  if (h->comp_pending) {
+    // the caller's stream sees the complete Bbar when the call's work is done
+    CK(cudaStreamWaitEvent(h->st, h->ev_comp, 0));
+    h->comp_pending = false;
   }
   h->steps_prof += 1;
   return post_call(h);

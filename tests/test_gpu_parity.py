@@ -159,6 +159,33 @@ def test_one_step_parity(somf, name, bcd_kernel):
     np.testing.assert_array_equal(st["D"][notS], ora.D[notS].astype(np.float32))
 
 
+@pytest.mark.parametrize("name", ["ridge_l1_fmri_small", "lasso_l2_hyper_small", "nmf_k128"])
+def test_one_step_parity_full_mode(somf, name):
+    """Mode F (Alg. 3 as printed): Bbar rows OUTSIDE the mask are also
+    updated, (1 - w) Bbar + (w / eta) X A^T, every row -- vs the oracle's mode F."""
+    p, k, eta, kw, kind = CASES[name]
+    X = _data(kind, p, k + 8 * eta)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=3, b_mode="F", **kw))
+    ora.set_components(X[:, :k])
+    for t in range(5):
+        ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
+    ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
+    gpu = somf.Somf(p, k, eta, seed=3, debug=True, b_mode="full", **kw)
+    gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
+    for s in range(2):
+        batch = X[:, k + (5 + s) * eta:k + (6 + s) * eta]
+        out = ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+        st = gpu.get_state()
+        errs = dict(Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar), D=rel(st["D"], ora.D))
+        assert all(v <= TOL_STEP for v in errs.values()), (s, errs)
+        notS = np.setdiff1d(np.arange(p), out["S"])
+        # the complement rows moved (mode F) ...
+        assert rel(st["Bbar"][notS], ora.Bbar[notS]) <= TOL_STEP
+        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
+                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
+
+
 @pytest.mark.parametrize("name", ["cfgA_ridge_l1", "lasso_l2_hyper_small", "nmf_small"])
 def test_masked_api_and_pinned_input_match(somf, name):
     ora, gpu, X, (p, k, eta) = _pair(somf, name)
