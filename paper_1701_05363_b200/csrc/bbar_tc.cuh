@@ -39,6 +39,7 @@ struct BtArgs {
   int np;                   // N: k rounded up to 16
   int ep;                   // eta rounded up to 16
   CbarFold cf;
+  int pdl;                  // launched as a programmatic dependent of the code solver
 };
 
 __device__ __forceinline__ void bt_split(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
@@ -95,30 +96,31 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
   uint8_t* Bhi = Alo + a_bytes;
   uint8_t* Blo = Bhi + b_bytes;
   float* Bold = reinterpret_cast<float*>(Blo + b_bytes);        // 128 x kp
-  if (P.cf.cpart) {
-    // my slice of the Cbar entries (Eq. somf_partial)
-    const int e0 = (int)((int64_t)P.cf.kk * blockIdx.x / G), e1 = (int)((int64_t)P.cf.kk * (blockIdx.x + 1) / G);
-    for (int e = e0 + tid; e < e1; e += kBtThreads) {
-      double s = 0.0;
-      for (int bq = 0; bq < P.cf.nparts; ++bq) s += P.cf.cpart[(size_t)bq * P.cf.kk + e];
-      const double c = (1.0 - w) * P.cf.C64[e] + (w / eta) * s;
-      P.cf.C64[e] = c;
-      P.cf.C32[e] = (float)c;
+  // Everything the code solver writes (the codes A, the Cbar partials) is read
+  // only after griddepcontrol.wait: with programmatic dependent launch the CTAs
+  // start while the solver still runs and stage their first tile of X rows and
+  // old Bbar rows (written by earlier kernels) in the meantime.
+  auto after_solver = [&]() {
+    if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (P.cf.cpart) {
+      // my slice of the Cbar entries (Eq. somf_partial)
+      const int e0 = (int)((int64_t)P.cf.kk * blockIdx.x / G), e1 = (int)((int64_t)P.cf.kk * (blockIdx.x + 1) / G);
+      for (int e = e0 + tid; e < e1; e += kBtThreads) {
+        double s = 0.0;
+        for (int bq = 0; bq < P.cf.nparts; ++bq) s += P.cf.cpart[(size_t)bq * P.cf.kk + e];
+        const double c = (1.0 - w) * P.cf.C64[e] + (w / eta) * s;
+        P.cf.C64[e] = c;
+        P.cf.C32[e] = (float)c;
+      }
     }
+  };
+  if (hi <= lo) {
+    after_solver();
+    return;
   }
-  if (hi <= lo) return;
   if (wid == 0) tc_alloc(&tmem_s, np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256);
   if (tid == 0) mbar_init(&mbar, 1);
-  // ---- B = codes (N = np x K = ep), split, once per CTA ------------------------------
-  for (int e = tid; e < np * nch; e += kBtThreads) {
-    const int n = e % np, c = e / np;              // n fastest: conflict-free 16-byte stores
-    float v[8];
-    if (n < k) bt_load8(P.A + (int64_t)n * eta, 8 * c, eta, false, v);
-    else
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = 0.f;
-    bt_store_chunk(v, Bhi, Blo, bt_off(n, 8 * c, nch));
-  }
+  bool waited = false;
   const uint32_t idesc = tc_idesc_bf16(kBtM, np);
   uint32_t phase = 0;
   for (int64_t t0 = lo; t0 < hi; t0 += kBtM) {
@@ -159,6 +161,20 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
           const int e = e0 + u * kBtThreads;
           if (e < kBtM * nch) bt_store_chunk(v[u], Ahi, Alo, bt_off(e % kBtM, 8 * (e / kBtM), nch));
         }
+      }
+    }
+    if (!waited) {
+      after_solver();
+      waited = true;
+      // ---- B = codes (N = np x K = ep), split, once per CTA ----
+      for (int e = tid; e < np * nch; e += kBtThreads) {
+        const int n = e % np, c = e / np;            // n fastest: conflict-free 16-byte stores
+        float v[8];
+        if (n < k) bt_load8(P.A + (int64_t)n * eta, 8 * c, eta, false, v);
+        else
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = 0.f;
+        bt_store_chunk(v, Bhi, Blo, bt_off(n, 8 * c, nch));
       }
     }
     tc_fence_smem_to_async();

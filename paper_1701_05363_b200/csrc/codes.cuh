@@ -50,6 +50,9 @@ __global__ void __launch_bounds__(kRcThreads)
 k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int k, int m, double lam,
               double* __restrict__ A64, float* __restrict__ A32, float* __restrict__ AT32, int ldt,
               double* __restrict__ cpart, int* __restrict__ err, long long* __restrict__ prof) {
+  // the B-bar kernel may launch now (programmatic dependent launch); it reads
+  // the codes only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ double rc_smem[];
   long long t_mark = clock64();
 #define RC_MARK(slot)                                                     \

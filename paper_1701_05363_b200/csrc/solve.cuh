@@ -101,6 +101,9 @@ k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m
      double l1, double l2, int positive, double tol, int max_sweeps,
      double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out,
      float* __restrict__ AT32, int ldt) {
+  // the B-bar kernel may launch now (programmatic dependent launch); it reads
+  // the codes only after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ float Pk[];            // packed upper triangle, k(k+1)/2
   const int tid = threadIdx.x, nt = blockDim.x;
   const int np = k * (k + 1) / 2;

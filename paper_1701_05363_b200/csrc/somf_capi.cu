@@ -336,7 +336,24 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
         a.cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32};
         *folded = true;
       }
-      k_bbar_tc<<<h->nsm, kBtThreads, smem, h->st>>>(a);
+      // programmatic dependent launch: the CTAs stage their first X tile while
+      // the code solver still runs (k_bbar_tc waits before reading the codes)
+      a.pdl = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(h->nsm);
+      cfg.blockDim = dim3(kBtThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = h->st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, k_bbar_tc, a) != cudaSuccess) {
+        cudaGetLastError();
+        if (folded) *folded = false;
+        return false;
+      }
       return true;
     }
     cudaGetLastError();
