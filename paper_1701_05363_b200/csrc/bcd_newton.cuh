@@ -1,5 +1,5 @@
 // bcd_newton.cuh -- (a4) Alg. 4 with all k projection thresholds
-// solved SIMULTANEOUSLY (v3), for k <= 96 and masked rows that fit on chip.
+// solved SIMULTANEOUSLY (v5), for k <= 128 and masked rows that fit on chip.
 //
 // Alg. 4 visits the atoms in the order pi; atom j's update
 //   u = d_j + (bbar_j - D c_j) / c_jj ,  d_j <- Proj(u; rho_j)
@@ -9,21 +9,22 @@
 // Given ALL thresholds, every masked row runs the whole recurrence on its own
 // (no communication).  So instead of one grid reduction per atom (v1/v2), this
 // kernel iterates rounds:
-//   1. every row runs the full recurrence with the current lambda_1..k
-//      (thread per row, residual R = P Bbar - P D Cbar in registers, the atom
-//      loop fully unrolled in permutation order so R is indexed statically);
+//   1. every row runs the full recurrence with the current lambda_1..k (groups
+//      of T lanes own M rows, the prescaled residual in registers, the atom
+//      loop fully unrolled in permutation order so the arrays stay in
+//      registers; see NtRec5);
 //   2. ONE grid reduction returns, per atom, the sums (count, S1, S2) of the
 //      |v| above its threshold, the smallest |v| above and the largest below;
 //   3. every CTA applies the same Michelot step lambda_j <- root of the
 //      active-set quadratic (R17) for the set {|v_j| > a lambda_j}.
-// The recurrence is triangular (atom j depends only on earlier atoms), so once
-// atoms 1..j-1 are fixed atom j's set can only shrink (Michelot from a
-// superset) and the iteration is finite.  It stops when every atom is EXACT
-// (largest |v| below <= a lambda' < smallest |v| above: the active set of the
-// new root is the one it was computed from) and lambda' equals lambda to
-// kNtLamTol: then the round's D is Alg. 4's result to fp32 rounding.  Radii
-// ride on round 0's reduction.  Warm start: lambda of the previous iteration.
-// Identical reduced values in every CTA => identical decisions.
+// The recurrence is triangular (atom j depends only on earlier atoms), so the
+// iteration is finite.  It stops when every atom is EXACT (largest |v| below
+// <= a lambda' < smallest |v| above: the active set of the new root is the one
+// it was computed from) and lambda' equals lambda to kNtLamTol: then the
+// round's D is Alg. 4's result to fp32 rounding.  Radii ride on round
+// 0's reduction.  Warm start: lambda of the previous iteration.  Identical
+// reduced values in every CTA => identical decisions.  The kernel also draws
+// the mask of the next iteration (NtArgs draw-ahead fields).
 #pragma once
 #include "common.cuh"
 
