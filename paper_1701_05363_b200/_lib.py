@@ -50,9 +50,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         base.append("-Xptxas=-v")
 
+    headers = [s for s in _sources() if not s.endswith(".cu")]
+    newest_hdr = max(os.path.getmtime(s) for s in headers)
+
     def compile_one(unit):
         name, src, extra = unit
         obj = os.path.join(objdir, name + ".o")
+        # an object is reused when it is newer than its source and every header
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) >= max(newest_hdr, os.path.getmtime(src))):
+            return name, obj, subprocess.CompletedProcess([], 0, "", "")
         res = subprocess.run(base + extra + ["-c", src, "-o", obj], capture_output=True, text=True)
         return name, obj, res
 

@@ -10,15 +10,22 @@
 #define NT_CAT2(a, b) a##b
 #define NT_CAT(a, b) NT_CAT2(a, b)
 
-// T threads x M rows per group; gen = generic parameters (mu > 0 or D >= 0)
+// T threads x M rows per group; gen = generic parameters (mu > 0 or D >= 0).
+// KPT = 128 only needs 8 x 2 (the residual of 4 x 2 would not fit the
+// registers); the smaller KPT also get 4 x 1 and 2 x 2 (SOMF_NT_M / SOMF_NT_T
+// tuning options).  Fewer variants keep the build of the 128-position
+// straight-line recurrences short.
 const void* NT_CAT(somf_nt_kernel_, NT_KPT)(int T, int M, int gen) {
+#if NT_KPT > 96
+  if (T == 8 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, true>
+                                   : (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, false>;
+#else
   if (T == 4 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, true>
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, false>;
   if (T == 4 && M == 1) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, true>
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, false>;
-  if (T == 8 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, true>
-                                   : (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, false>;
   if (T == 2 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, true>
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, false>;
+#endif
   return nullptr;
 }
