@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SOMF_ABI_VERSION 1
+#define SOMF_ABI_VERSION 2
 
 typedef struct somf_ctx* somf_handle;
 
@@ -91,11 +91,36 @@ typedef struct somf_config {
   void* stream;           /* cudaStream_t (NULL = legacy default stream)         */
   int32_t debug;          /* 1: synchronise and check after every call          */
   int32_t bcd_kernel;     /* Alg. 4 kernel: 0 = auto (simultaneous-threshold
-                             when k <= 96 and the masked rows fit on chip, else
+                             when k <= 128 and the masked rows fit on chip, else
                              on-chip per-atom, else global), 1 = global-memory
                              per-atom kernel, 2 = on-chip per-atom kernel,
                              3 = simultaneous-threshold kernel
                              (SOMF_E_UNSUPPORTED at create if it cannot fit)   */
+  /* Kernel selection of the other phases (0 = auto everywhere).  Every value
+   * computes the same step (parity tests force each one); a forced variant
+   * whose shape limits the call violates returns SOMF_E_UNSUPPORTED from the
+   * call that needs it.                                                     */
+  int32_t contract_kernel;/* (a1) beta, G (Eq. a): 0 auto, 1 tcgen05 3xTF32
+                             (k <= 128, eta + k <= 512, eta % 4 == 0),
+                             2 FFMA whole-slice (fused split-K), 3 FFMA tiled
+                             (register tiles + reduce kernel), 4 generic FFMA */
+  int32_t bbar_kernel;    /* (a3) P_t Bbar (Eq. somf_partial): 0 auto,
+                             1 tcgen05 bf16x3, 2 FFMA whole-slice, 3 FFMA
+                             tiled, 4 generic; mode FULL with a value other
+                             than 0 / 1 runs the complement rows on a side
+                             stream beside Alg. 4 (k_bbar_comp)             */
+  int32_t codes_kernel;   /* (a2) codes (Eq. somf_alpha): 0 auto, 1 ridge
+                             Cholesky (nu = 1, no positivity, k <= 160),
+                             2 coordinate descent with exact support jumps
+                             (k >= 32), 3 plain cyclic coordinate descent     */
+  double bcd_lam_tol;     /* simultaneous-threshold Alg. 4: relative
+                             tolerance on each projection multiplier between
+                             two rounds (0 = default 1e-5)     */
+  int32_t bcd_copies;     /* simultaneous-threshold Alg. 4: copies of each
+                             per-atom grid accumulator (1..16, 0 = 8); a
+                             performance knob only: the sums are fixed-point
+                             integers, so results are bit-identical for any
+                             value and any CTA arrival order                 */
 } somf_config;
 
 /* Fills *cfg with defaults: u = 0.917, r = 1, nu = 1, mu = 0,
@@ -188,6 +213,15 @@ somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* bcd_reductio
  * resident in registers + shared memory), 3 = on-chip simultaneous-threshold
  * rounds (all k thresholds per grid reduction).  0 on a null handle. */
 int32_t somf_bcd_variant(somf_handle h);
+
+/* Kernel variants the last somf_partial_fit ran (host int32 out[5]):
+ * out[0] contraction (1 tcgen05, 2 FFMA whole-slice, 3 FFMA tiled, 4 generic),
+ * out[1] codes (1 ridge Cholesky, 2 CD with support jumps, 3 plain CD),
+ * out[2] P_t Bbar (1 tcgen05, 2 FFMA whole-slice, 3 FFMA tiled, 4 generic),
+ * out[3] Alg. 4 (as somf_bcd_variant; 4 = row-sharded rounds),
+ * out[4] 1 when mode FULL ran the complement rows on the side stream.
+ * 0 before the first step.  Does not synchronise. */
+somf_status somf_last_kernels(somf_handle h, int32_t* out);
 
 /* SM-cycle breakdown of the simultaneous-threshold BCD kernel (CTA 0), summed
  * over the launches made while somf_profile_enable(h, 1) was on, then reset:

@@ -91,6 +91,8 @@ class SomfConfig(C.Structure):
         ("seed", C.c_uint64), ("row_lo", C.c_int64), ("row_hi", C.c_int64),
         ("device", C.c_int32), ("stream", C.c_void_p), ("debug", C.c_int32),
         ("bcd_kernel", C.c_int32),
+        ("contract_kernel", C.c_int32), ("bbar_kernel", C.c_int32), ("codes_kernel", C.c_int32),
+        ("bcd_lam_tol", C.c_double), ("bcd_copies", C.c_int32),
     ]
 
 
@@ -117,6 +119,7 @@ SIGNATURES = [
     ("somf_set_state", I32, [P, P, P, P, P, I64]),
     ("somf_last_step_info", I32, [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(D)]),
     ("somf_bcd_variant", I32, [P]),
+    ("somf_last_kernels", I32, [P, P]),
     ("somf_set_reducer", I32, [P, P, P]),
     ("somf_bcd_phase_cycles", I32, [P, P]),
     ("somf_profile_enable", I32, [P, I32]),

@@ -32,7 +32,9 @@ namespace somf {
 
 constexpr int kNtRing = 3;
 constexpr int kNtMaxK = 128;        // largest k of the simultaneous-threshold kernel
-constexpr int kNtRec = 16;          // doubles per accumulator record (128 bytes)
+constexpr int kNtRec = 16;          // 64-bit words per accumulator record (128 bytes)
+constexpr int kNtMaxCopies = 16;    // copies of each record (CTA b adds into copy b % ncopy)
+
 // Convergence: every atom exact (its active set reproduces itself) and its
 // lambda stable to this relative tolerance between two rounds.  The
 // recurrence runs in fp32 (v, d carry ~1e-7 relative rounding); a lambda
@@ -63,12 +65,15 @@ struct NtArgs {
   int part_in_cpi;           // the stats partials (5 H KPT words) fit the Cbar staging area
   int max_rounds;
   double lam_tol;           // convergence tolerance on lambda (kNtLamTol)
-  // per-atom grid accumulators, one 128-byte record each so the 148-way
-  // atomics of different atoms land in different L2 slices:
-  //   rec[((slot * k) + p) * kNtRec + {0,1,2}] = count, S1, S2 (fp64, zero between uses)
-  //   ((unsigned*)(rec + ... + 3))[0 / 1]     = min |v| above / max |v| below (float bits)
-  // slots 0..kNtRing-1: the round ring; slot kNtRing: radius sums in {0,1}
-  double* rec;
+  // per-atom grid accumulators, 128-byte records (u64 words) so the atomics
+  // of different atoms land in different L2 slices, ncopy copies per atom so
+  // the same-address chains are ncopy times shorter:
+  //   rec[((slot * ncopy + c) * k + p) * kNtRec + w]: w = 0 count, {1,2} S1
+  //   limbs, {3,4} S2 limbs (fx_red), 5 = two u32: min |v| above / max |v|
+  //   below (float bits); zero (min: all ones) between uses.
+  // slots 0..kNtRing-1: the round ring; slot kNtRing: radius sums in S1 / S2
+  unsigned long long* rec;
+  int ncopy;
   // draw-ahead of iteration t+1 while the CTAs wait on the rounds (null idx_next
   // = off): M_{t+1} (Eq. mt) into idx_next / q_next (per-CTA counts through
   // cnt_next, published before round 0's barrier), t+1 and w_{t+1} = (t+1)^-u
@@ -174,17 +179,40 @@ __device__ __forceinline__ double nt_norm_d(double a, double b, int mode, double
   return 0.0;
 }
 
-__device__ __forceinline__ void nt_rec_reset(double* rc) {
-  rc[0] = 0.0;
-  rc[1] = 0.0;
-  rc[2] = 0.0;
-  unsigned* mm = reinterpret_cast<unsigned*>(rc + 3);
-  mm[0] = 0xffffffffu;
-  mm[1] = 0u;
+__device__ __forceinline__ void nt_rec_reset(unsigned long long* rc) {
+#pragma unroll
+  for (int w = 0; w < 5; ++w) rc[w] = 0ull;
+  rc[5] = 0xffffffffull;          // min above: all ones; max below: 0
 }
 
-__device__ __forceinline__ void nt_red_add(double* p, double v) {
-  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+// the sums of atom p over the ncopy copies of a slot (integers: order-free)
+struct NtSums {
+  double cnt, S1, S2;
+  unsigned mn, mx;
+};
+__device__ __forceinline__ NtSums nt_read(const unsigned long long* slot0, int ncopy, int k, int p) {
+  unsigned long long c = 0, a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+  unsigned mn = 0xffffffffu, mx = 0u;
+  for (int cp = 0; cp < ncopy; ++cp) {
+    const unsigned long long* rc = slot0 + ((size_t)cp * k + p) * kNtRec;
+    const ulonglong2 v01 = __ldcg(reinterpret_cast<const ulonglong2*>(rc));
+    const ulonglong2 v23 = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 2));
+    const ulonglong2 v45 = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 4));
+    c += v01.x;
+    a1 += v01.y;
+    a2 += v23.x;
+    b1 += v23.y;
+    b2 += v45.x;
+    mn = min(mn, (unsigned)(v45.y & 0xffffffffull));
+    mx = max(mx, (unsigned)(v45.y >> 32));
+  }
+  NtSums r;
+  r.cnt = (double)c;
+  r.S1 = fx_value(a1, a2);
+  r.S2 = fx_value(b1, b2);
+  r.mn = mn;
+  r.mx = mx;
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -493,9 +521,10 @@ k_bcd_newton(NtArgs P) {
       d1 = warp_sum(d1);
       d2 = warp_sum(d2);
       if (lane == 0) {
-        double* rr = P.rec + ((size_t)kNtRing * k + p) * kNtRec;
-        nt_red_add(rr, d1);
-        nt_red_add(rr + 1, d2);
+        unsigned long long* rr =
+            P.rec + (((size_t)kNtRing * P.ncopy + blockIdx.x % P.ncopy) * k + p) * kNtRec;
+        const bool ok = fx_red(rr + 1, d1) & fx_red(rr + 3, d2);
+        if (!ok) atomicExch(P.err, 6);
       }
     }
   }
@@ -527,6 +556,12 @@ k_bcd_newton(NtArgs P) {
   int round = 0, cur = 0;
   constexpr int F = 0;          // (no frozen prefix: every round runs every atom)
   bool done = q == 0;
+  if (done && P.idx_next) {
+    // empty mask: no rounds, but the draw-ahead below reads every CTA's count
+    // of M_{t+1}, published above -- one barrier orders them
+    ++nbar;
+    nt_barrier(P.bar, nbar * G);
+  }
 #pragma unroll 1
   while (!done) {
     // ---- 1. the recurrence from the frozen prefix on, T threads x M rows ---------
@@ -587,12 +622,12 @@ k_bcd_newton(NtArgs P) {
           mn = min(mn, pmn[h * KPT + p]);
           mx = max(mx, pmx[h * KPT + p]);
         }
-        double* rc = P.rec + ((size_t)ring * k + p) * kNtRec;
-        unsigned* mm = reinterpret_cast<unsigned*>(rc + 3);
+        unsigned long long* rc = P.rec + (((size_t)ring * P.ncopy + blockIdx.x % P.ncopy) * k + p) * kNtRec;
+        unsigned* mm = reinterpret_cast<unsigned*>(rc + 5);
         if (cnt > 0) {
-          nt_red_add(rc, (double)cnt);
-          nt_red_add(rc + 1, S1);
-          nt_red_add(rc + 2, S2);
+          nt_red_u64(rc, (unsigned long long)cnt);
+          const bool ok = fx_red(rc + 1, S1) & fx_red(rc + 3, S2);
+          if (!ok) atomicExch(P.err, 6);
           atomicMin(mm, mn);
         }
         if (mx) atomicMax(mm + 1, mx);
@@ -605,7 +640,7 @@ k_bcd_newton(NtArgs P) {
     if (blockIdx.x == 0) {
       // recycle the ring slot of the NEXT-but-one round (its readers are done)
       const int rz = (round + 2) % kNtRing;
-      for (int p = tid; p < k; p += nthr) nt_rec_reset(P.rec + ((size_t)rz * k + p) * kNtRec);
+      for (int e = tid; e < P.ncopy * k; e += nthr) nt_rec_reset(P.rec + ((size_t)rz * P.ncopy * k + e) * kNtRec);
     }
     // ---- 3. the same Michelot step for every unfrozen atom in every CTA ----------
     int conv = 1, nmode = 0;
@@ -614,18 +649,15 @@ k_bcd_newton(NtArgs P) {
     const bool act = tid < nact;
     if (act) {
       if (round == 0) {
-        const double* rr = P.rec + ((size_t)kNtRing * k + p) * kNtRec;
-        const double d1 = __ldcg(rr), d2 = __ldcg(rr + 1);
-        rho_s[p] = fmax(0.0, rho_s[p] + a * d1 + 0.5 * b * d2);          // P:860, R9
+        const NtSums rs = nt_read(P.rec + (size_t)kNtRing * P.ncopy * k * kNtRec, P.ncopy, k, p);
+        rho_s[p] = fmax(0.0, rho_s[p] + a * rs.S1 + 0.5 * b * rs.S2);     // P:860, R9
       }
-      const double* acc = P.rec + ((size_t)ring * k + p) * kNtRec;
-      const unsigned* mm = reinterpret_cast<const unsigned*>(acc + 3);
-      cnt = __ldcg(acc);
-      S1 = __ldcg(acc + 1);
-      S2 = __ldcg(acc + 2);
-      const unsigned mnb = __ldcg(mm), mxb = __ldcg(mm + 1);
-      const double mnv = cnt > 0.0 ? (double)__uint_as_float(mnb) : INFINITY;
-      const double mxv = (double)__uint_as_float(mxb);
+      const NtSums sm = nt_read(P.rec + (size_t)ring * P.ncopy * k * kNtRec, P.ncopy, k, p);
+      cnt = sm.cnt;
+      S1 = sm.S1;
+      S2 = sm.S2;
+      const double mnv = cnt > 0.0 ? (double)__uint_as_float(sm.mn) : INFINITY;
+      const double mxv = (double)__uint_as_float(sm.mx);
       conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol);
     }
     // every atom converged: the round's v and parameters are final (a frozen
@@ -721,14 +753,18 @@ k_bcd_newton(NtArgs P) {
   if (tid == 0) {
     __threadfence();
     const unsigned old = atomicAdd(P.bar + 1, 1u);
-    if (old == (unsigned)G - 1) {
-      __threadfence();
-      for (int e = 0; e < (kNtRing + 1) * k; ++e) nt_rec_reset(P.rec + (size_t)e * kNtRec);
+    mcnt_s = old == (unsigned)G - 1;      // (mcnt_s is free now) I am the last CTA out
+  }
+  __syncthreads();
+  if (mcnt_s) {
+    __threadfence();
+    for (int e = tid; e < (kNtRing + 1) * P.ncopy * k; e += nthr) nt_rec_reset(P.rec + (size_t)e * kNtRec);
+    if (tid == 0) {
       if (P.nred_out) *P.nred_out = nbar;
       P.bar[0] = 0u;
       P.bar[1] = 0u;
-      __threadfence();
     }
+    __threadfence();
   }
 }
 

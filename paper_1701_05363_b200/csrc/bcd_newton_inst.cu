@@ -1,6 +1,6 @@
 // bcd_newton_inst.cu -- instantiates the simultaneous-threshold BCD kernel
-// k_bcd_newton<NT_KPT, T, M, gen> (bcd_newton.cuh) for groups of T = 4 or 2
-// threads owning M = 2 masked rows.  Compiled once per NT_KPT (-DNT_KPT=...) so the variants build in
+// k_bcd_newton<NT_KPT, T, M, gen> (bcd_newton.cuh) for groups of T = 4 (8 at
+// KPT = 128) threads owning M = 2 masked rows.  Compiled once per NT_KPT (-DNT_KPT=...) so the variants build in
 // parallel; the C ABI (somf_capi.cu) picks one through somf_nt_kernel_<KPT>.
 #include "bcd_newton.cuh"
 
@@ -11,10 +11,8 @@
 #define NT_CAT(a, b) NT_CAT2(a, b)
 
 // T threads x M rows per group; gen = generic parameters (mu > 0 or D >= 0).
-// KPT = 128 only needs 8 x 2 (the residual of 4 x 2 would not fit the
-// registers); the smaller KPT also get 4 x 1 and 2 x 2 (SOMF_NT_M / SOMF_NT_T
-// tuning options).  Fewer variants keep the build of the 128-position
-// straight-line recurrences short.
+// KPT = 128 uses 8 x 2 (the residual of 4 x 2 would not fit the registers),
+// the smaller KPT 4 x 2.
 const void* NT_CAT(somf_nt_kernel_, NT_KPT)(int T, int M, int gen) {
 #if NT_KPT > 96
   if (T == 8 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 8, 2, true>
@@ -22,10 +20,6 @@ const void* NT_CAT(somf_nt_kernel_, NT_KPT)(int T, int M, int gen) {
 #else
   if (T == 4 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, true>
                                    : (const void*)somf::k_bcd_newton<NT_KPT, 4, 2, false>;
-  if (T == 4 && M == 1) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, true>
-                                   : (const void*)somf::k_bcd_newton<NT_KPT, 4, 1, false>;
-  if (T == 2 && M == 2) return gen ? (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, true>
-                                   : (const void*)somf::k_bcd_newton<NT_KPT, 2, 2, false>;
 #endif
   return nullptr;
 }

@@ -19,7 +19,7 @@
 // Projection threshold (R17), sort-free and exact:
 //   every round reduces, over the grid, for NC candidate thresholds th_c the
 //   sums (count, S1, S2) of the |v_i| > th_c and the smallest such |v_i|
-//   (fp64 red.add / u32 atomicMin into a ring of L2 accumulators, then one
+//   (fixed-point u64 red.add / u32 atomicMin into a ring of L2 accumulators, then one
 //   grid barrier).  Every CTA then evaluates the same decision:
 //     - feasible (||v|| <= rho): lambda = 0;  rho = 0: d = 0;  mu = 1: closed form;
 //     - candidate c is a lower bound iff phi(th_c) = ||shrink(v, th_c)|| >= rho;
@@ -57,9 +57,9 @@ struct OcArgs {
   int pos;                  // D >= 0
   int cs_smem;              // Cbar (fp32) staged in shared memory
   int cap_rows;             // rows per CTA the shared memory holds
-  double* acc;              // [kRing][kNC][3]   (zero between uses)
+  unsigned long long* acc;  // [kRing][kNC][5]: count, S1 limbs, S2 limbs (fx_red; zero between uses)
   unsigned* accmin;         // [kRing][kNC]      (0xffffffff between uses)
-  double* rho_acc;          // [2k]              (zero between uses)
+  unsigned long long* rho_acc;  // [4k]: sum|d_j| limbs, sum d_j^2 limbs (zero between uses)
   unsigned* bar;            // [0] arrivals [1] exits [2] watchdog
   int64_t* nred_out;        // grid reductions performed (diagnostic)
   int* err;                 // 2: more masked rows than capacity
@@ -86,10 +86,6 @@ __device__ __forceinline__ void oc_barrier(unsigned* bar, unsigned target) {
     __threadfence();
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ void red_add_f64(double* p, double v) {
-  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 // ||shrink(v, th)|| from the sums over {|v| > th}: lam = th / a.
@@ -165,8 +161,7 @@ k_bcd_onchip(OcArgs P) {
       s2 += d * d;
     }
     if (nr > 0) {
-      red_add_f64(P.rho_acc + 2 * j, s1);
-      red_add_f64(P.rho_acc + 2 * j + 1, s2);
+      if (!(fx_red(P.rho_acc + 4 * j, s1) & fx_red(P.rho_acc + 4 * j + 2, s2))) atomicExch(P.err, 6);
     }
   }
   // ---- residual R = Bbar_M - D_M Cbar (registers) --------------------------
@@ -199,7 +194,8 @@ k_bcd_onchip(OcArgs P) {
   unsigned nbar = 1;
   oc_barrier(P.bar, nbar * G);
   for (int j = tid; j < k; j += kOcThreads) {
-    const double s1 = __ldcg(P.rho_acc + 2 * j), s2 = __ldcg(P.rho_acc + 2 * j + 1);
+    const double s1 = fx_value(__ldcg(P.rho_acc + 4 * j), __ldcg(P.rho_acc + 4 * j + 1));
+    const double s2 = fx_value(__ldcg(P.rho_acc + 4 * j + 2), __ldcg(P.rho_acc + 4 * j + 3));
     rho_s[j] = fmax(0.0, P.nslack[j] + a * s1 + 0.5 * b * s2);       // P:860, R9
   }
   __syncthreads();
@@ -277,10 +273,9 @@ k_bcd_onchip(OcArgs P) {
           s2 = warp_sum(s2);
           mn = __reduce_min_sync(0xffffffffu, mn);
           if (lane == 0 && cnt > 0.0) {
-            double* acc = P.acc + ((size_t)ring * kNC + wid) * 3;
-            red_add_f64(acc, cnt);
-            red_add_f64(acc + 1, s1);
-            red_add_f64(acc + 2, s2);
+            unsigned long long* acc = P.acc + ((size_t)ring * kNC + wid) * 5;
+            nt_red_u64(acc, (unsigned long long)cnt);
+            if (!(fx_red(acc + 1, s1) & fx_red(acc + 3, s2))) atomicExch(P.err, 6);
             atomicMin(P.accmin + ring * kNC + wid, mn);
           }
         }
@@ -289,17 +284,23 @@ k_bcd_onchip(OcArgs P) {
         if (blockIdx.x == 0 && tid < kNC * 4) {
           // recycle the ring slot two rounds ahead (its last readers are done)
           const int rz = (ring + 2) % kRing;
-          if (tid < kNC * 3) P.acc[(size_t)rz * kNC * 3 + tid] = 0.0;
-          else P.accmin[rz * kNC + (tid - kNC * 3)] = 0xffffffffu;
+          if (tid < kNC * 3) {
+            unsigned long long* z = P.acc + ((size_t)rz * kNC + tid / 3) * 5;
+            if (tid % 3 == 0) z[0] = 0ull;
+            else if (tid % 3 == 1) { z[1] = 0ull; z[2] = 0ull; }
+            else { z[3] = 0ull; z[4] = 0ull; }
+          } else {
+            P.accmin[rz * kNC + (tid - kNC * 3)] = 0xffffffffu;
+          }
         }
         if (wid == 0) {
           const int c = lane;
           double cnt = 0.0, S1 = 0.0, S2 = 0.0, th = 0.0, mnv = 0.0;
           if (c < kNC) {
-            const double* acc = P.acc + ((size_t)ring * kNC + c) * 3;
-            cnt = __ldcg(acc);
-            S1 = __ldcg(acc + 1);
-            S2 = __ldcg(acc + 2);
+            const unsigned long long* acc = P.acc + ((size_t)ring * kNC + c) * 5;
+            cnt = (double)__ldcg(acc);
+            S1 = fx_value(__ldcg(acc + 1), __ldcg(acc + 2));
+            S2 = fx_value(__ldcg(acc + 3), __ldcg(acc + 4));
             mnv = (double)__uint_as_float(__ldcg(P.accmin + ring * kNC + c));
             th = thr_s[c];
           }
@@ -414,9 +415,9 @@ k_bcd_onchip(OcArgs P) {
     const unsigned old = atomicAdd(P.bar + 1, 1u);
     if (old == (unsigned)G - 1) {
       __threadfence();
-      for (int e = 0; e < kRing * kNC * 3; ++e) P.acc[e] = 0.0;
+      for (int e = 0; e < kRing * kNC * 5; ++e) P.acc[e] = 0ull;
       for (int e = 0; e < kRing * kNC; ++e) P.accmin[e] = 0xffffffffu;
-      for (int e = 0; e < 2 * k; ++e) P.rho_acc[e] = 0.0;
+      for (int e = 0; e < 4 * k; ++e) P.rho_acc[e] = 0ull;
       if (P.nred_out) *P.nred_out = nbar;
       P.bar[0] = 0u;
       P.bar[1] = 0u;

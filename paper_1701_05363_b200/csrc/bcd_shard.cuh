@@ -25,6 +25,12 @@
 
 namespace somf {
 
+// fp64 grid sums of one rank's rows (the rank's total is then allreduced:
+// every rank receives the same reduced value, so replicated decisions agree)
+__device__ __forceinline__ void nt_red_add(double* p, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 constexpr int kShMaxK = 256;
 // "no element" for the min-above reduction: +inf bits (so the u32 MIN over
 // ranks is also a valid int32 MIN for the collectives, all values >= 0)

@@ -156,4 +156,33 @@ __device__ __forceinline__ double enet_lambda(double a, double b, double rho, do
   return den > 0.0 ? fmax(2.0 * C / den, 0.0) : 0.0;
 }
 
+// Deterministic grid sums.  The per-atom sums S1, S2 >= 0 are accumulated as
+// fixed-point integers, so the grid total does not depend on the arrival
+// order of the CTAs (integer addition is associative): x in [0, 2^48)
+// becomes floor(x 2^56) split in two limbs < 2^52, hi in units of 2^-4 and lo
+// in units of 2^-56 (absolute resolution 1.4e-17 per CTA term, far below the
+// fp32 rounding of the per-CTA partials).  Each limb sum stays < 2^60.
+constexpr double kFxHi = 16.0;                       // 2^4
+constexpr double kFxLo = 4503599627370496.0;         // 2^52
+constexpr double kFxMax = 281474976710656.0;         // 2^48
+__device__ __forceinline__ void nt_red_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// adds x into the limb pair p[0] (hi), p[1] (lo); false when x is out of range
+// (negative, >= 2^48 or NaN: the sum is then clamped and the caller flags it)
+__device__ __forceinline__ bool fx_red(unsigned long long* p, double x) {
+  const bool ok = x >= 0.0 && x < kFxMax;
+  x = ok ? x : (x >= kFxMax ? kFxMax * 0.999 : 0.0);
+  const double xs = x * kFxHi;
+  const double h = floor(xs);
+  const unsigned long long hi = (unsigned long long)h;
+  const unsigned long long lo = (unsigned long long)((xs - h) * kFxLo);
+  if (hi) nt_red_u64(p, hi);
+  if (lo) nt_red_u64(p + 1, lo);
+  return ok;
+}
+__device__ __forceinline__ double fx_value(unsigned long long hi, unsigned long long lo) {
+  return (double)hi * (1.0 / kFxHi) + (double)lo * (1.0 / (kFxHi * kFxLo));
+}
+
 }  // namespace somf

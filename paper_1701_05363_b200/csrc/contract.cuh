@@ -185,6 +185,7 @@ struct CtFuse {
   double r;
   double* beta;             // k x eta
   double* G;                // k x k
+  int* err;                 // watchdog: set to 5 when the barrier times out (protocol bug)
 };
 
 // Fused fixed-order split-K reduction (CtFuse): grid barrier, then CTA b
@@ -212,7 +213,10 @@ __device__ __forceinline__ void ct_fused_reduce(const float* __restrict__ partia
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(fz.bar), "r"(1u) : "memory");
     const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_gpu(fz.bar) < (unsigned)G) {
-      if (globaltimer_ns() - t0 > 2000000000ull) break;     // protocol bug: do not hang the GPU
+      if (globaltimer_ns() - t0 > 2000000000ull) {          // protocol bug: do not hang the GPU
+        if (fz.err) atomicExch(fz.err, 5);
+        break;
+      }
     }
   }
   __syncthreads();

@@ -1,11 +1,8 @@
 // solve.cuh -- (a2) batched code solve, Eq. (somf_alpha) P:592-596:
 //   alpha_s = argmin_a 1/2 a^T G a - a^T beta_s + lambda Omega(a)   (s = 1..m)
 //
-//  k_ridge_chol : nu = 1, no positivity: (G + lambda I) alpha = beta by a
-//                 float64 Cholesky in shared memory (k <= 160), every CTA
-//                 factorises (no inter-CTA dependency) and solves the RHS of
-//                 its warps (column-oriented substitutions, one warp per RHS).
-//  k_cd         : otherwise cyclic coordinate descent (the paper's solver,
+//  (the ridge closed form lives in codes.cuh)
+//  k_cd         : cyclic coordinate descent (the paper's solver,
 //                 P:1341-1342), one warp per column, maintained gradient
 //                 g = beta - G alpha in float64 registers, G packed (upper
 //                 triangle, float32) in shared memory so k = 256 fits.
@@ -16,77 +13,6 @@ namespace somf {
 
 constexpr int kSolveThreads = 256;
 constexpr int kRidgeMaxK = 160;
-
-// smem: (k*(k+1) + k) doubles + 8 warps * k doubles
-__global__ void __launch_bounds__(kSolveThreads)
-k_ridge_chol(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
-             double lam, double* __restrict__ A64, float* __restrict__ A32,
-             int* __restrict__ err) {
-  extern __shared__ double sm[];
-  const int ld = k + 1;
-  double* M = sm;                         // k x (k+1)
-  double* invd = M + (size_t)k * ld;      // k
-  double* ys = invd + k;                  // nwarps x k
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < k * k; e += nt) {
-    const int i = e / k, j = e % k;
-    M[i * ld + j] = G[e] + (i == j ? lam : 0.0);
-  }
-  __syncthreads();
-  // right-looking, unscaled: M_il -= M_ij M_lj / M_jj for j < l <= i
-  for (int j = 0; j < k; ++j) {
-    const double djj = M[j * ld + j];
-    const int n = k - j - 1;
-    if (n > 0 && djj > 0.0) {
-      const double inv = 1.0 / djj;
-      for (int e = tid; e < n * n; e += nt) {
-        const int i = j + 1 + e / n, l = j + 1 + e % n;
-        if (l <= i) M[i * ld + l] -= M[i * ld + j] * M[l * ld + j] * inv;
-      }
-    }
-    __syncthreads();
-  }
-  // scale: L_ij = M_ij / sqrt(M_jj)
-  for (int j = tid; j < k; j += nt) {
-    const double djj = M[j * ld + j];
-    if (!(djj > 0.0) && err) atomicExch(err, 1);
-    invd[j] = djj > 0.0 ? rsqrt(djj) : 0.0;
-  }
-  __syncthreads();
-  for (int e = tid; e < k * k; e += nt) {
-    const int i = e / k, j = e % k;
-    if (j <= i) M[i * ld + j] *= invd[j];
-  }
-  __syncthreads();
-  for (int j = tid; j < k; j += nt) invd[j] = M[j * ld + j] != 0.0 ? 1.0 / M[j * ld + j] : 0.0;
-  __syncthreads();
-  // substitutions: one warp per right-hand side
-  const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  double* y = ys + (size_t)wid * k;
-  for (int s = blockIdx.x * nw + wid; s < m; s += gridDim.x * nw) {
-    for (int i = lane; i < k; i += 32) y[i] = beta[(int64_t)i * m + s];
-    __syncwarp();
-    for (int j = 0; j < k; ++j) {                 // L y = b
-      const double yj = y[j] * invd[j];
-      __syncwarp();
-      if (lane == 0) y[j] = yj;
-      for (int i = j + 1 + lane; i < k; i += 32) y[i] -= M[i * ld + j] * yj;
-      __syncwarp();
-    }
-    for (int j = k - 1; j >= 0; --j) {            // L^T x = y
-      const double xj = y[j] * invd[j];
-      __syncwarp();
-      if (lane == 0) y[j] = xj;
-      for (int i = lane; i < j; i += 32) y[i] -= M[j * ld + i] * xj;
-      __syncwarp();
-    }
-    for (int i = lane; i < k; i += 32) {
-      A64[(int64_t)i * m + s] = y[i];
-      A32[(int64_t)i * m + s] = (float)y[i];
-    }
-    __syncwarp();
-  }
-}
 
 __device__ __forceinline__ int packed_off(int i, int k) { return i * k - (i * (i - 1)) / 2; }
 __device__ __forceinline__ float packed_get(const float* P, int i, int j, int k) {

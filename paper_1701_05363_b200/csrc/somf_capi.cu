@@ -36,7 +36,6 @@
 #include "bcd_shard.cuh"
 #include "bbar_tc.cuh"
 #include "contract_tc.cuh"
-#include "codes_mp.cuh"
 #include "cd_as.cuh"
 
 using namespace somf;
@@ -108,6 +107,7 @@ struct somf_ctx {
   int* cnt_next = nullptr;
   unsigned* ct_bar = nullptr;   // fused contract reduction barrier [arrivals, exits]
   int ct_launches = 2;          // kernels the last launch_contract issued
+  int kern[5] = {};             // kernel variants of the last step: contract, codes, bbar, bcd, bbar complement
   int64_t* q_next = nullptr;
   int64_t* t_next = nullptr;
   double* w_next = nullptr;
@@ -154,7 +154,8 @@ struct somf_ctx {
   int nt_cap_rows = 0, nt_kpt = 0, nt_threads = 0, nt_ct_in_w = 0, nt_part_in_cpi = 0;
   size_t nt_smem = 0;
   double* lam_ws = nullptr;
-  double* nt_acc = nullptr;
+  unsigned long long* nt_acc = nullptr;
+  int nt_ncopy = 8;
   long long* bcd_prof = nullptr;   // SM cycles per BCD phase (somf_bcd_phase_cycles)
   // row sharding (somf_set_reducer): the caller's allreduce over the ranks
   somf_reduce_fn reducer = nullptr;
@@ -162,9 +163,9 @@ struct somf_ctx {
   ShState sh{};
   bool sh_alloc = false;
   int* sh_conv_host = nullptr;     // pinned
-  double* oc_acc = nullptr;
+  unsigned long long* oc_acc = nullptr;
   unsigned* oc_accmin = nullptr;
-  double* oc_rho = nullptr;
+  unsigned long long* oc_rho = nullptr;
   unsigned* oc_bar = nullptr;
   // evaluation scratch (objective / transform)
   int64_t eval_cap = 0;
@@ -215,18 +216,28 @@ static void set_err(somf_ctx* h, const char* fmt, ...) {
 #define CKL()  CK(cudaGetLastError())
 
 // Device-side flags: err_dev (numerical) and bar[2] (grid-barrier watchdog).
+// A flag is reported once, then cleared (the call that reports it fails; the
+// handle's state after a failed step is whatever the kernels left, so callers
+// restore a checkpoint with somf_set_state).
 static somf_status check_flags(somf_ctx* h) {
   int e = 0;
   unsigned b = 0;
+  CK(cudaStreamSynchronize(h->st));
   CK(cudaMemcpy(&e, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
   unsigned b2 = 0;
   CK(cudaMemcpy(&b, h->bar + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
   if (h->oc_bar) CK(cudaMemcpy(&b2, h->oc_bar + 2, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  if (!(b || b2 || e)) return SOMF_OK;
+  CK(cudaMemset(h->err_dev, 0, sizeof(int)));
+  CK(cudaMemset(h->bar + 2, 0, sizeof(unsigned)));
+  if (h->oc_bar) CK(cudaMemset(h->oc_bar + 2, 0, sizeof(unsigned)));
   if (b || b2) { set_err(h, "grid barrier watchdog fired in the BCD kernel (results invalid)"); return SOMF_E_CUDA; }
   if (e == 2) { set_err(h, "more masked rows than the on-chip BCD capacity (q > mean + 10 sigma)"); return SOMF_E_CUDA; }
   if (e == 3 || e == 4) { set_err(h, "projection threshold search hit its round cap"); return SOMF_E_CUDA; }
-  if (e) { set_err(h, "device numerical error flag %d (non-SPD system in the code solve)", e); return SOMF_E_NONFINITE; }
-  return SOMF_OK;
+  if (e == 6) { set_err(h, "a BCD threshold sum left the fixed-point range [0, 2^48)"); return SOMF_E_NONFINITE; }
+  if (e == 5) { set_err(h, "grid barrier watchdog fired in the contraction kernel (results invalid)"); return SOMF_E_CUDA; }
+  set_err(h, "device numerical error flag %d (non-SPD system in the code solve)", e);
+  return SOMF_E_NONFINITE;
 }
 
 static somf_status post_call(somf_ctx* h) {
@@ -310,9 +321,9 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
                            const float* X, int64_t ldx, bool* folded = nullptr, bool all_rows = false) {
   if (folded) *folded = false;
   const int k = h->cfg.k, eta = h->cfg.eta;
+  const int sel = h->cfg.bbar_kernel;      // 0 auto, 1 tc, 2 slice, 3 tiled (4 generic: the caller)
   if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15)) return false;
-  static const bool tc_off = std::getenv("SOMF_BBAR_TC") && std::atoi(std::getenv("SOMF_BBAR_TC")) == 0;
-  if ((gather || all_rows) && !tc_off && k <= 256) {
+  if ((gather || all_rows) && (sel == 0 || sel == 1) && k <= 256) {
     // tensor cores (bbar_tc.cuh): bf16x3 tcgen05 GEMM per 128 masked rows
     BtArgs a{};
     a.np = (k + 15) & ~15;
@@ -354,6 +365,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
         if (folded) *folded = false;
         return false;
       }
+      h->kern[2] = 1;
       return true;
     }
     cudaGetLastError();
@@ -362,7 +374,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
   int kc = (k + 31) / 32;
   if (kc > 4) kc = 8;
   const int64_t per = ceil_div(std::max<int64_t>(q_est, 1), h->nsm);
-  if (gather && kc <= 4) {
+  if (gather && kc <= 4 && (sel == 0 || sel == 2)) {
     // v3: whole slice in shared memory (rows of one segment per warp: RT <= 16)
     const int rt = per <= 32 ? 4 : per <= 64 ? 8 : 16;
     const int64_t seg = 8 * rt;
@@ -381,11 +393,13 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
         }
         fn<<<h->nsm, kBbThreads, smem, h->st>>>(h->idx, q_dev, X, ldx, eta, h->AT32, h->kp, k, h->Bbar, h->w_dev,
                                                 (int)seg, cf);
+        h->kern[2] = 2;
         return true;
       }
       cudaGetLastError();
     }
   }
+  if (sel != 0 && sel != 3) return false;
   const BbVariant* v = nullptr;
   for (const BbVariant& bv : kBbVariants) {
     if (bv.kc != kc) continue;
@@ -401,6 +415,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
   }
   fn<<<h->nsm, kBbThreads, smem, h->st>>>(gather ? h->idx : nullptr, q_dev, X, ldx, eta, h->A32, k, h->Bbar,
                                           h->kp, h->w_dev);
+  h->kern[2] = 3;
   return true;
 }
 
@@ -424,14 +439,14 @@ static const Ct3Variant kCt3Variants[] = {CT3(2, 2), CT3(2, 4), CT3(2, 6), CT3(2
 #undef CT3
 
 // [beta | G] over rows given by idx (or all rows), scaled by r.
+// sel: 0 auto, 1 tcgen05, 2 FFMA whole-slice, 3 FFMA tiled, 4 generic (somf_config.contract_kernel)
 static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, const int64_t* q_dev,
                                    int64_t q_est, const float* X, int64_t ldx, int m, double r,
-                                   double* beta, double* G) {
+                                   double* beta, double* G, int sel = 0) {
   const int k = h->cfg.k;
   const int nc = m + k;
   h->ct_launches = 2;
-  static const bool tc_off = std::getenv("SOMF_CT_TC") && std::atoi(std::getenv("SOMF_CT_TC")) == 0;
-  if (gather && !tc_off && k <= kTcM) {
+  if (gather && (sel == 0 || sel == 1) && k <= kTcM) {
     // tensor cores (contract_tc.cuh): bf16x3 tcgen05 GEMMs + fused split-K reduction
     CtTcArgs a{};
     a.ep = (m + 15) & ~15;
@@ -455,18 +470,23 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
         a.eta = m;
         a.xcompact = xcompact;
         a.partial = h->partial;
-        a.fz = CtFuse{h->ct_bar, r, beta, G};
+        a.fz = CtFuse{h->ct_bar, r, beta, G, h->err_dev};
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel((const void*)k_contract_tc, dim3(h->nsm), dim3(kCtThreads), args, smem,
                                        h->st));
         h->ct_launches = 1;
+        h->kern[0] = 1;
         return SOMF_OK;
       }
     }
     cudaGetLastError();
   }
   const bool fast = (m % 4 == 0) && (ldx % 4 == 0) && (((uintptr_t)X & 15) == 0);
-  if (fast && gather) {
+  if (sel == 1) {
+    set_err(h, "contract_kernel = tcgen05 does not apply (k <= 128, eta + k <= 512, eta %% 4 == 0 required)");
+    return SOMF_E_UNSUPPORTED;
+  }
+  if (fast && gather && (sel == 0 || sel == 2)) {
     const Ct3Variant* v3 = nullptr;
     for (const Ct3Variant& cv : kCt3Variants)
       if (8 * cv.mt >= k && 32 * cv.nt >= nc && (!v3 || cv.mt * cv.nt < v3->mt * v3->nt)) v3 = &cv;
@@ -481,12 +501,11 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
       Ct3Fn fn = v3->fn[xcompact ? 0 : 1];
       CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       int occ = 0;
-      static const bool fuse_off = std::getenv("SOMF_CT_FUSE") && std::atoi(std::getenv("SOMF_CT_FUSE")) == 0;
-      if (!fuse_off &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kCtThreads, smem) == cudaSuccess &&
+      h->kern[0] = 2;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kCtThreads, smem) == cudaSuccess &&
           occ >= 1) {
         // split-K reduction fused behind one grid barrier (cooperative launch)
-        CtFuse fz{h->ct_bar, r, beta, G};
+        CtFuse fz{h->ct_bar, r, beta, G, h->err_dev};
         const int32_t* idxp = h->idx;
         float* Dp = h->D;
         int kp = h->kp, kk = k, mm = m, sg = seg;
@@ -507,7 +526,12 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
       return SOMF_OK;
     }
   }
-  if (fast) {
+  if (sel == 2) {
+    set_err(h, "contract_kernel = slice does not apply (eta %% 4 == 0, aligned rows, >= 32 rows per SM slice)");
+    return SOMF_E_UNSUPPORTED;
+  }
+  if (fast && (sel == 0 || sel == 3)) {
+    h->kern[0] = 3;
     // the fewest tiles (each gathered row is staged once per tile), then the
     // least padding; register tile MT x NT <= 96 accumulators
     const CtVariant* v = nullptr;
@@ -539,6 +563,11 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
     CKL();
     return SOMF_OK;
   }
+  if (sel == 3) {
+    set_err(h, "contract_kernel = tiled does not apply (eta %% 4 == 0 and aligned rows required)");
+    return SOMF_E_UNSUPPORTED;
+  }
+  h->kern[0] = 4;
   const int ta = (int)ceil_div(k, TM), tc = (int)ceil_div(nc, TN);
   const int ns = split_count(h, ta * tc, q_est);
   somf_status s = ensure_partial(h, (size_t)ns * k * nc);
@@ -559,14 +588,21 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
   return SOMF_OK;
 }
 
+// sel: 0 auto, 1 ridge Cholesky, 2 CD with support jumps, 3 plain CD (somf_config.codes_kernel)
 static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta, int m, double tol,
                                 double* A64, float* A32, bool want_cpart = false) {
   const somf_config& c = h->cfg;
   const int k = c.k;
+  const int sel = c.codes_kernel;
   const int nw = kSolveThreads / 32;
   const int grid = (int)std::max<int64_t>(1, ceil_div(m, nw));
   h->cpart_n = 0;
-  if (c.nu == 1.0 && !c.pos_code && k <= kRcMaxK) {
+  const bool ridge_ok = c.nu == 1.0 && !c.pos_code && k <= kRcMaxK;
+  if (sel == 1 && !ridge_ok) {
+    set_err(h, "codes_kernel = ridge requires nu = 1, no positivity and k <= %d", kRcMaxK);
+    return SOMF_E_UNSUPPORTED;
+  }
+  if (ridge_ok && (sel == 0 || sel == 1)) {
     // ridge closed form (v2): every CTA factorises, 8 right-hand sides per CTA
     const int k4 = (k + kRcSB - 1) & ~(kRcSB - 1);
     const size_t smem = ((size_t)((k4 + 31) / 32 <= kRcInvKPL ? 2 : 1) * k4 * (k4 + 1) + (size_t)8 * k4) *
@@ -578,50 +614,34 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     }
     double* cp = want_cpart ? h->cpart : nullptr;
     const void* fn = nullptr;
-    size_t sm = smem;
-    // mixed precision (codes_mp.cuh: fp32 factor + substitutions, one fp64
-    // refinement) is opt-in, SOMF_RIDGE_MP=1: measured at cfgC it factors 25 %
-    // faster but its two substitution passes make the kernel slower (51.5 vs
-    // 49.4 us per step); the chain is latency-bound, not precision-bound
-    static const bool mp_on = std::getenv("SOMF_RIDGE_MP") && std::atoi(std::getenv("SOMF_RIDGE_MP")) == 1;
-    if (mp_on) {
-      sm = (size_t)8 * k4 * sizeof(double) + (size_t)k * (k + 1) * sizeof(double) +
-           (size_t)k4 * (k4 + 1) * sizeof(float);
-      static const int pw8 = std::getenv("SOMF_RIDGE_PW") && std::atoi(std::getenv("SOMF_RIDGE_PW")) == 8;
-#define RMP(N) (pw8 ? (const void*)k_ridge_mp<N, 8> : (const void*)k_ridge_mp<N, 4>)
-      switch ((k4 + 31) / 32) {
-        case 1: fn = RMP(1); break;
-        case 2: fn = RMP(2); break;
-        case 3: fn = RMP(3); break;
-        case 4: fn = RMP(4); break;
-        default: fn = RMP(5); break;
-      }
-#undef RMP
-    } else {
-      switch ((k4 + 31) / 32) {
-        case 1: fn = (const void*)k_ridge_codes<1>; break;
-        case 2: fn = (const void*)k_ridge_codes<2>; break;
-        case 3: fn = (const void*)k_ridge_codes<3>; break;
-        case 4: fn = (const void*)k_ridge_codes<4>; break;
-        default: fn = (const void*)k_ridge_codes<5>; break;
-      }
+    switch ((k4 + 31) / 32) {
+      case 1: fn = (const void*)k_ridge_codes<1>; break;
+      case 2: fn = (const void*)k_ridge_codes<2>; break;
+      case 3: fn = (const void*)k_ridge_codes<3>; break;
+      case 4: fn = (const void*)k_ridge_codes<4>; break;
+      default: fn = (const void*)k_ridge_codes<5>; break;
     }
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     double lam = c.lambda;
     long long* rprof = h->prof_on ? h->bcd_prof + 72 : nullptr;    // slots 72..75 (ridge phases)
     float* at = want_cpart ? h->AT32 : nullptr;
     int ldt = h->kp;
     void* args[] = {(void*)&G, (void*)&beta, (void*)&k, (void*)&m, (void*)&lam, (void*)&A64, (void*)&A32,
                     (void*)&at, (void*)&ldt, (void*)&cp, (void*)&h->err_dev, (void*)&rprof};
-    CK(cudaLaunchKernel(fn, dim3(g), dim3(kRcThreads), args, sm, h->st));
+    CK(cudaLaunchKernel(fn, dim3(g), dim3(kRcThreads), args, smem, h->st));
+    h->kern[1] = 1;
     return SOMF_OK;
   }
   const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
   const size_t smem = (size_t)k * (k + 1) / 2 * sizeof(float);
   const int kpl = (int)ceil_div(k, 32);
-  static const bool as_off = std::getenv("SOMF_CD_AS") && std::atoi(std::getenv("SOMF_CD_AS")) == 0;
   const size_t smem_as = (size_t)(kAsThreads / 32) * cd_as_warp_bytes() + smem;
-  if (!as_off && k >= 32 && smem_as <= 220 * 1024) {
+  const bool as_ok = k >= 32 && smem_as <= 220 * 1024;
+  if (sel == 2 && !as_ok) {
+    set_err(h, "codes_kernel = cd_jump requires k >= 32");
+    return SOMF_E_UNSUPPORTED;
+  }
+  if (as_ok && (sel == 0 || sel == 2)) {
     // CD with exact support jumps (cd_as.cuh), 4 columns per CTA
     const int gas = (int)ceil_div(m, kAsThreads / 32);
 #define LAUNCH_AS(N)                                                                                  \
@@ -638,6 +658,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     }
 #undef LAUNCH_AS
     CKL();
+    h->kern[1] = 2;
     return SOMF_OK;
   }
 #define LAUNCH_CD(N)                                                                      \
@@ -654,6 +675,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
   }
 #undef LAUNCH_CD
   CKL();
+  h->kern[1] = 3;
   return SOMF_OK;
 }
 
@@ -695,26 +717,18 @@ static const NtVariant kNtVariants[] = {{16, somf_nt_kernel_16}, {32, somf_nt_ke
                                         {64, somf_nt_kernel_64}, {72, somf_nt_kernel_72}, {80, somf_nt_kernel_80},
                                         {96, somf_nt_kernel_96}, {128, somf_nt_kernel_128}};
 
-// threads per group of M = 2 masked rows in the simultaneous-threshold kernel:
-// 4 (default), SOMF_NT_T=2 selects pairs (diagnostics / tuning)
-static int nt_threads_per_row() {
-  const char* e = std::getenv("SOMF_NT_T");
-  return (e && std::atoi(e) == 2) ? 2 : 4;
-}
-
 static void choose_newton(somf_ctx* h) {
   const int k = h->cfg.k;
   const int cap = (int)ceil_div(h->q_cap, h->nsm);
-  const int T = nt_threads_per_row();
-  const char* em = std::getenv("SOMF_NT_M");
-  const int M = (em && std::atoi(em) == 1) ? 1 : 2;
+  // groups of T = 4 threads own M = 2 masked rows (8 threads at KPT = 128)
+  const int T = 4, M = 2;
   const int gen = h->cfg.mu > 0.0 || h->cfg.pos_dict;
-  const int max_thr = M == 1 ? 640 : NtCfg<4, 2>::kThreads;
+  const int max_thr = NtCfg<4, 2>::kThreads;
   const int64_t groups = ceil_div(cap, M);
   for (const NtVariant& v : kNtVariants) {
     if (v.kpt < k) continue;
     // KPT = 128: 8 threads per group keep the residual at 2 x 16 registers
-    const int Tv = (v.kpt > 96 && M == 2) ? 8 : T;
+    const int Tv = v.kpt > 96 ? 8 : T;
     if (Tv * groups > max_thr) return;
     // >= k threads: the per-atom statistics and threshold updates run one thread per atom
     const int nthr = (int)std::max<int64_t>(ceil_div(std::max(64, k), 32) * 32, ceil_div((int64_t)Tv * groups, 32) * 32);
@@ -752,7 +766,7 @@ static void choose_newton(somf_ctx* h) {
     h->nt_threads = nthr;
     h->nt_ct_in_w = ct_in_w;
     h->nt_mbits_off = (int)mb_off;
-    if (const char* et = std::getenv("SOMF_NT_TOL")) h->nt_lam_tol = std::atof(et);
+    if (h->cfg.bcd_lam_tol > 0.0) h->nt_lam_tol = h->cfg.bcd_lam_tol;
     h->nt_part_in_cpi = part_in_cpi;
     return;
   }
@@ -922,11 +936,11 @@ static cudaError_t init_accmm(unsigned* mm, int n) {
   k_init_accmm<<<(n + 255) / 256, 256>>>(mm, n);
   return cudaGetLastError();
 }
-__global__ void k_init_nt_rec(double* rec, int n) {
+__global__ void k_init_nt_rec(unsigned long long* rec, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) nt_rec_reset(rec + (size_t)i * kNtRec);
 }
-static cudaError_t init_nt_rec(double* rec, int n) {
+static cudaError_t init_nt_rec(unsigned long long* rec, int n) {
   k_init_nt_rec<<<(n + 255) / 256, 256>>>(rec, n);
   return cudaGetLastError();
 }
@@ -1020,6 +1034,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->tile_counts, (size_t)h->ntiles));
   A(dalloc(&h->perm, (size_t)k));
   A(dalloc(&h->cnt_next, (size_t)h->nsm));
+  A(cudaMemset(h->cnt_next, 0, (size_t)h->nsm * sizeof(int)));
   A(dalloc(&h->ct_bar, 2));
   A(cudaMemset(h->ct_bar, 0, 2 * sizeof(unsigned)));
   // [beta | G] contiguous: one allreduce when row-sharded
@@ -1047,13 +1062,14 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
     h->q_cap = c.r == 1.0 ? rows : std::min<int64_t>(rows, (int64_t)std::ceil(mean + 10.0 * sd) + 32);
   }
   A(dalloc(&h->theta_ws, (size_t)k));
-  A(dalloc(&h->oc_acc, (size_t)kRing * kNC * 3));
+  A(dalloc(&h->oc_acc, (size_t)kRing * kNC * 5));
   A(dalloc(&h->oc_accmin, (size_t)kRing * kNC));
-  A(dalloc(&h->oc_rho, (size_t)2 * k));
+  A(dalloc(&h->oc_rho, (size_t)4 * k));
   A(dalloc(&h->oc_bar, 4));
   A(dalloc(&h->lam_ws, (size_t)k));
   A(dalloc(&h->bcd_prof, 80));
-  A(dalloc(&h->nt_acc, (size_t)(kNtRing + 1) * k * kNtRec));
+  h->nt_ncopy = c.bcd_copies > 0 ? std::min(c.bcd_copies, kNtMaxCopies) : 8;
+  A(dalloc(&h->nt_acc, (size_t)(kNtRing + 1) * h->nt_ncopy * k * kNtRec));
   if (c.bcd_kernel == 0 || c.bcd_kernel == 3) choose_newton(h);
   if (c.bcd_kernel == 0 ? !h->nt_fn : c.bcd_kernel == 2) choose_onchip(h);
   if ((c.bcd_kernel == 2 && !h->oc_fn) || (c.bcd_kernel == 3 && !h->nt_fn)) {
@@ -1063,14 +1079,14 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
 #undef A
   if (cudaMemset(h->bar, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
       cudaMemset(h->oc_bar, 0, 4 * sizeof(unsigned)) != cudaSuccess ||
-      cudaMemset(h->oc_acc, 0, (size_t)kRing * kNC * 3 * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->oc_acc, 0, (size_t)kRing * kNC * 5 * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->oc_accmin, 0xff, (size_t)kRing * kNC * sizeof(unsigned)) != cudaSuccess ||
-      cudaMemset(h->oc_rho, 0, (size_t)2 * k * sizeof(double)) != cudaSuccess ||
+      cudaMemset(h->oc_rho, 0, (size_t)4 * k * sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(h->theta_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->lam_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->AT32, 0, (size_t)c.eta * ((k + 3) & ~3) * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->bcd_prof, 0, 80 * sizeof(long long)) != cudaSuccess ||
-      init_nt_rec(h->nt_acc, (kNtRing + 1) * k) != cudaSuccess ||
+      init_nt_rec(h->nt_acc, (kNtRing + 1) * h->nt_ncopy * k) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->C64, 0, (size_t)k * k * sizeof(double)) != cudaSuccess ||
@@ -1237,12 +1253,22 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_CONTRACT);                                      // Eq. (a)
-    if (somf_status s = launch_contract(h, true, compact, h->q_dev, q_est, Xd, ld, eta, c.r, h->beta64, h->G64))
+    if (somf_status s = launch_contract(h, true, compact, h->q_dev, q_est, Xd, ld, eta, c.r, h->beta64, h->G64,
+                                        c.contract_kernel))
       return s;
     if (somf_status s = reduce(h, h->beta64, (int64_t)k * eta + (int64_t)k * k, SOMF_DT_F64, SOMF_OP_SUM))
       return s;
     h->launches[SOMF_PH_CONTRACT] += h->ct_launches;
   }
+  // mode F: the all-rows B-bar kernel reads its row count before
+  // griddepcontrol.wait, so it is written before the code solver (its primary)
+  if (c.b_mode == SOMF_B_FULL) {
+    k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
+    CKL();
+    h->launches[SOMF_PH_MASK] += 1;
+  }
+  h->kern[2] = 4;
+  h->kern[4] = 0;
   {
     PhaseScope ps(h, SOMF_PH_CODES);                                         // Eq. somf_alpha
     if (somf_status s = launch_codes(h, h->G64, h->beta64, eta, c.cd_tol, h->A64, h->A32, true)) return s;
@@ -1255,9 +1281,9 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     if (c.b_mode == SOMF_B_FULL) {
       // mode F (P:602 + P:612): every row gets the same update.  On the tensor
       // cores in one launch over all rows when the bf16x3 kernel applies ...
-      k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
-      if (launch_bbar_v2(h, false, false, h->qfull_dev, h->rows, Xd, ld, &cbar_folded, true)) {
-        h->launches[SOMF_PH_BBAR] += 2;
+      const bool all_tc = c.bbar_kernel == 0 || c.bbar_kernel == 1;
+      if (all_tc && launch_bbar_v2(h, false, false, h->qfull_dev, h->rows, Xd, ld, &cbar_folded, true)) {
+        h->launches[SOMF_PH_BBAR] += 1;
       } else {
         // ... else the rows in M_t first (the BCD reads them) and the rows
         // outside M_t on the side stream beside the BCD (k_bbar_comp)
@@ -1268,7 +1294,9 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
           k_bbar_update<true, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
               h->idx, h->q_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
           h->launches[SOMF_PH_BBAR] += 1;
+          h->kern[2] = 4;
         }
+        h->kern[4] = 1;
         CK(cudaEventRecord(h->ev_codes, h->st));
         CK(cudaStreamWaitEvent(h->st2, h->ev_codes, 0));
         const int grid_c = (int)std::min<int64_t>(ceil_div(h->rows, TM), 2 * h->nsm);
@@ -1291,8 +1319,13 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
         k_bbar_update<true, false><<<dim3(grid_r, grid_a), kGemmThreads, 0, h->st>>>(
             h->idx, h->q_dev, Xd, ld, eta, h->A32, k, h->Bbar, h->kp, h->w_dev);
       h->launches[SOMF_PH_BBAR] += 1;
+      h->kern[2] = 4;
     }
     CKL();
+    if (c.bbar_kernel != 0 && h->kern[2] != c.bbar_kernel) {
+      set_err(h, "bbar_kernel %d does not apply to this shape / input (ran variant %d)", c.bbar_kernel, h->kern[2]);
+      return SOMF_E_UNSUPPORTED;
+    }
   }
   if (!cbar_folded) {
     PhaseScope ps(h, SOMF_PH_CBAR);                                          // Eq. somf_partial
@@ -1307,6 +1340,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
+    h->kern[3] = h->reducer ? 4 : h->nt_fn ? 3 : h->oc_fn ? 2 : 1;
     if (h->reducer) {
       if (somf_status s = bcd_sharded(h)) return s;
     } else if (h->nt_fn) {
@@ -1347,6 +1381,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.cyclic = c.perm_cyclic;
       na.mbits_off = h->nt_mbits_off;
       na.rec = h->nt_acc;
+      na.ncopy = h->nt_ncopy;
       na.part_in_cpi = h->nt_part_in_cpi;
       na.bar = h->oc_bar;
       na.nred_out = h->nred_dev;
@@ -1591,6 +1626,9 @@ SOMF_EXPORT somf_status somf_set_reducer(somf_handle h, somf_reduce_fn fn, void*
   if (!h) return SOMF_E_ARG;
   h->reducer = fn;
   h->reducer_user = user;
+  // the next step redraws t+1 (mask and the device copy of pi) itself: the
+  // draw-ahead buffers of the single-GPU kernel are not used by the sharded path
+  h->mask_ready = h->begin_ready = h->ahead_ready = false;
   return SOMF_OK;
 }
 
@@ -1605,6 +1643,12 @@ SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {
 }
 
 SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->nt_fn ? 3 : h->oc_fn ? 2 : 1) : 0; }
+
+SOMF_EXPORT somf_status somf_last_kernels(somf_handle h, int32_t* out) {
+  if (!h || !out) return SOMF_E_ARG;
+  for (int i = 0; i < 5; ++i) out[i] = h->kern[i];
+  return SOMF_OK;
+}
 
 SOMF_EXPORT somf_status somf_profile_enable(somf_handle h, int32_t on) {
   if (!h) return SOMF_E_ARG;

@@ -51,6 +51,10 @@ def _stream_ptr(stream) -> C.c_void_p:
 
 
 B_MODES = {"masked": 0, "unbiased": 1, "full": 2}
+# kernel selection (somf_config *_kernel fields, include/somf.h)
+CONTRACT_KERNELS = {"auto": 0, "tc": 1, "slice": 2, "tiled": 3, "generic": 4}
+BBAR_KERNELS = {"auto": 0, "tc": 1, "slice": 2, "tiled": 3, "generic": 4}
+CODES_KERNELS = {"auto": 0, "ridge": 1, "cd_jump": 2, "cd": 3}
 
 
 class _CudaArray:
@@ -85,7 +89,9 @@ class Somf:
                  r: float = 1.0, u: float = 0.917, b_mode: str = "masked",
                  perm_cyclic: bool = False, cd_tol: float = 1e-7, cd_max_sweeps: int = 4000,
                  seed: int = 0, row_lo: int = 0, row_hi: int = 0, device: int = 0,
-                 stream=None, debug: bool = False, bcd_kernel: str = "auto"):
+                 stream=None, debug: bool = False, bcd_kernel: str = "auto",
+                 contract_kernel: str = "auto", bbar_kernel: str = "auto", codes_kernel: str = "auto",
+                 bcd_lam_tol: float = 0.0, bcd_copies: int = 0):
         L = lib()
         cfg = _lib.SomfConfig()
         L.somf_config_default(C.byref(cfg))
@@ -105,6 +111,11 @@ class Somf:
         cfg.stream = _stream_ptr(self.stream)
         cfg.debug = int(debug)
         cfg.bcd_kernel = {"auto": 0, "global": 1, "onchip": 2, "newton": 3}[bcd_kernel]
+        cfg.contract_kernel = CONTRACT_KERNELS[contract_kernel]
+        cfg.bbar_kernel = BBAR_KERNELS[bbar_kernel]
+        cfg.codes_kernel = CODES_KERNELS[codes_kernel]
+        cfg.bcd_lam_tol = bcd_lam_tol
+        cfg.bcd_copies = bcd_copies
         h = C.c_void_p()
         st = L.somf_create(C.byref(cfg), C.byref(h))
         if st != 0:
@@ -256,6 +267,17 @@ class Somf:
     @property
     def bcd_variant(self) -> str:
         return {1: "global", 2: "onchip", 3: "newton"}.get(lib().somf_bcd_variant(self._h), "?")
+
+    def last_kernels(self):
+        """Kernel variants of the last partial_fit (somf_last_kernels): names
+        as in CONTRACT_KERNELS / CODES_KERNELS / BBAR_KERNELS."""
+        v = np.zeros(5, np.int32)
+        _check(lib().somf_last_kernels(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
+        inv = lambda d, x: {i: n for n, i in d.items()}.get(int(x), "none")  # noqa: E731
+        return dict(contract=inv(CONTRACT_KERNELS, v[0]), codes=inv(CODES_KERNELS, v[1]),
+                    bbar=inv(BBAR_KERNELS, v[2]),
+                    bcd={1: "global", 2: "onchip", 3: "newton", 4: "sharded"}.get(int(v[3]), "none"),
+                    bbar_complement=bool(v[4]))
 
     def last_step_info(self):
         q, nred, w = C.c_int64(), C.c_int64(), C.c_double()

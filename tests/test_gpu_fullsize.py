@@ -1,0 +1,377 @@
+"""GPU (CUDA, through the C ABI) vs float64 oracle at the BENCHMARKED sizes,
+every kernel variant forced, support match, long runs -- needs a B200.
+
+Bars (BASELINE.json north_star):
+  * one step's alpha, Cbar, Bbar, D: <= 1e-4 relative Frobenius error;
+  * the support of sparse D (l1 ball) / alpha (lasso) matches the oracle's
+    except entries within 1e-6 of the threshold (reading R22, DESIGN.md §2:
+    an entry is exempt when the nonzero side is <= 1e-6 in magnitude: the
+    projection / soft threshold maps |v| - theta <= 1e-6 to such values);
+  * objective after 100 iterations: <= 1e-3 relative.
+One-step cases start from a mid-trajectory-like state built from the seeded
+generators (data columns, random codes) and loaded into BOTH sides: no input
+and no expected value comes from the CUDA path.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import synth  # noqa: E402
+from oracle import streams as ostreams  # noqa: E402
+from oracle.somf import SomfOracle, OracleConfig  # noqa: E402
+
+TOL_STEP = 1e-4
+TOL_OBJ = 1e-3
+SUPPORT_TOL = 1e-6
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def f32(a):
+    return np.asarray(a, np.float32).astype(np.float64)
+
+
+def cuda(a):
+    return torch.tensor(np.asarray(a, np.float32), device="cuda")
+
+
+def support_mismatches(got, ref, tol=SUPPORT_TOL):
+    """Entries whose zero / nonzero status differs, except where the nonzero
+    side is within `tol` of zero (i.e. its |v| was within tol of the threshold)."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    differ = (got != 0.0) != (ref != 0.0)
+    return int((differ & (np.maximum(np.abs(got), np.abs(ref)) > tol)).sum())
+
+
+@pytest.fixture(scope="module")
+def somf():
+    import paper_1701_05363_b200 as pkg
+    pkg.lib()
+    return pkg
+
+
+# ---------------------------------------------------------------------------
+# workloads at (or shaped like) BASELINE.json configs[1], [3], [4]
+# ---------------------------------------------------------------------------
+def _hyper_cols(n, seed):
+    return f32(synth.hyperspectral_patches(n, size=16, bands=224, n_end=256, seed=seed))
+
+
+def _nmf_cols(n, seed):
+    return f32(synth.nmf_matrix(p=16384, n=n, k_true=128, seed=seed))
+
+
+def _fmri256_cols(n, seed, p=200_000):
+    X, _, _ = synth.fmri_matrix(shape=(61, 73, 61), p=p, k=256, n_records=1, T=max(n, 1200), seed=seed)
+    return f32(X[:, :n])
+
+
+WORKLOADS = {
+    # name: (p, k, eta, method kwargs, generator, n_hist)
+    "cfgB_r12": (57344, 256, 256, dict(lam=0.1, nu=0.0, mu=1.0, r=12.0, u=0.917), _hyper_cols, 256),
+    "cfgD_r8": (16384, 128, 512, dict(lam=0.05, nu=1.0, pos_code=True, mu=1.0, pos_dict=True, r=8.0, u=0.917),
+                _nmf_cols, 512),
+    "cfgE_shape_r12": (200_000, 256, 512, dict(lam=0.05, nu=0.0, mu=0.5, r=12.0, u=0.917), _fmri256_cols, 256),
+}
+
+
+def _warm_state(name, seed=0):
+    """(oracle, X batch, state) with a mid-trajectory-like state: D0 = the
+    first k data columns projected onto C (the oracle's set_components), Bbar =
+    X_h A_h^T / n_h and Cbar = A_h A_h^T / n_h for n_h further data columns and
+    random sparse codes A_h (nonnegative for the NMF case), t = 50."""
+    p, k, eta, kw, gen, nh = WORKLOADS[name]
+    X = gen(k + nh + eta, seed)
+    rng = np.random.default_rng(seed + 7)
+    Ah = rng.standard_normal((k, nh)) * (rng.random((k, nh)) < 0.2)
+    if kw.get("pos_code"):
+        Ah = np.abs(Ah)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=seed + 3, **kw))
+    ora.set_components(X[:, :k])
+    Xh = X[:, k:k + nh]
+    state = dict(D=f32(ora.D), Bbar=f32(Xh @ Ah.T / nh), Cbar=Ah @ Ah.T / nh, n=ora.n.copy(), t=50)
+    ora.set_state(state["D"], state["Bbar"], state["Cbar"], state["n"], state["t"])
+    return ora, X[:, k + nh:k + nh + eta], state
+
+
+@pytest.mark.parametrize("name", list(WORKLOADS))
+def test_fullsize_one_step(somf, name):
+    """One step at the benchmarked size in the launch configuration bench.py
+    times (kernel selection auto), element-wise vs the oracle, plus the
+    support criterion on alpha (lasso) and D (l1 part of the ball)."""
+    p, k, eta, kw, _, _ = WORKLOADS[name]
+    ora, batch, st0 = _warm_state(name)
+    gpu = somf.Somf(p, k, eta, seed=3, **kw)
+    gpu.set_state(st0["D"], st0["Bbar"], st0["Cbar"], st0["n"], st0["t"])
+    out = ora.partial_fit(batch)
+    gpu.partial_fit(cuda(batch))
+    A = gpu.get_codes().cpu().numpy()
+    st = gpu.get_state()
+    info = gpu.last_step_info()
+    assert info["q"] == out["S"].size
+    S = out["S"]
+    errs = dict(alpha=rel(A, out["A"]), Cbar=rel(st["Cbar"], ora.Cbar), Bbar_S=rel(st["Bbar"][S], ora.Bbar[S]),
+                D_S=rel(st["D"][S], ora.D[S]))
+    assert all(v <= TOL_STEP for v in errs.values()), (errs, gpu.last_kernels())
+    np.testing.assert_allclose(st["n"], ora.n, rtol=0, atol=1e-5)
+    notS = np.setdiff1d(np.arange(p), S)
+    np.testing.assert_array_equal(st["D"][notS], st0["D"][notS].astype(np.float32))
+    if kw["nu"] < 1.0 or kw.get("pos_code"):
+        assert support_mismatches(A, out["A"]) == 0, "alpha support"
+    if kw["mu"] < 1.0 or kw.get("pos_dict"):
+        assert support_mismatches(st["D"][S], ora.D[S]) == 0, "D support"
+
+
+def test_fullsize_fmri_support_and_step(somf):
+    """cfgC at full size (BASELINE configs[2]): two steps from D0, then the
+    support of the l1-ball atoms D_S and the step's outputs vs the oracle."""
+    import bench
+    p, k, eta, r = 212445, 70, 200, 12.0
+    X, D0 = bench.fmri_inputs_cpu(n_cols=k + 2 * eta, seed=0)
+    kw = dict(lam=1e-3, nu=1.0, mu=0.0, r=r, u=0.917)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=0, **kw))
+    ora.set_components(D0)
+    gpu = somf.Somf(p, k, eta, seed=0, **kw)
+    gpu.set_components(cuda(D0))
+    for t in range(2):
+        batch = X[:, t * eta:(t + 1) * eta]
+        out = ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+        # continue from the GPU's float32 state so each step is its own pin
+        st = gpu.get_state()
+        S = out["S"]
+        assert rel(st["D"][S], ora.D[S]) <= TOL_STEP
+        assert support_mismatches(st["D"][S], ora.D[S]) == 0
+        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
+                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
+
+
+# ---------------------------------------------------------------------------
+# every kernel variant (the fallbacks the auto selection takes at other shapes)
+# ---------------------------------------------------------------------------
+VARIANT_CASES = {
+    # name: (p, k, eta, kwargs, data kind)
+    "ridge_l1": (3000, 24, 40, dict(lam=1e-3, nu=1.0, mu=0.0, r=12.0), "fmri"),
+    "lasso_l2": (1536, 40, 32, dict(lam=0.1, nu=0.0, mu=1.0, r=4.0), "hyper"),
+    "nmf": (2048, 48, 48, dict(lam=0.05, nu=1.0, pos_code=True, mu=1.0, pos_dict=True, r=8.0), "nmf"),
+    "k256_eta256": (2600, 256, 256, dict(lam=0.1, nu=0.0, mu=1.0, r=4.0), "hyper"),
+    "k128_eta512": (2048, 128, 512, dict(lam=0.05, nu=1.0, pos_code=True, mu=1.0, pos_dict=True, r=4.0), "nmf"),
+}
+
+
+def _vdata(kind, p, n, seed=0):
+    if kind == "fmri":
+        X, _, _ = synth.fmri_matrix(shape=(20, 20, 20), p=p, k=16, n_records=1, T=max(n, 64), seed=seed)
+        X = X[:, :n]
+    elif kind == "hyper":
+        X = synth.hyperspectral_patches(n, size=4, bands=-(-p // 16), n_end=16, seed=seed)[:p]
+    else:
+        X = synth.nmf_matrix(p=p, n=n, k_true=12, seed=seed)
+    return f32(X)
+
+
+def _vpair(somf, name, seed=3, **gkw):
+    p, k, eta, kw, kind = VARIANT_CASES[name]
+    X = _vdata(kind, p, k + 2 * eta)
+    rng = np.random.default_rng(5)
+    Ah = rng.standard_normal((k, eta)) * (rng.random((k, eta)) < 0.3)
+    if kw.get("pos_code"):
+        Ah = np.abs(Ah)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=seed, **kw))
+    ora.set_components(X[:, :k])
+    st0 = dict(D=f32(ora.D), Bbar=f32(X[:, k:k + eta] @ Ah.T / eta), Cbar=Ah @ Ah.T / eta, n=ora.n.copy(), t=20)
+    ora.set_state(st0["D"], st0["Bbar"], st0["Cbar"], st0["n"], st0["t"])
+    gpu = somf.Somf(p, k, eta, seed=seed, debug=True, **kw, **gkw)
+    gpu.set_state(st0["D"], st0["Bbar"], st0["Cbar"], st0["n"], st0["t"])
+    return ora, gpu, X[:, k + eta:k + 2 * eta], st0
+
+
+def _check_step(ora, gpu, batch, b_mode="masked"):
+    out = ora.partial_fit(batch)
+    gpu.partial_fit(cuda(batch))
+    A = gpu.get_codes().cpu().numpy()
+    st = gpu.get_state()
+    errs = dict(alpha=rel(A, out["A"]), Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar),
+                D=rel(st["D"], ora.D))
+    assert all(v <= TOL_STEP for v in errs.values()), errs
+    np.testing.assert_allclose(st["n"], ora.n, rtol=0, atol=1e-5)
+    return out, st
+
+
+def _forced_step(somf, ora, gpu, batch):
+    """One step with a forced kernel variant; skips when the variant does not
+    apply to the case's shape (the library refuses it: SOMF_E_UNSUPPORTED)."""
+    try:
+        return _check_step(ora, gpu, batch)
+    except somf.SomfError as e:
+        if "does not apply" in str(e) or "requires" in str(e):
+            pytest.skip(f"variant does not apply to this shape: {e}")
+        raise
+
+
+@pytest.mark.parametrize("variant", ["tc", "slice", "tiled", "generic"])
+@pytest.mark.parametrize("name", list(VARIANT_CASES))
+def test_contract_variants(somf, name, variant):
+    ora, gpu, batch, _ = _vpair(somf, name, contract_kernel=variant)
+    _forced_step(somf, ora, gpu, batch)
+    assert gpu.last_kernels()["contract"] == variant
+
+
+@pytest.mark.parametrize("variant", ["tc", "slice", "tiled", "generic"])
+@pytest.mark.parametrize("name", list(VARIANT_CASES))
+def test_bbar_variants(somf, name, variant):
+    ora, gpu, batch, _ = _vpair(somf, name, bbar_kernel=variant)
+    _forced_step(somf, ora, gpu, batch)
+    assert gpu.last_kernels()["bbar"] == variant
+
+
+@pytest.mark.parametrize("variant", ["ridge", "cd_jump", "cd"])
+@pytest.mark.parametrize("name", list(VARIANT_CASES))
+def test_codes_variants(somf, name, variant):
+    ora, gpu, batch, _ = _vpair(somf, name, codes_kernel=variant)
+    out, _ = _forced_step(somf, ora, gpu, batch)
+    assert gpu.last_kernels()["codes"] == variant
+    p, k, eta, kw, _ = VARIANT_CASES[name]
+    if kw["nu"] < 1.0 or kw.get("pos_code"):
+        assert support_mismatches(gpu.get_codes().cpu().numpy(), out["A"]) == 0
+
+
+@pytest.mark.parametrize("variant", ["slice", "tiled", "generic"])
+@pytest.mark.parametrize("name", ["ridge_l1", "nmf", "k256_eta256"])
+def test_full_mode_complement_stream(somf, name, variant):
+    """Mode F with a non-tensor-core B-bar kernel: the rows of M_t first, the
+    complement rows (k_bbar_comp) on the side stream beside Alg. 4."""
+    p, k, eta, kw, kind = VARIANT_CASES[name]
+    X = _vdata(kind, p, k + 3 * eta)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=3, b_mode="F", **kw))
+    ora.set_components(X[:, :k])
+    ora.partial_fit(X[:, k:k + eta])
+    ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
+    gpu = somf.Somf(p, k, eta, seed=3, debug=True, b_mode="full", bbar_kernel=variant, **kw)
+    gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
+    out, st = _forced_step(somf, ora, gpu, X[:, k + eta:k + 2 * eta])
+    kern = gpu.last_kernels()
+    assert kern["bbar_complement"] and kern["bbar"] == variant
+    notS = np.setdiff1d(np.arange(p), out["S"])
+    assert rel(st["Bbar"][notS], ora.Bbar[notS]) <= TOL_STEP
+
+
+def test_forced_variant_that_does_not_apply_fails_loudly(somf):
+    p, k, eta, kw, kind = VARIANT_CASES["k256_eta256"]
+    X = _vdata(kind, p, k + eta)
+    gpu = somf.Somf(p, k, eta, seed=3, contract_kernel="tc", **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    with pytest.raises(somf.SomfError):
+        gpu.partial_fit(cuda(X[:, k:k + eta]))
+
+
+# ---------------------------------------------------------------------------
+# determinism: fixed-point grid sums => bit-identical reruns, any copy count
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("bcd_kernel", ["newton", "onchip"])
+def test_bcd_bitwise_deterministic(somf, bcd_kernel):
+    p, k, eta, kw, kind = VARIANT_CASES["ridge_l1"]
+    X = _vdata(kind, p, k + 6 * eta)
+    runs = []
+    for copies in (1, 8, 16, 8):
+        gpu = somf.Somf(p, k, eta, seed=3, bcd_kernel=bcd_kernel, bcd_copies=copies, **kw)
+        gpu.set_components(cuda(X[:, :k]))
+        for t in range(5):
+            gpu.partial_fit(cuda(X[:, k + t * eta:k + (t + 1) * eta]))
+        runs.append(gpu.get_state())
+    for st in runs[1:]:
+        for key in ("D", "Bbar", "Cbar", "n"):
+            np.testing.assert_array_equal(st[key], runs[0][key])
+
+
+# ---------------------------------------------------------------------------
+# empty masks recurring inside a run (draw-ahead with q = 0)
+# ---------------------------------------------------------------------------
+def test_recurring_empty_masks(somf):
+    p, k, eta = 64, 4, 5
+    kw = dict(lam=0.1, nu=1.0, mu=0.0, r=32.0)
+    X = f32(synth.tiny_dictionary_learning(p=p, n=k + 40 * eta, seed=2)[0])
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=1, **kw))
+    ora.set_components(X[:, :k])
+    gpu = somf.Somf(p, k, eta, seed=1, debug=True, bcd_kernel="newton", **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    n_empty = 0
+    for t in range(40):
+        batch = X[:, k + t * eta:k + (t + 1) * eta]
+        out = ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+        info = gpu.last_step_info()
+        assert info["q"] == out["S"].size, t
+        n_empty += out["S"].size == 0
+        st = gpu.get_state()
+        assert rel(st["D"], ora.D) <= TOL_STEP and rel(st["Cbar"], ora.Cbar) <= TOL_STEP, t
+        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
+                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
+    assert n_empty >= 5
+    q, idx = gpu.next_mask()
+    assert np.array_equal(idx, ostreams.mask_rows(1, ora.t + 1, p, 32.0))
+
+
+# ---------------------------------------------------------------------------
+# trajectories: 100 iterations at full cfgC size; 1000 iterations (drift)
+# ---------------------------------------------------------------------------
+def test_trajectory_fullsize_fmri_100(somf):
+    import bench
+    p, k, eta, r = 212445, 70, 200, 12.0
+    iters, m_te = 100, 200
+    X, D0 = bench.fmri_inputs_cpu(n_cols=iters * eta + m_te, seed=1)
+    Xte = X[:, -m_te:]
+    kw = dict(lam=1e-3, nu=1.0, mu=0.0, r=r, u=0.917)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=0, **kw))
+    ora.set_components(D0)
+    gpu = somf.Somf(p, k, eta, seed=0, **kw)
+    gpu.set_components(cuda(D0))
+    for t in range(iters):
+        batch = np.ascontiguousarray(X[:, t * eta:(t + 1) * eta])
+        ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+    f_ref = ora.objective(Xte)
+    f_gpu = gpu.objective(cuda(Xte))
+    assert abs(f_gpu - f_ref) <= TOL_OBJ * abs(f_ref), (f_gpu, f_ref)
+    st = gpu.get_state()
+    # the persistent statistics after 100 steps, and the support of D
+    assert rel(st["Cbar"], ora.Cbar) <= TOL_OBJ
+    assert rel(st["Bbar"], ora.Bbar) <= TOL_OBJ
+    frac = support_mismatches(st["D"], ora.D) / st["D"].size
+    assert frac <= 1e-3, frac
+
+
+def test_trajectory_1000_steps_drift(somf):
+    """1000 iterations (w_t down to 1000^-0.917): Bbar (bf16x3 tensor-core
+    update) and Cbar must not drift from the float64 oracle."""
+    p, k, eta, r = 12000, 70, 200, 12.0
+    iters = 1000
+    X, _, _ = synth.fmri_matrix(shape=(30, 30, 30), p=p, k=40, n_records=1, T=1200, seed=4)
+    X = f32(X)
+    kw = dict(lam=1e-3, nu=1.0, mu=0.0, r=r, u=0.917)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=2, **kw))
+    ora.set_components(X[:, :k])
+    gpu = somf.Somf(p, k, eta, seed=2, **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    Xg = cuda(X)
+    cols = np.arange(k, X.shape[1])
+    for t in range(iters):
+        c0 = (t * eta) % (cols.size - eta)
+        sl = slice(k + c0, k + c0 + eta)
+        ora.partial_fit(X[:, sl])
+        gpu.partial_fit(Xg[:, sl].contiguous())
+    st = gpu.get_state()
+    errs = dict(Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar), D=rel(st["D"], ora.D))
+    assert all(v <= TOL_OBJ for v in errs.values()), errs
+    Xte = X[:, -200:]
+    f_ref, f_gpu = ora.objective(Xte), gpu.objective(cuda(Xte))
+    assert abs(f_gpu - f_ref) <= TOL_OBJ * abs(f_ref), (f_gpu, f_ref)
