@@ -400,7 +400,7 @@ def run_somf(args):
 
     def make(rr, burn_in, b_mode="masked"):
         m = somf_pkg.Somf(p, k, eta, lam=w["lam"], nu=w["nu"], mu=w["mu"], pos_code=w["pos_code"],
-                          row_lo=lo, row_hi=hi, b_mode=b_mode,
+                          row_lo=lo, row_hi=hi, b_mode=b_mode, bcd_copies=args.bcd_copies,
                           pos_dict=w["pos_dict"], r=rr, u=w["u"], seed=0, device=dev.index, stream=stream)
         if world > 1:
             m.set_reducer(somf_pkg.dist_reducer())      # NCCL allreduce at every exchange point
@@ -641,6 +641,8 @@ def main():
     ap.add_argument("--burn-in", type=int, default=60,
                     help="untimed SOMF iterations before warm-up (steady state, t > burn-in)")
     ap.add_argument("--r", type=float, default=WORKLOAD["r"])
+    ap.add_argument("--bcd-copies", type=int, default=0,
+                    help="copies of each per-atom BCD accumulator (performance knob; 0 = library default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

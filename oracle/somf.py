@@ -16,6 +16,21 @@ rows.  Statement order follows the paper:
     [mode F: also P_t^perp Bbar, P:612 ; mode U: reading R6]
     Alg. 4 on the rows S, atoms in permutation order
 
+Estimators of the code step (Table I), ``estimator``:
+  (a) masked    G = D^T M_t D, beta = D^T M_t x              Eq. (a)
+  (b) averaged  per-sample G^(i), beta^(i):                  Eq. (b)
+                c^(i) += 1, gamma = c^(i)^-v,                P:585-590, P:708-714
+                beta^(i) <- (1-gamma) beta^(i) + gamma D^T M_t x^(i)
+                G^(i)    <- (1-gamma) G^(i)    + gamma D^T M_t D
+  (c) exact Gram + averaged beta^(i): G = D_{t-1}^T D_{t-1},  Eq. (c)
+                maintained through Alg. 4's partial update:
+                G <- G - P_t D_old^T P_t D_old + P_t D_new^T P_t D_new
+with gamma_c = c^-v (v = 0.751 P:1361).  Readings R23-R25
+(DESIGN.md §2): Alg. 3's "beta^(i) <- (1-gamma) G^(i)_{t-1}" is read as
+beta^(i)_{t-1} (SURVEY ledger 17); the averages start at c = 1 where gamma = 1
+overwrites them; the ids of one mini-batch must be distinct (the mini-batch
+extension P:633-636 applies the per-sample rule once per sample).
+
 Readings: R1-R2 mask, R4 batch means, R5/R6 Bbar modes,
 R7 literal Eq. 2 norm, R9 radius, R10 dead atoms, R11 radius 0, R13 order.
 """
@@ -46,6 +61,9 @@ class OracleConfig:
     b_mode: str = "M"         # Bbar rows updated: M masked, F full, U unbiased
     perm_cyclic: bool = False
     seed: int = 0
+    estimator: str = "a"      # code-step estimator: a masked, b averaged, c exact Gram (Table I)
+    n_samples: int = 0        # n: sample ids in [0, n) (estimators b / c)
+    v: float = 0.751          # gamma_c = c^-v
 
 
 def surrogate_value(D, Bbar, Cbar) -> float:
@@ -88,6 +106,10 @@ class SomfOracle:
             raise ValueError("invalid mixing / weight parameter")
         if cfg.b_mode not in B_MODES:
             raise ValueError("b_mode must be one of M, F, U")
+        if cfg.estimator not in ("a", "b", "c"):
+            raise ValueError("estimator must be one of a, b, c")
+        if cfg.estimator != "a" and cfg.n_samples < 1:
+            raise ValueError("estimators b / c need n_samples >= 1")
         self.cfg = cfg
         p, k = cfg.p, cfg.k
         self.D = np.zeros((p, k))
@@ -96,6 +118,18 @@ class SomfOracle:
         self.n = np.ones(k)
         self.t = 0
         self.cd_tol = 1e-12
+        self._reset_estimator()
+
+    def _reset_estimator(self):
+        """Per-sample statistics of estimators (b) / (c): visit counts c^(i),
+        averaged beta^(i) (n x k), averaged G^(i) (n x k x k, (b) only) and the
+        exact Gram G = D^T D ((c) only)."""
+        c = self.cfg
+        n = c.n_samples if c.estimator != "a" else 0
+        self.count = np.zeros(n, dtype=np.int64)
+        self.beta_avg = np.zeros((n, c.k))
+        self.G_avg = np.zeros((n, c.k, c.k)) if c.estimator == "b" else None
+        self.G_exact = self.D.T @ self.D if c.estimator == "c" else None
 
     # -- state ---------------------------------------------------------------
     def set_components(self, D0):
@@ -110,6 +144,7 @@ class SomfOracle:
         self.Bbar = np.zeros_like(self.D)
         self.Cbar = np.zeros((c.k, c.k))
         self.t = 0
+        self._reset_estimator()
 
     def set_state(self, D, Bbar, Cbar, n, t):
         self.D = np.array(D, np.float64)
@@ -117,11 +152,14 @@ class SomfOracle:
         self.Cbar = np.array(Cbar, np.float64)
         self.n = np.array(n, np.float64)
         self.t = int(t)
+        self._reset_estimator()
 
     # -- one iteration of Alg. 3 -------------------------------------------------
-    def partial_fit(self, X):
-        """One SOMF iteration on the batch X (p x eta).  Returns the step's
-        intermediates (S, G, beta, A, perm, w) for parity tests."""
+    def partial_fit(self, X, ids=None):
+        """One SOMF iteration on the batch X (p x eta) whose columns are the
+        samples ``ids`` (estimators b / c).  Returns the step's intermediates
+        (S, G, beta, A, perm, w) for parity tests; for (b) G is per column
+        (eta x k x k)."""
         c = self.cfg
         X = np.asarray(X, np.float64)
         eta = X.shape[1]
@@ -133,7 +171,34 @@ class SomfOracle:
         XS = X[S]
         G = c.r * (DS.T @ DS)                                    # Eq. (a)
         beta = c.r * (DS.T @ XS)
-        A = solve_codes(G, beta, c.lam, c.nu, c.pos_code, tol=self.cd_tol)
+        if c.estimator == "a":
+            A = solve_codes(G, beta, c.lam, c.nu, c.pos_code, tol=self.cd_tol)
+        else:
+            ids = np.asarray(ids, dtype=np.int64)
+            if ids.shape != (eta,) or ids.min() < 0 or ids.max() >= c.n_samples:
+                raise ValueError("ids must hold eta sample ids in [0, n_samples)")
+            if np.unique(ids).size != eta:
+                raise ValueError("the ids of one mini-batch must be distinct (reading R25)")
+            beta_used = np.empty_like(beta)
+            G_used = np.empty((eta, c.k, c.k)) if c.estimator == "b" else None
+            for s_, i in enumerate(ids):
+                self.count[i] += 1
+                gamma = float(self.count[i]) ** (-c.v)
+                self.beta_avg[i] = (1.0 - gamma) * self.beta_avg[i] + gamma * beta[:, s_]
+                beta_used[:, s_] = self.beta_avg[i]
+                if c.estimator == "b":
+                    self.G_avg[i] = (1.0 - gamma) * self.G_avg[i] + gamma * G
+                    G_used[s_] = self.G_avg[i]
+            if c.estimator == "b":                               # Eq. (b): a Gram per column
+                A = np.empty_like(beta)
+                for s_ in range(eta):
+                    A[:, s_] = solve_codes(G_used[s_], beta_used[:, s_], c.lam, c.nu, c.pos_code,
+                                           tol=self.cd_tol)
+                G = G_used
+            else:                                                # Eq. (c): the exact Gram D_{t-1}^T D_{t-1}
+                G = self.G_exact.copy()
+                A = solve_codes(G, beta_used, c.lam, c.nu, c.pos_code, tol=self.cd_tol)
+            beta = beta_used
         self.Cbar = (1.0 - w) * self.Cbar + (w / eta) * (A @ A.T)  # Eq. somf_partial
         if c.b_mode == "M":
             self.Bbar[S] = (1.0 - w) * self.Bbar[S] + (w / eta) * (XS @ A.T)
@@ -145,7 +210,12 @@ class SomfOracle:
             self.Bbar *= (1.0 - w)
             self.Bbar[S] += (w * c.r / eta) * (XS @ A.T)
         perm = atom_permutation(c.seed, t, c.k, c.perm_cyclic)
+        DS_old = self.D[S].copy()
         self._partial_dictionary_update(S, perm)
+        if c.estimator == "c":
+            # the Gram of D_t from that of D_{t-1}: only the rows S changed
+            DS_new = self.D[S]
+            self.G_exact = self.G_exact - DS_old.T @ DS_old + DS_new.T @ DS_new
         return dict(S=S, G=G, beta=beta, A=A, perm=perm, w=w)
 
     def _partial_dictionary_update(self, S, perm):
