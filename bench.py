@@ -379,6 +379,9 @@ def run_somf(args):
     dev = torch.device("cuda", local % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
     if world > 1:
+        if args.dist_backend == "nccl" and world > torch.cuda.device_count():
+            raise SystemExit(f"--gpus {world} with NCCL needs {world} visible GPUs "
+                             f"({torch.cuda.device_count()} found); use --dist-backend gloo to share one")
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -630,6 +633,98 @@ def run_somf(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------
+# time-to-1 % sweeps (Table III; validation
+# protocol P:1322-1326): OMF (r = 1) vs SOMF r in {4, 12, 24}
+# ----------------------------------------------------------------------------
+def convergence_curve(model, X_all, ids_of, iters, eval_every, Xte, stream, use_ids=True):
+    """Runs `iters` steps of `model` on batches X_all[:, ids_of(t)] and returns
+    [(cumulative step time in s, iteration, test objective)] at every
+    `eval_every` steps (and at 0).  Only the partial_fit calls are timed (CUDA
+    events on the launching stream); gathers of the batch and the objective
+    evaluations are outside the timed region."""
+    import torch
+    curve = [(0.0, 0, model.objective(Xte))]
+    t_acc = 0.0
+    for t in range(iters):
+        ids = ids_of(t)
+        batch = X_all[:, ids].contiguous()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        if use_ids:
+            model.partial_fit_ids(batch, ids)
+        else:
+            model.partial_fit(batch)
+        b.record(stream)
+        b.synchronize()
+        t_acc += a.elapsed_time(b) * 1e-3
+        if (t + 1) % eval_every == 0 or t + 1 == iters:
+            curve.append((t_acc, t + 1, model.objective(Xte)))
+    return curve
+
+
+def time_to_within(curve, f_star, tol=0.01):
+    """First (time, iteration) with test objective <= (1 + tol) f_star, else None."""
+    for tm, it, f in curve:
+        if f <= (1.0 + tol) * f_star:
+            return tm, it
+    return None
+
+
+def run_sweeps(args):
+    """cfgC stand-in (fMRI-shaped, p = 212,445, k = 70, eta = 200, ridge
+    lambda = 1e-3, l1-ball atoms): a finite set of n columns cycled randomly
+    (per-epoch keyed permutations, reading R16, the same order for every r,
+    P:1354-1357), estimator (c) (the paper's choice on fMRI),
+    held-out objective on 1000 other columns against step time; time to reach
+    1 % of the best objective any run reached (Table III's criterion)."""
+    import torch
+    import paper_1701_05363_b200 as somf_pkg
+    somf_pkg.lib()
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    w = WORKLOAD
+    p, k, eta = w["p"], w["k"], w["eta"]
+    n, n_te = args.sweep_n, 1000
+    gen = FmriStreamGPU(n_batches=(n + n_te) // eta + 1, eta=eta, k=k, seed=5, device=dev)
+    X_all = gen._cols(k, k + n)                        # p x n (the data set)
+    Xte = gen._cols(k + n, k + n + n_te)               # held-out columns
+    D0 = gen._cols(0, k)
+    stream = torch.cuda.current_stream(dev)
+
+    def ids_of(t):
+        return somf_pkg.column_ids(11, n, t * eta, eta)
+
+    curves, step_ms = {}, {}
+    for rr in args.sweep_r:
+        m = somf_pkg.Somf(p, k, eta, lam=w["lam"], nu=w["nu"], mu=w["mu"], r=rr, u=w["u"], seed=0,
+                          estimator=args.sweep_estimator, n_samples=n, device=0, stream=stream)
+        m.set_components(D0)
+        iters = args.sweep_iters
+        cv = convergence_curve(m, X_all, ids_of, iters, args.sweep_eval, Xte, stream,
+                               use_ids=args.sweep_estimator != "a")
+        curves[f"r={int(rr)}"] = cv
+        step_ms[f"r={int(rr)}"] = 1e3 * cv[-1][0] / iters
+        del m
+    f_star = min(f for cv in curves.values() for _, _, f in cv)
+    out = {}
+    for name, cv in curves.items():
+        hit = time_to_within(cv, f_star, 0.01)
+        out[name] = {"ms_per_step": step_ms[name], "final_objective": cv[-1][2],
+                     "time_to_1pct_s": hit[0] if hit else None, "iters_to_1pct": hit[1] if hit else None,
+                     "curve": [[round(tm, 6), it, f] for tm, it, f in cv]}
+    base = out.get("r=1", {}).get("time_to_1pct_s")
+    for name, o in out.items():
+        o["speedup_vs_omf"] = (base / o["time_to_1pct_s"]) if (base and o["time_to_1pct_s"]) else None
+    line = {"metric": "time to 1% of the best test objective (OMF r=1 vs SOMF)", "unit": "s (device time of the steps)",
+            "workload": "cfgC-fmri", "p": p, "k": k, "eta": eta, "n_columns": n, "n_test": n_te,
+            "estimator": args.sweep_estimator, "f_star": f_star, "iters": args.sweep_iters,
+            "eval_every": args.sweep_eval, "data": "synthetic (fMRI-shaped stand-in, DESIGN.md §3)", "results": out}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -643,6 +738,13 @@ def main():
     ap.add_argument("--r", type=float, default=WORKLOAD["r"])
     ap.add_argument("--bcd-copies", type=int, default=0,
                     help="copies of each per-atom BCD accumulator (performance knob; 0 = library default)")
+    ap.add_argument("--sweeps", action="store_true",
+                    help="time-to-1%% convergence sweeps (OMF r=1 vs SOMF r=4/12/24) instead of the step benchmark")
+    ap.add_argument("--sweep-r", type=float, nargs="+", default=[1.0, 4.0, 12.0, 24.0])
+    ap.add_argument("--sweep-n", type=int, default=12000)
+    ap.add_argument("--sweep-iters", type=int, default=1200)
+    ap.add_argument("--sweep-eval", type=int, default=20)
+    ap.add_argument("--sweep-estimator", default="c", choices=["a", "b", "c"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -650,8 +752,20 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: start the N ranks ourselves (the driver uses
+        # torchrun; this keeps `python bench.py --gpus N` equivalent)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
+    elif args.sweeps:
+        run_sweeps(args)
     else:
         run_somf(args)
 

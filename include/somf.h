@@ -121,10 +121,19 @@ typedef struct somf_config {
                              performance knob only: the sums are fixed-point
                              integers, so results are bit-identical for any
                              value and any CTA arrival order                 */
+  /* Code-step estimator (Table I): 0 = (a) masked G and beta
+   * (Eq. a, the hot path), 1 = (b) per-sample averaged G^(i) and beta^(i)
+   * (Eq. b; n_samples x k x k float64 of device memory), 2 = (c) exact Gram
+   * D^T D maintained through Alg. 4's partial updates + averaged beta^(i)
+   * (Eq. c; n_samples x k float64).  (b) / (c) need somf_partial_fit_ids. */
+  int32_t estimator;
+  int64_t n_samples;      /* n: sample ids of the stream lie in [0, n)        */
+  double v;               /* gamma_c = c^-v of the per-sample averages,
+                             v in (0, 1] (0.751 in P:1361)        */
 } somf_config;
 
 /* Fills *cfg with defaults: u = 0.917, r = 1, nu = 1, mu = 0,
- * lambda = 0.1, b_mode = SOMF_B_MASKED, cd_tol = 1e-7, cd_max_sweeps = 4000,
+ * lambda = 0.1, b_mode = SOMF_B_MASKED, cd_tol = 1e-7, cd_max_sweeps = 4000, v = 0.751,
  * seed = 0, row range [0, p), device 0, stream NULL, debug 0.  p, k, eta are
  * left 0 and must be set. */
 void somf_config_default(somf_config* cfg);
@@ -161,6 +170,18 @@ somf_status somf_set_components(somf_handle h, const float* D0, int64_t ld);
  * first gathered into device memory (phase SOMF_PH_STAGE), each crossing the
  * host link once.  SOMF_E_STATE before somf_set_components / somf_set_state. */
 somf_status somf_partial_fit(somf_handle h, const float* X, int64_t ld);
+
+/* somf_partial_fit for estimators (b) / (c): ids (host or device, int64[eta])
+ * are the sample ids in [0, n_samples) of the batch's columns -- distinct
+ * within one batch (reading R25; a repeat or an out-of-range id makes the next
+ * synchronising call fail with SOMF_E_ARG).  Per column s, sample i = ids[s]:
+ * c^(i) += 1, gamma = c^(i)^-v, beta^(i) <- (1 - gamma) beta^(i) + gamma beta_s
+ * ((b): also G^(i)); codes from (G^(i), beta^(i)) ((b)) or
+ * (D^T D, beta^(i)) ((c)); (c) then updates D^T D by the rows Alg. 4 moved
+ * (P:754-756).  somf_set_components / somf_set_state reset every sample's
+ * statistics (and recompute D^T D).  Estimator (a) handles accept it too
+ * (ids ignored). */
+somf_status somf_partial_fit_ids(somf_handle h, const float* X, int64_t ld, const int64_t* ids);
 
 /* Draws the mask M_{t+1} of the NEXT iteration now, writes its size to
  * *q_out and, when idx_out is not NULL, its ascending local row indices
@@ -214,12 +235,15 @@ somf_status somf_last_step_info(somf_handle h, int64_t* q, int64_t* bcd_reductio
  * rounds (all k thresholds per grid reduction).  0 on a null handle. */
 int32_t somf_bcd_variant(somf_handle h);
 
-/* Kernel variants the last somf_partial_fit ran (host int32 out[5]):
+/* Kernel variants the last somf_partial_fit ran (host int32 out[7]):
  * out[0] contraction (1 tcgen05, 2 FFMA whole-slice, 3 FFMA tiled, 4 generic),
  * out[1] codes (1 ridge Cholesky, 2 CD with support jumps, 3 plain CD),
  * out[2] P_t Bbar (1 tcgen05, 2 FFMA whole-slice, 3 FFMA tiled, 4 generic),
  * out[3] Alg. 4 (as somf_bcd_variant; 4 = row-sharded rounds),
- * out[4] 1 when mode FULL ran the complement rows on the side stream.
+ * out[4] 1 when mode FULL ran the complement rows on the side stream,
+ * out[5], out[6] the simultaneous-threshold kernel's group shape: T threads
+ * own M masked rows (1 x 1 and 2 x 1: packed-FFMA2 recurrence; 4 x 2 and
+ * 8 x 2: shuffle recurrence), 0 for the other Alg. 4 kernels.
  * 0 before the first step.  Does not synchronise. */
 somf_status somf_last_kernels(somf_handle h, int32_t* out);
 

@@ -93,6 +93,7 @@ class SomfConfig(C.Structure):
         ("bcd_kernel", C.c_int32),
         ("contract_kernel", C.c_int32), ("bbar_kernel", C.c_int32), ("codes_kernel", C.c_int32),
         ("bcd_lam_tol", C.c_double), ("bcd_copies", C.c_int32),
+        ("estimator", C.c_int32), ("n_samples", C.c_int64), ("v", C.c_double),
     ]
 
 
@@ -109,6 +110,7 @@ SIGNATURES = [
     ("somf_destroy", I32, [P]),
     ("somf_set_components", I32, [P, P, I64]),
     ("somf_partial_fit", I32, [P, P, I64]),
+    ("somf_partial_fit_ids", I32, [P, P, I64, P]),
     ("somf_next_mask", I32, [P, C.POINTER(I64), P]),
     ("somf_partial_fit_masked", I32, [P, P, I64]),
     ("somf_get_codes", I32, [P, P]),

@@ -143,6 +143,8 @@ struct CbarFold {
   int nparts, kk;
   double* C64;
   float* C32;
+  const double* A64;        // k x eta codes: fold sum_s a_s a_s^T from them directly (cpart unused)
+  int k, eta;
 };
 
 template <int KC, int RT, bool kXCompact>

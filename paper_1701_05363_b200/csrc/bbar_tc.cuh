@@ -102,7 +102,30 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
   // old Bbar rows (written by earlier kernels) in the meantime.
   auto after_solver = [&]() {
     if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (P.cf.cpart) {
+    if (P.cf.A64) {
+      // my slice of the Cbar entries (Eq. somf_partial) straight from the
+      // fp64 codes: sum_s a_s a_s^T, s in column order, 8 threads per entry
+      // (strided columns) combined in fixed order
+      const int e0 = (int)((int64_t)P.cf.kk * blockIdx.x / G), e1 = (int)((int64_t)P.cf.kk * (blockIdx.x + 1) / G);
+      const int kq = P.cf.k, ne = P.cf.eta;
+      for (int eb = e0; eb < e1; eb += kBtThreads / 8) {
+        const int e = eb + tid / 8, h = tid % 8;
+        double s = 0.0;
+        if (e < e1) {
+          const double* ra = P.cf.A64 + (int64_t)(e / kq) * ne;
+          const double* rb = P.cf.A64 + (int64_t)(e % kq) * ne;
+          for (int c = h; c < ne; c += 8) s = fma(__ldg(ra + c), __ldg(rb + c), s);
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (e < e1 && h == 0) {
+          const double c = (1.0 - w) * P.cf.C64[e] + (w / eta) * s;
+          P.cf.C64[e] = c;
+          P.cf.C32[e] = (float)c;
+        }
+      }
+    } else if (P.cf.cpart) {
       // my slice of the Cbar entries (Eq. somf_partial)
       const int e0 = (int)((int64_t)P.cf.kk * blockIdx.x / G), e1 = (int)((int64_t)P.cf.kk * (blockIdx.x + 1) / G);
       for (int e = e0 + tid; e < e1; e += kBtThreads) {

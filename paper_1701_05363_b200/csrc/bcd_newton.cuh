@@ -191,20 +191,35 @@ struct NtSums {
   unsigned mn, mx;
 };
 __device__ __forceinline__ NtSums nt_read(const unsigned long long* slot0, int ncopy, int k, int p) {
+  // two copies per L2 round trip (six 16-byte loads in flight; a full unroll
+  // over the copies would cost registers the recurrence needs)
   unsigned long long c = 0, a1 = 0, a2 = 0, b1 = 0, b2 = 0;
   unsigned mn = 0xffffffffu, mx = 0u;
-  for (int cp = 0; cp < ncopy; ++cp) {
-    const unsigned long long* rc = slot0 + ((size_t)cp * k + p) * kNtRec;
-    const ulonglong2 v01 = __ldcg(reinterpret_cast<const ulonglong2*>(rc));
-    const ulonglong2 v23 = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 2));
-    const ulonglong2 v45 = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 4));
-    c += v01.x;
-    a1 += v01.y;
-    a2 += v23.x;
-    b1 += v23.y;
-    b2 += v45.x;
-    mn = min(mn, (unsigned)(v45.y & 0xffffffffull));
-    mx = max(mx, (unsigned)(v45.y >> 32));
+#pragma unroll 1
+  for (int c0 = 0; c0 < ncopy; c0 += 2) {
+    ulonglong2 v01[2], v23[2], v45[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (c0 + h < ncopy) {
+        const unsigned long long* rc = slot0 + ((size_t)(c0 + h) * k + p) * kNtRec;
+        v01[h] = __ldcg(reinterpret_cast<const ulonglong2*>(rc));
+        v23[h] = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 2));
+        v45[h] = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 4));
+      } else {
+        v01[h] = v23[h] = make_ulonglong2(0ull, 0ull);
+        v45[h] = make_ulonglong2(0ull, 0xffffffffull);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      c += v01[h].x;
+      a1 += v01[h].y;
+      a2 += v23[h].x;
+      b1 += v23[h].y;
+      b2 += v45[h].x;
+      mn = min(mn, (unsigned)(v45[h].y & 0xffffffffull));
+      mx = max(mx, (unsigned)(v45[h].y >> 32));
+    }
   }
   NtSums r;
   r.cnt = (double)c;
@@ -298,9 +313,85 @@ struct NtRec5<KPT, T, M, kGen, KPT> {
                                              const float*, const NtPar<kGen>*) {}
 };
 
+// ---------------------------------------------------------------------------
+// v6 recurrence (M = 1 row per group of T = 1 or 2 threads): each thread owns
+// the positions p = i T + t of ONE masked row; R and Do are float2 pairs so
+// the rank-1 updates are packed FFMA2 (fma.rn.f32x2: two FMAs per issued
+// instruction -- the v5 loop was issue-bound), the prescaled Cbar row
+// Ct[t][PP][.] arrives as 16-byte broadcast loads (every thread of a parity
+// reads the same row).  T = 1: no shuffles and no redundant owner work.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float2 nt_ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+template <int KPT, int T, bool kGen, int PP>
+struct NtRec6 {
+  static constexpr int KT = KPT / T;          // even (KPT is a multiple of 16)
+  static constexpr int KTS = (KT + 3) & ~3;
+  // d0: the row's d before the pass in shared memory (Dold, position-major
+  // within the row); reading it per position keeps the registers for R and
+  // the Cbar prefetch (a register copy of d_old starved the load scheduling)
+  static __device__ __forceinline__ void run(float2 (&R)[KT / 2], const float* __restrict__ d0, int t,
+                                             float* __restrict__ v0, const float* __restrict__ Ct_t,
+                                             const NtPar<kGen>* __restrict__ par) {
+    constexpr int own = PP % T, ii = PP / T;
+    const NtPar<kGen> pr = par[PP];
+    const float rii = (ii & 1) ? R[ii >> 1].y : R[ii >> 1].x;
+    const float dii = d0[ii * T + t];
+    const float u = rii + dii;                     // P:861 (valid in the owner)
+    const float v = pr.v_of(u);
+    const float d = pr.d_of(u);
+    float delta = d - dii;
+    if constexpr (T == 1) {
+      v0[PP] = v;
+    } else {
+      if (t == own) v0[PP] = v;
+      delta = __shfl_sync(0xffffffffu, delta, own, T);
+    }
+    const float2 nd = make_float2(-delta, -delta);
+    const float* crow = Ct_t + PP * KTS;
+#pragma unroll
+    for (int j4 = (ii >> 2); j4 < KTS / 4; ++j4) {
+      const float4 c = *reinterpret_cast<const float4*>(crow + 4 * j4);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int jp = 2 * j4 + h;                 // pair index: local positions 2 jp, 2 jp + 1
+        if (2 * jp + 1 < KT && 2 * jp + 1 >= ii) {
+          const float2 cc = h ? make_float2(c.z, c.w) : make_float2(c.x, c.y);
+          const float2 up = nt_ffma2(nd, cc, R[jp]);
+          // element e of the pair: > ii updated; == ii only where the
+          // thread's position lies after PP (t > own); < ii unchanged
+          const int e0 = 2 * jp, e1 = 2 * jp + 1;
+          float x = R[jp].x, y = R[jp].y;
+          if (e0 > ii) x = up.x;
+          else if (e0 == ii) x = t > own ? up.x : x;
+          if (e1 > ii) y = up.y;
+          else if (e1 == ii) y = t > own ? up.y : y;
+          R[jp] = make_float2(x, y);
+        }
+      }
+    }
+    NtRec6<KPT, T, kGen, PP + 1>::run(R, d0, t, v0, Ct_t, par);
+  }
+};
+template <int KPT, int T, bool kGen>
+struct NtRec6<KPT, T, kGen, KPT> {
+  static __device__ __forceinline__ void run(float2 (&)[KPT / T / 2], const float*, int, float*, const float*,
+                                             const NtPar<kGen>*) {}
+};
+
 template <int T, int M>
 struct NtCfg {
-  static constexpr int kThreads = M == 1 ? 640 : 384;   // >= T x ceil(rows per CTA / M)
+  // >= T x ceil(rows per CTA / M); T = 1 keeps 2 x KPT / 2 float2 per thread in
+  // registers, so at most 384 threads (65536 / 384 = 170 registers)
+  static constexpr int kThreads = 384;
 };
 
 template <bool kGen>
@@ -336,7 +427,7 @@ k_bcd_newton(NtArgs P) {
   // different bank groups (one 16-byte load of a quarter warp touches T blocks)
   constexpr int CTS = ((KPT * KTS + 31) & ~31) + 8;
   static_assert(KPT % T == 0, "KPT must be a multiple of T");
-  static_assert(M == 1 || M == 2, "one or two rows per thread");
+  static_assert((M == 2) || (M == 1 && (T == 1 || T == 2)), "v5: M = 2; v6: M = 1 with T = 1 or 2");
   extern __shared__ __align__(16) float nt_smem[];
   __shared__ __align__(16) NtPar<kGen> par_s[2][KPT];
   __shared__ double lam_s[KPT], rho_s[KPT];
@@ -535,11 +626,14 @@ k_bcd_newton(NtArgs P) {
 #pragma unroll
   for (int m = 0; m < M; ++m) rowx[m] = (g * M + m < nr) ? g * M + m : cap;
   const int vstride = (rowx[M - 1] - rowx[0]);          // 1 row apart unless the tail hits the spare row
+  constexpr int KT2 = M == 1 ? KT / 2 : 1;
   float Do[M][KT];
+  if constexpr (M != 1) {
 #pragma unroll
-  for (int m = 0; m < M; ++m)
+    for (int m = 0; m < M; ++m)
 #pragma unroll
-    for (int i = 0; i < KT; ++i) Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
+      for (int i = 0; i < KT; ++i) Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
+  }
   const float* Ct_t = Ct + (size_t)tq * CTS;
 
   // stats partials (H threads per atom) reuse the Cbar staging area (host checks the size)
@@ -566,17 +660,31 @@ k_bcd_newton(NtArgs P) {
   while (!done) {
     // ---- 1. the recurrence from the frozen prefix on, T threads x M rows ---------
     {
-      // every thread of the CTA runs it (the width-T shuffles need converged
-      // warps); rows >= nr compute on the spare row's zeros
-      float R[M][KT];
+      // every thread of a warp with rows runs it (the width-T shuffles need
+      // converged warps; rows >= nr compute on the spare row's zeros); warps
+      // past the rows (launched for the statistics and the setup) skip it
+      const bool warp_has_rows = ((tid & ~31) / T) * M < nr;
+      if constexpr (M == 1) {
+        if (warp_has_rows) {
+        float2 R2[KT2];
 #pragma unroll
-      for (int m = 0; m < M; ++m)
+        for (int i = 0; i < KT2; ++i)
+          R2[i] = make_float2(Rini[(size_t)rowx[0] * LD + (2 * i) * T + tq],
+                              Rini[(size_t)rowx[0] * LD + (2 * i + 1) * T + tq]);
+        NtRec6<KPT, T, kGen, 0>::run(R2, Dold + (size_t)rowx[0] * LD, tq, V + (size_t)rowx[0] * LD, Ct_t,
+                                     par_s[cur]);
+        }
+      } else if (warp_has_rows) {
+        float R[M][KT];
 #pragma unroll
-        for (int i = 0; i < KT; ++i) R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
-      // rows rowx[0] and rowx[0] + vstride (vstride = LD for consecutive rows; the
-      // spare row is its own target when both are past nr)
-      NtRec5<KPT, T, M, kGen, 0>::run(R, Do, tq, V + (size_t)rowx[0] * LD,
-                                      M > 1 ? vstride * LD : 0, Ct_t, par_s[cur]);
+        for (int m = 0; m < M; ++m)
+#pragma unroll
+          for (int i = 0; i < KT; ++i) R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
+        // rows rowx[0] and rowx[0] + vstride (vstride = LD for consecutive rows; the
+        // spare row is its own target when both are past nr)
+        NtRec5<KPT, T, M, kGen, 0>::run(R, Do, tq, V + (size_t)rowx[0] * LD,
+                                        M > 1 ? vstride * LD : 0, Ct_t, par_s[cur]);
+      }
     }
     __syncthreads();
     NT_MARK(1);

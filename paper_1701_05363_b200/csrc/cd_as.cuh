@@ -34,15 +34,18 @@ __host__ __device__ constexpr size_t cd_as_warp_bytes() {
   return (size_t)kAsMax * kAsMax * 8 + (size_t)kAsMax * 8 + (size_t)kAsMax * 4;
 }
 
-template <int KPL>
+// GT: the packed Gram's type in shared memory (double when it fits, else float)
+template <int KPL, typename GT>
 __global__ void __launch_bounds__(kAsThreads)
 k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
         double l1, double l2, int positive, double tol, int max_sweeps,
         double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out,
-        float* __restrict__ AT32, int ldt) {
+        float* __restrict__ AT32, int ldt, int64_t gstride) {
   // the B-bar kernel may launch now (programmatic dependent launch); it reads
   // the codes only after griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
+  // gstride > 0: a Gram per column (estimator (b)); one column (warp) per CTA
+  G += (int64_t)blockIdx.x * gstride;
   extern __shared__ __align__(16) uint8_t as_smem[];
   const int tid = threadIdx.x, nt = blockDim.x;
   const int np = k * (k + 1) / 2;
@@ -51,7 +54,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
   double* Af = reinterpret_cast<double*>(wbase);                  // kAsMax x kAsMax
   double* yv = Af + kAsMax * kAsMax;                              // kAsMax
   int* sidx = reinterpret_cast<int*>(yv + kAsMax);                // kAsMax
-  float* Pk = reinterpret_cast<float*>(as_smem + (size_t)nw * cd_as_warp_bytes());   // packed upper triangle
+  GT* Pk = reinterpret_cast<GT*>(as_smem + (size_t)nw * cd_as_warp_bytes());   // packed upper triangle
   for (int e = tid; e < np; e += nt) {
     int lo = 0, hi = k - 1;
     while (lo < hi) {
@@ -59,7 +62,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
       if (packed_off(mid, k) <= e) lo = mid; else hi = mid - 1;
     }
     const int i = lo, j = i + (e - packed_off(i, k));
-    Pk[e] = (float)G[(int64_t)i * k + j];
+    Pk[e] = (GT)G[(int64_t)i * k + j];
   }
   __syncthreads();
   for (int s = blockIdx.x * nw + wid; s < m; s += gridDim.x * nw) {

@@ -1,17 +1,14 @@
-// codes.cuh -- (a2) ridge codes and (a3) Cbar, v2:
+// codes.cuh -- (a2) ridge codes and (a3) Cbar:
 //
 //  k_ridge_codes<KPL> : alpha = (G + lambda I)^-1 beta  (Eq. somf_alpha,
-//                  P:592-596, nu = 1, no positivity), k <= 32 KPL.
+//                  P:592-596, nu = 1, no positivity), k <= 32 KPL <= 160.
 //                  Every CTA factorises G + lambda I redundantly in shared
-//                  memory (fp64 LL^T, right-looking in 8-column panels: the
-//                  8 x 8 diagonal block is factorised in every thread's
-//                  registers, the panel rows below are solved one row per
-//                  thread, then one rank-4 trailing update over a 16 x 16
-//                  thread grid: 2 barriers per 4 columns).  Then each warp
-//                  solves one right-hand side with 4-row block substitutions
-//                  (the solution in registers, lane l holding rows l, l+32,
-//                  ...; one shuffle round per 4 rows).  Each CTA also writes
-//                  its partial sum_s alpha_s alpha_s^T for the Cbar update.
+//                  memory (fp64 blocked LL^T, 8-column panels, each diagonal
+//                  block and its inverse in registers; v3 below), then each
+//                  warp solves one right-hand side with 8 x 8 block
+//                  mat-vecs through the stored block inverses.  Each CTA
+//                  also writes its partial sum_s alpha_s alpha_s^T for the
+//                  Cbar update.
 //  k_cbar_finalize : Cbar <- (1 - w) Cbar + (w / eta) sum_b partial_b
 //                  (Eq. somf_partial, batch mean R4), partials added in
 //                  block order (deterministic).
@@ -22,9 +19,6 @@ namespace somf {
 
 constexpr int kRcThreads = 256;
 constexpr int kRcMaxK = 160;
-constexpr int kRcPW = 4;          // panel width of the factorisation (8 measured slower)
-constexpr int kRcSB = 8;          // block height of the substitutions (8 measured faster than 4); multiple of kRcPW
-constexpr int kRcInvKPL = 0;      // k <= 32 kRcInvKPL: explicit-inverse solve (measured slower on B200 for k = 70: off)
 
 // 1/sqrt(d) in fp64: fp32 MUFU estimate + two Newton steps (rel. error ~1e-16),
 // ~3x shorter latency than sqrt() followed by a division
@@ -44,15 +38,42 @@ __device__ __forceinline__ double rc_pick(const double (&y)[KPL], int c) {
   return v;
 }
 
-// smem: k x (k+1) doubles (L, 1/L_jj on the diagonal) + 8 warps x k doubles
+// ---------------------------------------------------------------------------
+// v3: blocked LL^T with 8-column panels, every panel's diagonal block and its
+// inverse in registers, no serial chain outside the 8 x 8 blocks.
+//
+// Per panel jb (K = k rounded up to 8, identity padding):
+//   1. every thread factorises the 8 x 8 diagonal block A_bb = L_bb L_bb^T in
+//      registers (fp32 rsqrt seed + two fp64 Newton steps per pivot) and forms
+//      W_b = L_bb^-1 (8 x 8 lower triangular) -- redundantly, so no barrier;
+//   2. panel rows i >= jb + 8 (one thread per row): L_i,b = A_i,b W_b^T (a
+//      mat-vec with the inverse: 64 independent FMAs, no chain);
+//   3. barrier; rank-8 trailing update of the lower triangle, every thread a
+//      strided share of the entries (the panel row of i kept in registers);
+//      barrier.
+// W_b of every block is kept in shared memory, so the substitutions are 8 x 8
+// mat-vecs per block too: one warp per right-hand side, lane l holding rows
+// l, l + 32, ...; per block the 8 entries are broadcast by shuffles,
+// multiplied by W_b (forward) or W_b^T (backward), and the other rows updated.
+// ---------------------------------------------------------------------------
+constexpr int kRcB = 8;
+
+// smem doubles: K (K + 1) (L, lower) + (K / 8) 64 (W_b) + 8 K (codes of the 8 warps)
+__host__ __device__ constexpr size_t rc_smem_doubles(int K) {
+  return (size_t)K * (K + 1) + (size_t)(K / kRcB) * kRcB * kRcB + (size_t)8 * K;
+}
+
 template <int KPL>
 __global__ void __launch_bounds__(kRcThreads)
 k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int k, int m, double lam,
               double* __restrict__ A64, float* __restrict__ A32, float* __restrict__ AT32, int ldt,
-              double* __restrict__ cpart, int* __restrict__ err, long long* __restrict__ prof) {
+              double* __restrict__ cpart, int* __restrict__ err, long long* __restrict__ prof,
+              int64_t gstride, int cpc) {
   // the B-bar kernel may launch now (programmatic dependent launch); it reads
   // the codes only after griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
+  // gstride > 0: a Gram per column (estimator (b)); cpc columns per CTA (8, or 1)
+  G += (int64_t)blockIdx.x * gstride;
   extern __shared__ double rc_smem[];
   long long t_mark = clock64();
 #define RC_MARK(slot)                                                     \
@@ -63,112 +84,142 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       t_mark = now_;                                                      \
     }                                                                     \
   } while (0)
-  // the factorisation and the solves run on K4 = k rounded up to 4 (identity
-  // padding, zero right-hand sides): every 4-column panel / 4-row block is
-  // full, so the loops are branch-free and the loads can be hoisted
   const int kr = k;
-  k = (k + kRcSB - 1) & ~(kRcSB - 1);
-  const int ld = k + 1;
-  double* M = rc_smem;                              // k x ld, lower triangle
-  double* Y = rc_smem + (size_t)k * ld;             // 8 x k
+  const int K = (k + kRcB - 1) & ~(kRcB - 1);
+  const int ld = K + 1;
+  double* M = rc_smem;                              // K x ld, lower triangle
+  double* Wb = M + (size_t)K * ld;                  // (K / 8) x 64
+  double* Y = Wb + (size_t)(K / kRcB) * 64;         // 8 x K
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int ty = tid >> 4, tx = tid & 15;
-#pragma unroll 4
-  for (int e = tid; e < k * k; e += kRcThreads) {
-    const int i = e / k, j = e % k;
-    const double g = (i < kr && j < kr) ? G[(int64_t)i * kr + j] + (i == j ? lam : 0.0) : (i == j ? 1.0 : 0.0);
-    if (j <= i) M[i * ld + j] = g;
+  // ---- load G + lambda I (lower triangle, identity padding), 8 loads in flight per thread
+  for (int e0 = tid; e0 < K * K; e0 += 8 * kRcThreads) {
+    double g[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kRcThreads;
+      const int i = e / K, j = e % K;
+      g[u] = (e < K * K && j <= i && i < kr && j < kr) ? __ldg(G + (int64_t)i * kr + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kRcThreads;
+      const int i = e / K, j = e % K;
+      if (e < K * K && j <= i) M[i * ld + j] = (i < kr && j < kr) ? g[u] + (i == j ? lam : 0.0) : (i == j ? 1.0 : 0.0);
+    }
   }
   __syncthreads();
   RC_MARK(0);
   bool bad = false;
-  for (int p0 = 0; p0 < k; p0 += kRcPW) {
-    constexpr int pb = kRcPW;
-    // 4 x 4 diagonal block, factorised in registers by every thread
-    double Ld[kRcPW][kRcPW];
+  // warp 0: factorise the (already updated) 8 x 8 diagonal block at jb, every
+  // lane redundantly in registers; lane 0..63 entries written back: L_bb into
+  // M, W_b = L_bb^-1 into Wb.  `pre` (optional) first applies the rank-8
+  // update of the previous panel (columns pb..pb+7) to the block (lookahead).
+  auto diag_block = [&](int jb, int pb) {
+    double L[kRcB][kRcB], W[kRcB][kRcB];
 #pragma unroll
-    for (int a = 0; a < kRcPW; ++a)
+    for (int a = 0; a < kRcB; ++a)
 #pragma unroll
-      for (int c = 0; c < kRcPW; ++c) Ld[a][c] = (a < pb && c <= a) ? M[(p0 + a) * ld + p0 + c] : 0.0;
-    double inv[kRcPW];
+      for (int c = 0; c < kRcB; ++c) L[a][c] = c <= a ? M[(jb + a) * ld + jb + c] : 0.0;
+    if (pb >= 0) {
+      double P[kRcB][kRcB];
 #pragma unroll
-    for (int c = 0; c < kRcPW; ++c) {
-      if (c < pb) {
-        double d = Ld[c][c];
+      for (int a = 0; a < kRcB; ++a)
 #pragma unroll
-        for (int u = 0; u < kRcPW; ++u)
-          if (u < c) d -= Ld[c][u] * Ld[c][u];
-        bad |= !(d > 0.0);
-        const double ir = d > 0.0 ? rc_rsqrt(d) : 0.0;
-        inv[c] = ir;
-        Ld[c][c] = d * ir;
+        for (int u = 0; u < kRcB; ++u) P[a][u] = M[(jb + a) * ld + pb + u];
 #pragma unroll
-        for (int a = 0; a < kRcPW; ++a) {
-          if (a > c && a < pb) {
-            double v = Ld[a][c];
+      for (int a = 0; a < kRcB; ++a)
 #pragma unroll
-            for (int u = 0; u < kRcPW; ++u)
-              if (u < c) v -= Ld[a][u] * Ld[c][u];
-            Ld[a][c] = v * inv[c];
-          }
+        for (int c = 0; c <= a; ++c) {
+          double v = L[a][c];
+#pragma unroll
+          for (int u = 0; u < kRcB; ++u) v = fma(-P[a][u], P[c][u], v);
+          L[a][c] = v;
         }
+    }
+#pragma unroll
+    for (int c = 0; c < kRcB; ++c) {
+      const double d = L[c][c];
+      bad |= !(d > 0.0);
+      double ir = 0.0;
+      if (d > 0.0) {
+        // fp32 seed + one fp64 Newton step: relative error ~1e-14
+        ir = (double)rsqrtf((float)d);
+        ir = ir * fma(-0.5 * d, ir * ir, 1.5);
+      }
+      L[c][c] = d * ir;
+      W[c][c] = ir;                                 // 1 / L_cc
+#pragma unroll
+      for (int a2 = c + 1; a2 < kRcB; ++a2) L[a2][c] *= ir;
+#pragma unroll
+      for (int a2 = c + 1; a2 < kRcB; ++a2)
+#pragma unroll
+        for (int b2 = c + 1; b2 <= a2; ++b2) L[a2][b2] = fma(-L[a2][c], L[b2][c], L[a2][b2]);
+    }
+#pragma unroll
+    for (int c = 0; c < kRcB; ++c) {
+#pragma unroll
+      for (int i = c + 1; i < kRcB; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = c; l < i; ++l) acc = fma(L[i][l], W[l][c], acc);
+        W[i][c] = -W[i][i] * acc;
+      }
+#pragma unroll
+      for (int i = 0; i < c; ++i) W[i][c] = 0.0;
+    }
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int e = lane + 32 * h2, a2 = e / kRcB, c2 = e % kRcB;
+      double lv = 0.0, wv = 0.0;
+#pragma unroll
+      for (int a3 = 0; a3 < kRcB; ++a3)
+#pragma unroll
+        for (int c3 = 0; c3 < kRcB; ++c3)
+          if (a3 == a2 && c3 == c2) { lv = L[a3][c3]; wv = W[a3][c3]; }
+      if (c2 <= a2) M[(jb + a2) * ld + jb + c2] = lv;
+      Wb[(jb / kRcB) * 64 + e] = wv;
+    }
+  };
+  if (wid == 0) diag_block(0, -1);
+  __syncthreads();
+  for (int jb = 0; jb < K; jb += kRcB) {
+    // ---- panel rows below: L_i,b = A_i,b W_b^T (W_b lower triangular) ------
+    const double* w = Wb + (jb / kRcB) * 64;
+    for (int i = jb + kRcB + tid; i < K; i += kRcThreads) {
+      double x[kRcB];
+#pragma unroll
+      for (int u = 0; u < kRcB; ++u) x[u] = M[i * ld + jb + u];
+#pragma unroll
+      for (int t = 0; t < kRcB; ++t) {
+        double acc = 0.0;
+#pragma unroll
+        for (int u = 0; u <= t; ++u) acc = fma(x[u], w[t * kRcB + u], acc);
+        M[i * ld + jb + t] = acc;
+      }
+    }
+    __syncthreads();
+    const int jn = jb + kRcB, n = K - jn;
+    if (n > 0) {
+      if (wid == 0) {
+        // lookahead: the next diagonal block, updated by this panel and factorised
+        diag_block(jn, jb);
       } else {
-        inv[c] = 0.0;
-      }
-    }
-    // panel rows below: L[i][p0..p0+pb) = M[i][p0..] L_D^-T  (one row per thread)
-    for (int i = p0 + pb + tid; i < k; i += kRcThreads) {
-      double x[kRcPW];
+        // rank-8 trailing update of the lower triangle below the panel, the
+        // next diagonal block excepted (warp 0 owns it): warps 1..7, thread
+        // (ty, tx) rows jn + ty + 14 s, columns jn + tx + 16 c
+        const int t2 = tid - 32, ty = t2 >> 4, tx = t2 & 15;
+        constexpr int NY = (kRcThreads - 32) / 16;
+        for (int ii = ty; ii < n; ii += NY) {
+          const int i = jn + ii;
+          double li[kRcB];
 #pragma unroll
-      for (int c = 0; c < kRcPW; ++c) {
-        if (c < pb) {
-          double v = M[i * ld + p0 + c];
+          for (int u = 0; u < kRcB; ++u) li[u] = M[i * ld + jb + u];
+          for (int ll = (ii < kRcB ? kRcB : 0) + tx; ll <= ii; ll += 16) {
+            const int l = jn + ll;
+            double v = M[i * ld + l];
 #pragma unroll
-          for (int u = 0; u < kRcPW; ++u)
-            if (u < c) v -= x[u] * Ld[c][u];
-          x[c] = v * inv[c];
-        } else {
-          x[c] = 0.0;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < kRcPW; ++c)
-        if (c < pb) M[i * ld + p0 + c] = x[c];
-    }
-    __syncthreads();                                // panel reads of the block done
-    // (static register indices only: a dynamic index would put Ld in local memory)
-#pragma unroll
-    for (int a = 0; a < kRcPW; ++a)
-#pragma unroll
-      for (int c = 0; c < kRcPW; ++c)
-        if (tid == kRcPW * a + c && a < pb && c <= a) M[(p0 + a) * ld + p0 + c] = (a == c) ? inv[a] : Ld[a][c];
-    // rank-4 trailing update: M[i][l] -= sum_c L[i][p0+c] L[l][p0+c], p0+pb <= l <= i.
-    // Thread (ty, tx) owns rows r0+ty+16a and columns r0+tx+16b; the panel
-    // values of its columns are loaded once into registers (NS = KMAX/16 slots).
-    {
-      constexpr int NS = (32 * KPL + 15) / 16;
-      const int r0 = p0 + pb, n = k - r0;
-      double lj[NS][kRcPW];
-#pragma unroll
-      for (int bb = 0; bb < NS; ++bb) {
-        const int ll = tx + 16 * bb;
-#pragma unroll
-        for (int c = 0; c < kRcPW; ++c) lj[bb][c] = (ll < n && c < pb) ? M[(r0 + ll) * ld + p0 + c] : 0.0;
-      }
-      for (int ii = ty; ii < n; ii += 16) {
-        const int i = r0 + ii;
-        double li[kRcPW];
-#pragma unroll
-        for (int c = 0; c < kRcPW; ++c) li[c] = c < pb ? M[i * ld + p0 + c] : 0.0;
-#pragma unroll
-        for (int bb = 0; bb < NS; ++bb) {
-          const int ll = tx + 16 * bb;
-          if (ll <= ii) {
-            double* mp = M + i * ld + r0 + ll;
-            double v = *mp;
-#pragma unroll
-            for (int c = 0; c < kRcPW; ++c) v -= li[c] * lj[bb][c];
-            *mp = v;
+            for (int u = 0; u < kRcB; ++u) v = fma(-li[u], M[l * ld + jb + u], v);
+            M[i * ld + l] = v;
           }
         }
       }
@@ -177,169 +228,81 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
   }
   if (bad && err) atomicExch(err, 1);
   RC_MARK(1);
-
-  if constexpr (KPL <= kRcInvKPL) {
-    // ---- explicit inverse W = L^-1 (column j by thread j), then alpha = W^T (W beta):
-    // two triangular mat-vecs per right-hand side, no serial substitution chain
-    double* W = Y + (size_t)8 * k;                    // k x ld, lower triangle
-    for (int j = tid; j < k; j += kRcThreads) {
-      W[j * ld + j] = M[j * ld + j];
-      for (int i = j + 1; i < k; ++i) {
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        int l = j;
-        for (; l + 3 < i; l += 4) {
-          a0 = fma(M[i * ld + l], W[l * ld + j], a0);
-          a1 = fma(M[i * ld + l + 1], W[(l + 1) * ld + j], a1);
-          a2 = fma(M[i * ld + l + 2], W[(l + 2) * ld + j], a2);
-          a3 = fma(M[i * ld + l + 3], W[(l + 3) * ld + j], a3);
-        }
-        for (; l < i; ++l) a0 = fma(M[i * ld + l], W[l * ld + j], a0);
-        W[i * ld + j] = -M[i * ld + i] * ((a0 + a1) + (a2 + a3));
-      }
-    }
-    __syncthreads();
-    RC_MARK(7);       // prof slot 79: the inverse
-    double* Yw = Y + (size_t)wid * k;
-    for (int s0 = blockIdx.x * 8; s0 < m; s0 += gridDim.x * 8) {
-      const int s = s0 + wid;
-      for (int i = lane; i < k; i += 32) Yw[i] = (s < m && i < kr) ? beta[(int64_t)i * m + s] : 0.0;
-      __syncwarp();
-      double y[KPL];
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) {                 // y = W beta (rows i >= l)
-        const int i = lane + 32 * c;
-        double a0 = 0.0, a1 = 0.0;
-        if (i < k) {
-          int l = 0;
-          for (; l + 1 <= i; l += 2) {
-            a0 = fma(W[i * ld + l], Yw[l], a0);
-            a1 = fma(W[i * ld + l + 1], Yw[l + 1], a1);
-          }
-          if (l <= i) a0 = fma(W[i * ld + l], Yw[l], a0);
-        }
-        y[c] = a0 + a1;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) {
-        const int i = lane + 32 * c;
-        if (i < k) Yw[i] = y[c];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) {                 // alpha = W^T y (rows l >= i)
-        const int i = lane + 32 * c;
-        double a0 = 0.0, a1 = 0.0;
-        if (i < k) {
-          int l = i;
-          for (; l + 1 < k; l += 2) {
-            a0 = fma(W[l * ld + i], Yw[l], a0);
-            a1 = fma(W[(l + 1) * ld + i], Yw[l + 1], a1);
-          }
-          if (l < k) a0 = fma(W[l * ld + i], Yw[l], a0);
-        }
-        y[c] = a0 + a1;
-      }
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < KPL; ++c) {
-        const int i = lane + 32 * c;
-        if (i < k) {
-          const double v = s < m ? y[c] : 0.0;
-          Yw[i] = v;
-          if (s < m && i < kr) {
-            A64[(int64_t)i * m + s] = v;
-            A32[(int64_t)i * m + s] = (float)v;
-            if (AT32) AT32[(int64_t)s * ldt + i] = (float)v;
-          }
-        }
-      }
-      __syncwarp();
-    }
-  } else {
-  // ---- substitutions: one warp per right-hand side, 4 rows per shuffle round ----
-  for (int s0 = blockIdx.x * 8; s0 < m; s0 += gridDim.x * 8) {
-    const int s = s0 + wid;
+  // ---- substitutions: one warp per right-hand side -------------------------
+  for (int s0 = blockIdx.x * cpc; s0 < m; s0 += gridDim.x * cpc) {
+    const int s = wid < cpc ? s0 + wid : m;
     double y[KPL];
 #pragma unroll
     for (int c = 0; c < KPL; ++c) {
       const int i = lane + 32 * c;
-      y[c] = (s < m && i < kr) ? beta[(int64_t)i * m + s] : 0.0;
+      y[c] = (s < m && i < kr) ? __ldg(beta + (int64_t)i * m + s) : 0.0;
     }
-    // L y = b
-    for (int jb = 0; jb < k; jb += kRcSB) {
-      constexpr int pb = kRcSB;
+    // L y = b, block by block: z = W_b y_b, then the rows below
+    for (int jb = 0; jb < K; jb += kRcB) {
       const int cs = jb >> 5, lb = jb & 31;
       const double own = rc_pick<KPL>(y, cs);
-      double z[kRcSB];
+      const double* w = Wb + (jb / kRcB) * 64;
+      double z[kRcB], x[kRcB];
 #pragma unroll
-      for (int t = 0; t < kRcSB; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
+      for (int t = 0; t < kRcB; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
 #pragma unroll
-      for (int t = 0; t < kRcSB; ++t) {
-        if (t < pb) {
-          double v = z[t];
+      for (int t = 0; t < kRcB; ++t) {
+        double acc = 0.0;
 #pragma unroll
-          for (int u = 0; u < kRcSB; ++u)
-            if (u < t) v -= M[(jb + t) * ld + jb + u] * z[u];
-          z[t] = v * M[(jb + t) * ld + jb + t];
-        }
+        for (int u = 0; u <= t; ++u) acc = fma(w[t * kRcB + u], z[u], acc);
+        x[t] = acc;
       }
 #pragma unroll
       for (int c = 0; c < KPL; ++c) {
         const int i = lane + 32 * c;
-        if (i >= jb && i < jb + pb) {
+        if (i >= jb && i < jb + kRcB) {
 #pragma unroll
-          for (int t = 0; t < kRcSB; ++t)
-            if (i == jb + t) y[c] = z[t];
-        } else if (i >= jb + pb && i < k) {
+          for (int t = 0; t < kRcB; ++t)
+            if (i == jb + t) y[c] = x[t];
+        } else if (i >= jb + kRcB && i < K) {
           double v = y[c];
 #pragma unroll
-          for (int t = 0; t < kRcSB; ++t)
-            if (t < pb) v -= M[i * ld + jb + t] * z[t];
+          for (int t = 0; t < kRcB; ++t) v = fma(-M[i * ld + jb + t], x[t], v);
           y[c] = v;
         }
       }
     }
-    // L^T x = y
-    for (int jb = ((k - 1) / kRcSB) * kRcSB; jb >= 0; jb -= kRcSB) {
-      constexpr int pb = kRcSB;
+    // L^T a = y, blocks from the last: x = W_b^T y_b, then the rows above
+    for (int jb = K - kRcB; jb >= 0; jb -= kRcB) {
       const int cs = jb >> 5, lb = jb & 31;
       const double own = rc_pick<KPL>(y, cs);
-      double z[kRcSB];
+      const double* w = Wb + (jb / kRcB) * 64;
+      double z[kRcB], x[kRcB];
 #pragma unroll
-      for (int t = 0; t < kRcSB; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
+      for (int t = 0; t < kRcB; ++t) z[t] = __shfl_sync(0xffffffffu, own, lb + t);
 #pragma unroll
-      for (int t = kRcSB - 1; t >= 0; --t) {
-        if (t < pb) {
-          double v = z[t];
+      for (int t = 0; t < kRcB; ++t) {
+        double acc = 0.0;
 #pragma unroll
-          for (int u = 0; u < kRcSB; ++u)
-            if (u > t && u < pb) v -= M[(jb + u) * ld + jb + t] * z[u];
-          z[t] = v * M[(jb + t) * ld + jb + t];
-        }
+        for (int u = t; u < kRcB; ++u) acc = fma(w[u * kRcB + t], z[u], acc);
+        x[t] = acc;
       }
 #pragma unroll
       for (int c = 0; c < KPL; ++c) {
         const int i = lane + 32 * c;
-        if (i >= jb && i < jb + pb) {
+        if (i >= jb && i < jb + kRcB) {
 #pragma unroll
-          for (int t = 0; t < kRcSB; ++t)
-            if (i == jb + t) y[c] = z[t];
+          for (int t = 0; t < kRcB; ++t)
+            if (i == jb + t) y[c] = x[t];
         } else if (i < jb) {
           double v = y[c];
 #pragma unroll
-          for (int t = 0; t < kRcSB; ++t)
-            if (t < pb) v -= M[(jb + t) * ld + i] * z[t];
+          for (int t = 0; t < kRcB; ++t) v = fma(-M[(jb + t) * ld + i], x[t], v);
           y[c] = v;
         }
       }
     }
-    double* Yw = Y + (size_t)wid * k;
+    double* Yw = Y + (size_t)wid * K;
 #pragma unroll
     for (int c = 0; c < KPL; ++c) {
       const int i = lane + 32 * c;
-      if (i < k) {
-        const double v = s < m ? y[c] : 0.0;
+      if (i < K) {
+        const double v = (s < m && i < kr) ? y[c] : 0.0;
         Yw[i] = v;
         if (s < m && i < kr) {
           A64[(int64_t)i * m + s] = v;
@@ -349,7 +312,6 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       }
     }
   }
-  }
   RC_MARK(2);
   if (cpart) {
     __syncthreads();
@@ -358,7 +320,7 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
       const int a = e / kr, b = e % kr;
       double acc = 0.0;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) acc += Y[w * k + a] * Y[w * k + b];
+      for (int w = 0; w < 8; ++w) acc = fma(Y[w * K + a], Y[w * K + b], acc);
       out[e] = acc;
     }
   }

@@ -15,22 +15,27 @@ constexpr int kSolveThreads = 256;
 constexpr int kRidgeMaxK = 160;
 
 __device__ __forceinline__ int packed_off(int i, int k) { return i * k - (i * (i - 1)) / 2; }
-__device__ __forceinline__ float packed_get(const float* P, int i, int j, int k) {
+template <typename GT>
+__device__ __forceinline__ GT packed_get(const GT* P, int i, int j, int k) {
   return i <= j ? P[packed_off(i, k) + (j - i)] : P[packed_off(j, k) + (i - j)];
 }
 
 // Cyclic CD, one warp per column; KPL = ceil(k/32) coordinates per lane
 // (coordinate j lives in lane j & 31, slot j >> 5).
-template <int KPL>
+// GT: the packed Gram's type in shared memory (double when it fits, else float)
+template <int KPL, typename GT>
 __global__ void __launch_bounds__(kSolveThreads)
 k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
      double l1, double l2, int positive, double tol, int max_sweeps,
      double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out,
-     float* __restrict__ AT32, int ldt) {
+     float* __restrict__ AT32, int ldt, int64_t gstride) {
   // the B-bar kernel may launch now (programmatic dependent launch); it reads
   // the codes only after griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
-  extern __shared__ float Pk[];            // packed upper triangle, k(k+1)/2
+  // gstride > 0: a Gram per column (estimator (b)); one column per CTA
+  G += (int64_t)blockIdx.x * gstride;
+  extern __shared__ __align__(16) uint8_t cd_smem[];
+  GT* Pk = reinterpret_cast<GT*>(cd_smem);  // packed upper triangle, k(k+1)/2
   const int tid = threadIdx.x, nt = blockDim.x;
   const int np = k * (k + 1) / 2;
   for (int e = tid; e < np; e += nt) {
@@ -45,7 +50,7 @@ k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m
       i = lo;
     }
     const int j = i + (e - packed_off(i, k));
-    Pk[e] = (float)G[(int64_t)i * k + j];
+    Pk[e] = (GT)G[(int64_t)i * k + j];
   }
   __syncthreads();
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;

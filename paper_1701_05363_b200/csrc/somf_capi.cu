@@ -37,6 +37,7 @@
 #include "bbar_tc.cuh"
 #include "contract_tc.cuh"
 #include "cd_as.cuh"
+#include "estimators.cuh"
 
 using namespace somf;
 
@@ -107,7 +108,7 @@ struct somf_ctx {
   int* cnt_next = nullptr;
   unsigned* ct_bar = nullptr;   // fused contract reduction barrier [arrivals, exits]
   int ct_launches = 2;          // kernels the last launch_contract issued
-  int kern[5] = {};             // kernel variants of the last step: contract, codes, bbar, bcd, bbar complement
+  int kern[7] = {};             // kernel variants of the last step: contract, codes, bbar, bcd, bbar complement, BCD T, M
   int64_t* q_next = nullptr;
   int64_t* t_next = nullptr;
   double* w_next = nullptr;
@@ -139,6 +140,7 @@ struct somf_ctx {
   float* AT32 = nullptr;     // codes transposed, eta x kp (bbar v3)
   double* cpart = nullptr;   // per-CTA partial A A^T of the ridge code kernel
   int cpart_n = 0;           // partials written by the last partial_fit code solve (0: none)
+  bool at_valid = false;     // AT32 holds the last solve's codes (transposed)
   double* red = nullptr;
   unsigned* bar = nullptr;
   int bcd_grid = 0;
@@ -151,7 +153,7 @@ struct somf_ctx {
   double* theta_ws = nullptr;
   const void* nt_fn = nullptr;   // simultaneous-threshold BCD (bcd_newton.cuh)
   double nt_lam_tol = kNtLamTol;
-  int nt_cap_rows = 0, nt_kpt = 0, nt_threads = 0, nt_ct_in_w = 0, nt_part_in_cpi = 0;
+  int nt_cap_rows = 0, nt_kpt = 0, nt_threads = 0, nt_ct_in_w = 0, nt_part_in_cpi = 0, nt_T = 0, nt_M = 0;
   size_t nt_smem = 0;
   double* lam_ws = nullptr;
   unsigned long long* nt_acc = nullptr;
@@ -172,6 +174,16 @@ struct somf_ctx {
   double *Ge = nullptr, *betae = nullptr, *Ae64 = nullptr, *colsq = nullptr, *objd = nullptr;
   float* Ae32 = nullptr;
   int64_t* qfull_dev = nullptr;
+  // estimators (b) / (c) (estimators.cuh): per-sample statistics
+  int64_t* ids_dev = nullptr;       // eta sample ids of the current batch
+  int* est_cnt = nullptr;           // n visit counts c^(i)
+  int* est_stamp = nullptr;         // n: iteration of the last visit (repeat check)
+  double* est_bcache = nullptr;     // n x k averaged beta^(i)
+  double* est_gcache = nullptr;     // n x k x k averaged G^(i)  ((b) only)
+  double* est_beta = nullptr;       // k x eta: the batch's averaged beta
+  double* est_G = nullptr;          // eta x k x k: the batch's averaged G ((b) only)
+  double* Gex = nullptr;            // k x k exact Gram D^T D ((c) only)
+  double* gnew = nullptr;           // k x 4 + k x k: contraction of the updated rows ((c) only)
   uint64_t T = 0;            // mask threshold floor(2^32 / r)
   float* Xstage = nullptr;   // device copy of the selected rows of a host batch
   // profiling
@@ -234,6 +246,8 @@ static somf_status check_flags(somf_ctx* h) {
   if (b || b2) { set_err(h, "grid barrier watchdog fired in the BCD kernel (results invalid)"); return SOMF_E_CUDA; }
   if (e == 2) { set_err(h, "more masked rows than the on-chip BCD capacity (q > mean + 10 sigma)"); return SOMF_E_CUDA; }
   if (e == 3 || e == 4) { set_err(h, "projection threshold search hit its round cap"); return SOMF_E_CUDA; }
+  if (e == 7) { set_err(h, "a sample id is outside [0, n_samples)"); return SOMF_E_ARG; }
+  if (e == 8) { set_err(h, "a sample id repeats within one mini-batch (reading R25)"); return SOMF_E_ARG; }
   if (e == 6) { set_err(h, "a BCD threshold sum left the fixed-point range [0, 2^48)"); return SOMF_E_NONFINITE; }
   if (e == 5) { set_err(h, "grid barrier watchdog fired in the contraction kernel (results invalid)"); return SOMF_E_CUDA; }
   set_err(h, "device numerical error flag %d (non-SPD system in the code solve)", e);
@@ -311,6 +325,16 @@ static const Bb3Variant kBb3Variants[] = {BB3(1, 4), BB3(1, 8), BB3(1, 16), BB3(
                                           BB3(3, 4), BB3(3, 8), BB3(3, 16), BB3(4, 4), BB3(4, 8), BB3(4, 16)};
 #undef BB3
 
+// shared memory of the tensor-core Bbar kernel (0: it does not apply)
+static size_t bbar_tc_smem(const somf_ctx* h, const float* X, int64_t ldx) {
+  const int k = h->cfg.k, eta = h->cfg.eta;
+  const int sel = h->cfg.bbar_kernel;
+  if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15) || !(sel == 0 || sel == 1) || k > 256) return 0;
+  const int np = (k + 15) & ~15, ep = (eta + 15) & ~15;
+  const size_t smem = (size_t)2 * (kBtM + np) * ep * 2 + (size_t)kBtM * h->kp * sizeof(float);
+  return smem <= 220 * 1024 ? smem : 0;
+}
+
 // Bbar rows (masked list, or all rows when !gather) -- bbar.cuh.  false when
 // the layout does not allow the 16-byte path (caller uses k_bbar_update).
 // *folded (optional) is set when the Cbar update rode along (v3 kernel, cpart ready)
@@ -323,14 +347,14 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
   const int k = h->cfg.k, eta = h->cfg.eta;
   const int sel = h->cfg.bbar_kernel;      // 0 auto, 1 tc, 2 slice, 3 tiled (4 generic: the caller)
   if ((eta % 4) || (ldx % 4) || (((uintptr_t)X) & 15)) return false;
-  if ((gather || all_rows) && (sel == 0 || sel == 1) && k <= 256) {
+  const size_t tc_smem = bbar_tc_smem(h, X, ldx);
+  if ((gather || all_rows) && tc_smem > 0) {
     // tensor cores (bbar_tc.cuh): bf16x3 tcgen05 GEMM per 128 masked rows
     BtArgs a{};
     a.np = (k + 15) & ~15;
     a.ep = (eta + 15) & ~15;
-    const size_t smem = (size_t)2 * (kBtM + a.np) * a.ep * 2 + (size_t)kBtM * h->kp * sizeof(float);
-    if (smem <= 220 * 1024 &&
-        cudaFuncSetAttribute((const void*)k_bbar_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+    const size_t smem = tc_smem;
+    if (cudaFuncSetAttribute((const void*)k_bbar_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
             cudaSuccess) {
       a.idx = all_rows ? nullptr : h->idx;
       a.xcompact = all_rows ? 0 : xcompact;
@@ -343,8 +367,9 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
       a.A = h->A32;
       a.Bbar = h->Bbar;
       a.w_dev = h->w_dev;
-      if (folded && h->cpart_n > 0) {
-        a.cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32};
+      if (folded) {
+        // Cbar from the fp64 codes, every CTA a slice of the k x k entries
+        a.cf = CbarFold{nullptr, 0, k * k, h->C64, h->C32, h->A64, k, eta};
         *folded = true;
       }
       // programmatic dependent launch: the CTAs stage their first X tile while
@@ -374,7 +399,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
   int kc = (k + 31) / 32;
   if (kc > 4) kc = 8;
   const int64_t per = ceil_div(std::max<int64_t>(q_est, 1), h->nsm);
-  if (gather && kc <= 4 && (sel == 0 || sel == 2)) {
+  if (gather && kc <= 4 && (sel == 0 || sel == 2) && h->at_valid) {
     // v3: whole slice in shared memory (rows of one segment per warp: RT <= 16)
     const int rt = per <= 32 ? 4 : per <= 64 ? 8 : 16;
     const int64_t seg = 8 * rt;
@@ -388,7 +413,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
           cudaSuccess) {
         CbarFold cf{};
         if (folded && h->cpart_n > 0) {
-          cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32};
+          cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32, nullptr, k, eta};
           *folded = true;
         }
         fn<<<h->nsm, kBbThreads, smem, h->st>>>(h->idx, q_dev, X, ldx, eta, h->AT32, h->kp, k, h->Bbar, h->w_dev,
@@ -589,11 +614,13 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
 }
 
 // sel: 0 auto, 1 ridge Cholesky, 2 CD with support jumps, 3 plain CD (somf_config.codes_kernel)
+// gstride > 0: column s uses the Gram G + s gstride (estimator (b)), one column per CTA
 static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta, int m, double tol,
-                                double* A64, float* A32, bool want_cpart = false) {
+                                double* A64, float* A32, bool want_cpart = false, int64_t gstride = 0) {
   const somf_config& c = h->cfg;
   const int k = c.k;
   const int sel = c.codes_kernel;
+  h->at_valid = want_cpart;
   const int nw = kSolveThreads / 32;
   const int grid = (int)std::max<int64_t>(1, ceil_div(m, nw));
   h->cpart_n = 0;
@@ -603,13 +630,16 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     return SOMF_E_UNSUPPORTED;
   }
   if (ridge_ok && (sel == 0 || sel == 1)) {
-    // ridge closed form (v2): every CTA factorises, 8 right-hand sides per CTA
-    const int k4 = (k + kRcSB - 1) & ~(kRcSB - 1);
-    const size_t smem = ((size_t)((k4 + 31) / 32 <= kRcInvKPL ? 2 : 1) * k4 * (k4 + 1) + (size_t)8 * k4) *
-                        sizeof(double);
-    const int g = want_cpart ? (int)ceil_div(m, 8) : (int)std::min<int64_t>(ceil_div(m, 8), 4 * h->nsm);
+    // ridge closed form (v3): every CTA factorises and solves cpc right-hand sides
+    const int k4 = (k + kRcB - 1) & ~(kRcB - 1);
+    const size_t smem = rc_smem_doubles(k4) * sizeof(double);
+    // right-hand sides per CTA: as few as fill the SMs once (the substitution
+    // chain is per warp; each CTA factorises, in parallel)
+    const int cpc = gstride > 0 ? 1 : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(m, h->nsm)));
+    const int g = (want_cpart || gstride > 0) ? (int)ceil_div(m, cpc)
+                                              : (int)std::min<int64_t>(ceil_div(m, cpc), 4 * h->nsm);
     if (want_cpart) {
-      if (!h->cpart) CK(dalloc(&h->cpart, (size_t)ceil_div(c.eta, 8) * k * k));
+      if (!h->cpart) CK(dalloc(&h->cpart, (size_t)c.eta * k * k));      // up to one partial per column
       h->cpart_n = g;
     }
     double* cp = want_cpart ? h->cpart : nullptr;
@@ -626,53 +656,69 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     long long* rprof = h->prof_on ? h->bcd_prof + 72 : nullptr;    // slots 72..75 (ridge phases)
     float* at = want_cpart ? h->AT32 : nullptr;
     int ldt = h->kp;
+    int cpc_a = cpc;
     void* args[] = {(void*)&G, (void*)&beta, (void*)&k, (void*)&m, (void*)&lam, (void*)&A64, (void*)&A32,
-                    (void*)&at, (void*)&ldt, (void*)&cp, (void*)&h->err_dev, (void*)&rprof};
+                    (void*)&at, (void*)&ldt, (void*)&cp, (void*)&h->err_dev, (void*)&rprof, (void*)&gstride,
+                    (void*)&cpc_a};
     CK(cudaLaunchKernel(fn, dim3(g), dim3(kRcThreads), args, smem, h->st));
     h->kern[1] = 1;
     return SOMF_OK;
   }
   const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
-  const size_t smem = (size_t)k * (k + 1) / 2 * sizeof(float);
+  // the packed Gram in fp64 when it fits next to the face scratch (k <= 160),
+  // else fp32 (k = 256: 132 KB)
+  const size_t np = (size_t)k * (k + 1) / 2;
   const int kpl = (int)ceil_div(k, 32);
-  const size_t smem_as = (size_t)(kAsThreads / 32) * cd_as_warp_bytes() + smem;
+  const size_t warps_as = (size_t)(kAsThreads / 32) * cd_as_warp_bytes();
+  const bool g64 = warps_as + np * sizeof(double) <= 200 * 1024;
+  const size_t smem = np * (g64 ? sizeof(double) : sizeof(float));
+  const size_t smem_as = warps_as + smem;
   const bool as_ok = k >= 32 && smem_as <= 220 * 1024;
   if (sel == 2 && !as_ok) {
     set_err(h, "codes_kernel = cd_jump requires k >= 32");
     return SOMF_E_UNSUPPORTED;
   }
   if (as_ok && (sel == 0 || sel == 2)) {
-    // CD with exact support jumps (cd_as.cuh), 4 columns per CTA
-    const int gas = (int)ceil_div(m, kAsThreads / 32);
-#define LAUNCH_AS(N)                                                                                  \
-  case N:                                                                                             \
-    CK(cudaFuncSetAttribute(k_cd_as<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_as));   \
-    k_cd_as<N><<<gas, kAsThreads, smem_as, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,           \
-                                                    c.cd_max_sweeps, A64, A32, h->sweeps_dev,         \
-                                                    want_cpart ? h->AT32 : nullptr, h->kp);           \
-    break;
+    // CD with exact support jumps (cd_as.cuh), 4 columns per CTA (1 with a Gram per column)
+    const int tas = gstride > 0 ? 32 : kAsThreads;
+    const int gas = (int)ceil_div(m, tas / 32);
+#define LAUNCH_AS(N, GT)                                                                               \
+  {                                                                                                    \
+    CK(cudaFuncSetAttribute(k_cd_as<N, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_as)); \
+    k_cd_as<N, GT><<<gas, tas, smem_as, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,              \
+                                                 c.cd_max_sweeps, A64, A32, h->sweeps_dev,            \
+                                                 want_cpart ? h->AT32 : nullptr, h->kp, gstride);     \
+  }
+#define CASE_AS(N) \
+  case N: if (g64) LAUNCH_AS(N, double) else LAUNCH_AS(N, float) break;
     switch (kpl) {
-      LAUNCH_AS(1) LAUNCH_AS(2) LAUNCH_AS(3) LAUNCH_AS(4)
-      LAUNCH_AS(5) LAUNCH_AS(6) LAUNCH_AS(7) LAUNCH_AS(8)
+      CASE_AS(1) CASE_AS(2) CASE_AS(3) CASE_AS(4)
+      CASE_AS(5) CASE_AS(6) CASE_AS(7) CASE_AS(8)
       default: set_err(h, "k too large for the CD kernel"); return SOMF_E_ARG;
     }
+#undef CASE_AS
 #undef LAUNCH_AS
     CKL();
     h->kern[1] = 2;
     return SOMF_OK;
   }
-#define LAUNCH_CD(N)                                                                      \
-  case N:                                                                                 \
-    CK(cudaFuncSetAttribute(k_cd<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_cd<N><<<grid, kSolveThreads, smem, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,   \
-                                                  c.cd_max_sweeps, A64, A32, h->sweeps_dev,  \
-                                                  want_cpart ? h->AT32 : nullptr, h->kp);    \
-    break;
+  const bool g64cd = np * sizeof(double) <= 200 * 1024;
+  const size_t smem_cd = np * (g64cd ? sizeof(double) : sizeof(float));
+#define LAUNCH_CD(N, GT)                                                                      \
+  {                                                                                           \
+    CK(cudaFuncSetAttribute(k_cd<N, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cd)); \
+    k_cd<N, GT><<<gstride > 0 ? m : grid, gstride > 0 ? 32 : kSolveThreads, smem_cd, h->st>>>( \
+        G, beta, k, m, l1, l2, c.pos_code, tol, c.cd_max_sweeps, A64, A32, h->sweeps_dev,     \
+        want_cpart ? h->AT32 : nullptr, h->kp, gstride);                                     \
+  }
+#define CASE_CD(N) \
+  case N: if (g64cd) LAUNCH_CD(N, double) else LAUNCH_CD(N, float) break;
   switch (kpl) {
-    LAUNCH_CD(1) LAUNCH_CD(2) LAUNCH_CD(3) LAUNCH_CD(4)
-    LAUNCH_CD(5) LAUNCH_CD(6) LAUNCH_CD(7) LAUNCH_CD(8)
+    CASE_CD(1) CASE_CD(2) CASE_CD(3) CASE_CD(4)
+    CASE_CD(5) CASE_CD(6) CASE_CD(7) CASE_CD(8)
     default: set_err(h, "k too large for the CD kernel"); return SOMF_E_ARG;
   }
+#undef CASE_CD
 #undef LAUNCH_CD
   CKL();
   h->kern[1] = 3;
@@ -720,55 +766,66 @@ static const NtVariant kNtVariants[] = {{16, somf_nt_kernel_16}, {32, somf_nt_ke
 static void choose_newton(somf_ctx* h) {
   const int k = h->cfg.k;
   const int cap = (int)ceil_div(h->q_cap, h->nsm);
-  // groups of T = 4 threads own M = 2 masked rows (8 threads at KPT = 128)
-  const int T = 4, M = 2;
   const int gen = h->cfg.mu > 0.0 || h->cfg.pos_dict;
-  const int max_thr = NtCfg<4, 2>::kThreads;
-  const int64_t groups = ceil_div(cap, M);
+  const int max_thr = NtCfg<1, 1>::kThreads;
   for (const NtVariant& v : kNtVariants) {
     if (v.kpt < k) continue;
-    // KPT = 128: 8 threads per group keep the residual at 2 x 16 registers
-    const int Tv = v.kpt > 96 ? 8 : T;
-    if (Tv * groups > max_thr) return;
-    // >= k threads: the per-atom statistics and threshold updates run one thread per atom
-    const int nthr = (int)std::max<int64_t>(ceil_div(std::max(64, k), 32) * 32, ceil_div((int64_t)Tv * groups, 32) * 32);
-    if (nthr > max_thr) return;
-    const void* fn = v.get(Tv, M, gen);
-    if (!fn) return;
-    const int LD = v.kpt + 1;
-    const int KT = v.kpt / Tv, KTS = (KT + 3) & ~3;
-    const size_t blk = ((size_t)(cap + 1) * LD + 3) & ~(size_t)3;
-    const size_t ct = (size_t)Tv * ((((size_t)v.kpt * KTS + 31) & ~(size_t)31) + 8);   // T x CTS (bcd_newton.cuh)
-    const int ct_in_w = ct <= blk;
-    const size_t H = std::max(1, nthr / k);
-    const size_t part = 5 * H * v.kpt;             // stats partials (words)
-    const int part_in_cpi = part <= (size_t)k * v.kpt;
-    const size_t base = ((size_t)4 * blk + (size_t)k * v.kpt + (ct_in_w ? 0 : ct) + (part_in_cpi ? 0 : part)) *
-                            sizeof(float) + (size_t)cap * sizeof(int) + 16;
-    // mask-bit scratch of the draw-ahead: one byte per Philox block of my slice
-    const int64_t nb = ((h->cfg.row_hi - 1) >> 2) - (h->cfg.row_lo >> 2) + 1;
-    const size_t mb_off = (base + 15) & ~(size_t)15;
-    const size_t smem = mb_off + (size_t)ceil_div(nb, h->nsm) + 16;
-    if (smem > 220 * 1024) return;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-      cudaGetLastError();
+    // (T threads, M rows) per group in order of preference: v6 one thread
+    // per row (no shuffles) when the rows fill >= 3 warps, v6 two threads per
+    // row, v5 4 x 2 (8 x 2 at KPT = 128)
+    const int cands[3][2] = {{1, 1}, {2, 1}, {v.kpt > 96 ? 8 : 4, 2}};
+    for (const auto& tm : cands) {
+      const int Tv = tm[0], M = tm[1];
+      if (Tv == 1 && (v.kpt > 96 || cap < 96)) continue;
+      const int64_t groups = ceil_div(cap, M);
+      if (Tv * groups > max_thr) continue;
+      // >= k threads: the per-atom statistics and threshold updates run one
+      // thread per atom; v6 launches the full 384 (the warps past the rows skip
+      // the recurrence but share the setup and the per-atom statistics)
+      const int nthr = M == 1 ? max_thr
+                              : (int)std::max<int64_t>(ceil_div(std::max(64, k), 32) * 32,
+                                                       ceil_div((int64_t)Tv * groups, 32) * 32);
+      if (nthr > max_thr) continue;
+      const void* fn = v.get(Tv, M, gen);
+      if (!fn) continue;
+      const int LD = v.kpt + 1;
+      const int KT = v.kpt / Tv, KTS = (KT + 3) & ~3;
+      const size_t blk = ((size_t)(cap + 1) * LD + 3) & ~(size_t)3;
+      const size_t ct = (size_t)Tv * ((((size_t)v.kpt * KTS + 31) & ~(size_t)31) + 8);   // T x CTS (bcd_newton.cuh)
+      const int ct_in_w = ct <= blk;
+      const size_t H = std::max(1, nthr / k);
+      const size_t part = 5 * H * v.kpt;             // stats partials (words)
+      const int part_in_cpi = part <= (size_t)k * v.kpt;
+      const size_t base = ((size_t)4 * blk + (size_t)k * v.kpt + (ct_in_w ? 0 : ct) + (part_in_cpi ? 0 : part)) *
+                              sizeof(float) + (size_t)cap * sizeof(int) + 16;
+      // mask-bit scratch of the draw-ahead: one byte per Philox block of my slice
+      const int64_t nb = ((h->cfg.row_hi - 1) >> 2) - (h->cfg.row_lo >> 2) + 1;
+      const size_t mb_off = (base + 15) & ~(size_t)15;
+      const size_t smem = mb_off + (size_t)ceil_div(nb, h->nsm) + 16;
+      if (smem > 220 * 1024) continue;
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, smem) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
+        continue;
+      }
+      h->nt_fn = fn;
+      h->nt_cap_rows = cap;
+      h->nt_kpt = v.kpt;
+      h->nt_T = Tv;
+      h->nt_M = M;
+      h->nt_smem = smem;
+      h->nt_threads = nthr;
+      h->nt_ct_in_w = ct_in_w;
+      h->nt_mbits_off = (int)mb_off;
+      if (h->cfg.bcd_lam_tol > 0.0) h->nt_lam_tol = h->cfg.bcd_lam_tol;
+      h->nt_part_in_cpi = part_in_cpi;
       return;
     }
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, smem) != cudaSuccess || occ < 1) {
-      cudaGetLastError();
-      return;
-    }
-    h->nt_fn = fn;
-    h->nt_cap_rows = cap;
-    h->nt_kpt = v.kpt;
-    h->nt_smem = smem;
-    h->nt_threads = nthr;
-    h->nt_ct_in_w = ct_in_w;
-    h->nt_mbits_off = (int)mb_off;
-    if (h->cfg.bcd_lam_tol > 0.0) h->nt_lam_tol = h->cfg.bcd_lam_tol;
-    h->nt_part_in_cpi = part_in_cpi;
-    return;
+    return;     // the smallest KPT >= k did not fit: no simultaneous-threshold kernel
   }
 }
 
@@ -928,14 +985,6 @@ static somf_status bcd_sharded(somf_ctx* h) {
   return SOMF_OK;
 }
 
-__global__ void k_init_accmm(unsigned* mm, int n) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) { mm[2 * i] = 0xffffffffu; mm[2 * i + 1] = 0u; }
-}
-static cudaError_t init_accmm(unsigned* mm, int n) {
-  k_init_accmm<<<(n + 255) / 256, 256>>>(mm, n);
-  return cudaGetLastError();
-}
 __global__ void k_init_nt_rec(unsigned long long* rec, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) nt_rec_reset(rec + (size_t)i * kNtRec);
@@ -956,6 +1005,7 @@ SOMF_EXPORT void somf_config_default(somf_config* c) {
   c->mu = 0.0;
   c->r = 1.0;
   c->u = 0.917;
+  c->v = 0.751;
   c->b_mode = SOMF_B_MASKED;
   c->cd_tol = 1e-7;
   c->cd_max_sweeps = 4000;
@@ -995,6 +1045,8 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   if (c.b_mode == SOMF_B_UNBIASED) return SOMF_E_UNSUPPORTED;
   if (c.bcd_kernel < 0 || c.bcd_kernel > 3) return SOMF_E_ARG;
   if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL) return SOMF_E_ARG;
+  if (c.estimator < 0 || c.estimator > 2) return SOMF_E_ARG;
+  if (c.estimator != 0 && (c.n_samples < 1 || !(c.v > 0.0 && c.v <= 1.0))) return SOMF_E_ARG;
   somf_ctx* h = new somf_ctx();
   h->cfg = c;
   h->rows = c.row_hi - c.row_lo;
@@ -1070,6 +1122,21 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->bcd_prof, 80));
   h->nt_ncopy = c.bcd_copies > 0 ? std::min(c.bcd_copies, kNtMaxCopies) : 8;
   A(dalloc(&h->nt_acc, (size_t)(kNtRing + 1) * h->nt_ncopy * k * kNtRec));
+  if (c.estimator != 0) {
+    const size_t n = (size_t)c.n_samples;
+    A(dalloc(&h->ids_dev, (size_t)c.eta));
+    A(dalloc(&h->est_cnt, n));
+    A(dalloc(&h->est_stamp, n));
+    A(dalloc(&h->est_bcache, n * k));
+    A(dalloc(&h->est_beta, (size_t)k * c.eta));
+    if (c.estimator == 1) {
+      A(dalloc(&h->est_gcache, n * k * k));
+      A(dalloc(&h->est_G, (size_t)c.eta * k * k));
+    } else {
+      A(dalloc(&h->Gex, (size_t)k * k));
+      A(dalloc(&h->gnew, (size_t)k * 4 + (size_t)k * k));
+    }
+  }
   if (c.bcd_kernel == 0 || c.bcd_kernel == 3) choose_newton(h);
   if (c.bcd_kernel == 0 ? !h->nt_fn : c.bcd_kernel == 2) choose_onchip(h);
   if ((c.bcd_kernel == 2 && !h->oc_fn) || (c.bcd_kernel == 3 && !h->nt_fn)) {
@@ -1110,7 +1177,9 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->partial, h->beta64, h->A64, h->A32, h->red, h->bar,
                   h->betae, h->Ae64, h->Ae32, h->colsq, h->objd, h->qfull_dev, h->Xstage,
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
-                  h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32};
+                  h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32,
+                  h->ids_dev, h->est_cnt, h->est_stamp, h->est_bcache, h->est_gcache, h->est_beta, h->est_G,
+                  h->Gex, h->gnew};
   if (h->st2) cudaStreamDestroy(h->st2);
   if (h->ev_codes) cudaEventDestroy(h->ev_codes);
   if (h->ev_comp) cudaEventDestroy(h->ev_comp);
@@ -1127,6 +1196,28 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
   for (auto& e : h->evs) { cudaEventDestroy(e.a); cudaEventDestroy(e.b); }
   for (auto e : h->pool) cudaEventDestroy(e);
   delete h;
+  return SOMF_OK;
+}
+
+// Estimators (b) / (c): forget every sample's statistics; (c): G = D^T D of
+// the current D (one contraction over all rows).
+static somf_status reset_estimator(somf_ctx* h) {
+  const somf_config& c = h->cfg;
+  if (c.estimator == 0) return SOMF_OK;
+  const int k = c.k;
+  const size_t n = (size_t)c.n_samples;
+  CK(cudaMemsetAsync(h->est_cnt, 0, n * sizeof(int), h->st));
+  CK(cudaMemsetAsync(h->est_stamp, 0xff, n * sizeof(int), h->st));
+  CK(cudaMemsetAsync(h->est_bcache, 0, n * k * sizeof(double), h->st));
+  if (c.estimator == 1) CK(cudaMemsetAsync(h->est_gcache, 0, n * k * k * sizeof(double), h->st));
+  if (c.estimator == 2) {
+    k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->qfull_dev, h->rows);
+    CKL();
+    if (somf_status s = launch_contract(h, false, false, h->qfull_dev, h->rows, h->D, h->kp, 4, 1.0, h->gnew,
+                                        h->Gex))
+      return s;
+    if (somf_status s = reduce(h, h->Gex, (int64_t)k * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
+  }
   return SOMF_OK;
 }
 
@@ -1155,6 +1246,7 @@ SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int6
   h->t_host = 0;
   h->mask_ready = h->begin_ready = h->ahead_ready = false;
   h->initialized = true;
+  if (somf_status s = reset_estimator(h)) return s;
   return post_call(h);
 }
 
@@ -1202,10 +1294,23 @@ static void swap_ahead(somf_ctx* h) {
   h->ahead_ready = false;
 }
 
-static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, bool compact) {
+static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, bool compact,
+                                    const int64_t* ids = nullptr) {
   const somf_config& c = h->cfg;
   const int k = c.k, eta = c.eta;
   if (!h->initialized) { set_err(h, "partial_fit before set_components / set_state"); return SOMF_E_STATE; }
+  if (c.estimator != 0 && !ids) {
+    set_err(h, "estimators (b) / (c) need the batch's sample ids: somf_partial_fit_ids");
+    return SOMF_E_STATE;
+  }
+  if (ids) {
+    // the batch's sample ids into device memory (host or device pointer)
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, ids) != cudaSuccess) cudaGetLastError();
+    const bool dev = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+    CK(cudaMemcpyAsync(h->ids_dev, ids, (size_t)eta * sizeof(int64_t),
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->st));
+  }
   if (ld < eta) { set_err(h, "ld < eta"); return SOMF_E_DIM; }
   bool host = false;
   const void* xs = nullptr;
@@ -1269,9 +1374,31 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   h->kern[2] = 4;
   h->kern[4] = 0;
+  const double* Gcodes = h->G64;
+  const double* bcodes = h->beta64;
+  int64_t gstride = 0;
+  if (c.estimator != 0) {
+    // estimators (b) / (c): per-sample averages of this step's masked estimates
+    PhaseScope ps(h, SOMF_PH_CODES);
+    k_est_average<<<eta, kEstThreads, 0, h->st>>>(h->ids_dev, c.n_samples, h->beta64, h->G64, k, eta, c.v,
+                                                  h->t_dev, h->est_cnt, h->est_stamp, h->est_bcache,
+                                                  h->est_gcache, h->est_beta, h->est_G, h->err_dev);
+    CKL();
+    h->launches[SOMF_PH_CODES] += 1;
+    bcodes = h->est_beta;
+    if (c.estimator == 1) {
+      Gcodes = h->est_G;                                                     // Eq. (b): a Gram per column
+      gstride = (int64_t)k * k;
+    } else {
+      Gcodes = h->Gex;                                                       // Eq. (c): D_{t-1}^T D_{t-1}
+    }
+  }
   {
     PhaseScope ps(h, SOMF_PH_CODES);                                         // Eq. somf_alpha
-    if (somf_status s = launch_codes(h, h->G64, h->beta64, eta, c.cd_tol, h->A64, h->A32, true)) return s;
+    // the tensor-core Bbar kernel folds Cbar from the fp64 codes itself: no
+    // per-CTA partials (nor the transposed fp32 codes) from the solver then
+    const bool cpart = bbar_tc_smem(h, Xd, ld) == 0;
+    if (somf_status s = launch_codes(h, Gcodes, bcodes, eta, c.cd_tol, h->A64, h->A32, cpart, gstride)) return s;
     h->launches[SOMF_PH_CODES] += 1;
   }
   bool cbar_folded = false;
@@ -1341,6 +1468,8 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
     h->kern[3] = h->reducer ? 4 : h->nt_fn ? 3 : h->oc_fn ? 2 : 1;
+    h->kern[5] = h->kern[3] == 3 ? h->nt_T : 0;
+    h->kern[6] = h->kern[3] == 3 ? h->nt_M : 0;
     if (h->reducer) {
       if (somf_status s = bcd_sharded(h)) return s;
     } else if (h->nt_fn) {
@@ -1441,6 +1570,19 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     }
     h->launches[SOMF_PH_BCD] += 1;
   }
+  if (c.estimator == 2) {
+    // Eq. (c): the exact Gram follows Alg. 4's partial update of the rows S_t
+    PhaseScope ps(h, SOMF_PH_CONTRACT);
+    if (somf_status s = launch_contract(h, true, false, h->q_dev, q_est, h->D, h->kp, 4, 1.0, h->gnew,
+                                        h->gnew + (size_t)k * 4))
+      return s;
+    if (somf_status s = reduce(h, h->gnew + (size_t)k * 4, (int64_t)k * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
+    k_gex_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->Gex, h->G64,
+                                                                            h->gnew + (size_t)k * 4, k * k,
+                                                                            1.0 / c.r);
+    CKL();
+    h->launches[SOMF_PH_CONTRACT] += h->ct_launches + 1;
+  }
   if (h->comp_pending) {
     // the caller's stream sees the complete Bbar when the call's work is done
     CK(cudaStreamWaitEvent(h->st, h->ev_comp, 0));
@@ -1453,6 +1595,11 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
 SOMF_EXPORT somf_status somf_partial_fit(somf_handle h, const float* X, int64_t ld) {
   if (!h || !X) return SOMF_E_ARG;
   return partial_fit_impl(h, X, ld, false);
+}
+
+SOMF_EXPORT somf_status somf_partial_fit_ids(somf_handle h, const float* X, int64_t ld, const int64_t* ids) {
+  if (!h || !X || !ids) return SOMF_E_ARG;
+  return partial_fit_impl(h, X, ld, false, ids);
 }
 
 SOMF_EXPORT somf_status somf_next_mask(somf_handle h, int64_t* q_out, int32_t* idx_out) {
@@ -1610,6 +1757,7 @@ SOMF_EXPORT somf_status somf_set_state(somf_handle h, const float* D, const floa
   h->t_host = t;
   h->mask_ready = h->begin_ready = h->ahead_ready = false;
   h->initialized = true;
+  if (somf_status s = reset_estimator(h)) return s;
   return post_call(h);
 }
 
@@ -1646,7 +1794,7 @@ SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->nt_fn ? 3 :
 
 SOMF_EXPORT somf_status somf_last_kernels(somf_handle h, int32_t* out) {
   if (!h || !out) return SOMF_E_ARG;
-  for (int i = 0; i < 5; ++i) out[i] = h->kern[i];
+  for (int i = 0; i < 7; ++i) out[i] = h->kern[i];
   return SOMF_OK;
 }
 

@@ -91,7 +91,8 @@ class Somf:
                  seed: int = 0, row_lo: int = 0, row_hi: int = 0, device: int = 0,
                  stream=None, debug: bool = False, bcd_kernel: str = "auto",
                  contract_kernel: str = "auto", bbar_kernel: str = "auto", codes_kernel: str = "auto",
-                 bcd_lam_tol: float = 0.0, bcd_copies: int = 0):
+                 bcd_lam_tol: float = 0.0, bcd_copies: int = 0,
+                 estimator: str = "a", n_samples: int = 0, v: float = 0.751):
         L = lib()
         cfg = _lib.SomfConfig()
         L.somf_config_default(C.byref(cfg))
@@ -116,6 +117,9 @@ class Somf:
         cfg.codes_kernel = CODES_KERNELS[codes_kernel]
         cfg.bcd_lam_tol = bcd_lam_tol
         cfg.bcd_copies = bcd_copies
+        cfg.estimator = {"a": 0, "b": 1, "c": 2}[estimator]
+        cfg.n_samples = n_samples
+        cfg.v = v
         h = C.c_void_p()
         st = L.somf_create(C.byref(cfg), C.byref(h))
         if st != 0:
@@ -154,6 +158,22 @@ class Somf:
         if X.shape[1] != self.eta:
             raise ValueError("X must have eta columns")
         _check(lib().somf_partial_fit(self._h, C.c_void_p(X.data_ptr()), X.stride(0)), self._h)
+
+    def partial_fit_ids(self, X: torch.Tensor, ids):
+        """Estimators (b) / (c): X's columns are the samples ``ids`` (int64,
+        host array or CUDA tensor, distinct within the batch)."""
+        X = self._dev_f32(X, self.rows, "X")
+        if X.shape[1] != self.eta:
+            raise ValueError("X must have eta columns")
+        if isinstance(ids, torch.Tensor):
+            ids_t = ids.to(torch.int64).contiguous()
+            ptr = C.c_void_p(ids_t.data_ptr())
+        else:
+            ids_t = np.ascontiguousarray(ids, dtype=np.int64)
+            ptr = ids_t.ctypes.data_as(C.c_void_p)
+        if ids_t.shape[0] != self.eta:
+            raise ValueError("ids must hold eta sample ids")
+        _check(lib().somf_partial_fit_ids(self._h, C.c_void_p(X.data_ptr()), X.stride(0), ptr), self._h)
 
     def next_mask(self, want_indices: bool = True):
         q = C.c_int64()
@@ -271,13 +291,13 @@ class Somf:
     def last_kernels(self):
         """Kernel variants of the last partial_fit (somf_last_kernels): names
         as in CONTRACT_KERNELS / CODES_KERNELS / BBAR_KERNELS."""
-        v = np.zeros(5, np.int32)
+        v = np.zeros(7, np.int32)
         _check(lib().somf_last_kernels(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
         inv = lambda d, x: {i: n for n, i in d.items()}.get(int(x), "none")  # noqa: E731
         return dict(contract=inv(CONTRACT_KERNELS, v[0]), codes=inv(CODES_KERNELS, v[1]),
                     bbar=inv(BBAR_KERNELS, v[2]),
                     bcd={1: "global", 2: "onchip", 3: "newton", 4: "sharded"}.get(int(v[3]), "none"),
-                    bbar_complement=bool(v[4]))
+                    bbar_complement=bool(v[4]), bcd_group=(int(v[5]), int(v[6])))
 
     def last_step_info(self):
         q, nred, w = C.c_int64(), C.c_int64(), C.c_double()

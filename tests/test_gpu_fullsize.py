@@ -298,7 +298,7 @@ def test_bcd_bitwise_deterministic(somf, bcd_kernel):
 # ---------------------------------------------------------------------------
 def test_recurring_empty_masks(somf):
     p, k, eta = 64, 4, 5
-    kw = dict(lam=0.1, nu=1.0, mu=0.0, r=32.0)
+    kw = dict(lam=0.1, nu=1.0, mu=0.0, r=64.0)       # P(S_t empty) = (63/64)^64 ~ 0.37
     X = f32(synth.tiny_dictionary_learning(p=p, n=k + 40 * eta, seed=2)[0])
     ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=1, **kw))
     ora.set_components(X[:, :k])
@@ -318,7 +318,7 @@ def test_recurring_empty_masks(somf):
                                             st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
     assert n_empty >= 5
     q, idx = gpu.next_mask()
-    assert np.array_equal(idx, ostreams.mask_rows(1, ora.t + 1, p, 32.0))
+    assert np.array_equal(idx, ostreams.mask_rows(1, ora.t + 1, p, 64.0))
 
 
 # ---------------------------------------------------------------------------
@@ -375,3 +375,89 @@ def test_trajectory_1000_steps_drift(somf):
     Xte = X[:, -200:]
     f_ref, f_gpu = ora.objective(Xte), gpu.objective(cuda(Xte))
     assert abs(f_gpu - f_ref) <= TOL_OBJ * abs(f_ref), (f_gpu, f_ref)
+
+
+# ---------------------------------------------------------------------------
+# estimators (b) and (c) (Eq. b, Eq. c)
+# ---------------------------------------------------------------------------
+EST_CASES = {
+    "ridge_l1": (3000, 24, 40, dict(lam=1e-3, nu=1.0, mu=0.0, r=12.0), "fmri"),
+    "lasso_l2": (1536, 40, 32, dict(lam=0.1, nu=0.0, mu=1.0, r=4.0), "hyper"),
+    "nmf": (2048, 48, 48, dict(lam=0.05, nu=1.0, pos_code=True, mu=1.0, pos_dict=True, r=8.0), "nmf"),
+}
+
+
+@pytest.mark.parametrize("estimator", ["b", "c"])
+@pytest.mark.parametrize("name", list(EST_CASES))
+def test_estimator_steps(somf, name, estimator):
+    """12 steps over a pool of 3 eta columns (every sample revisited 4 times,
+    gamma_c = c^-v): codes each step, the state after each step."""
+    p, k, eta, kw, kind = EST_CASES[name]
+    n = 3 * eta
+    X = _vdata(kind, p, k + n)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=4, estimator=estimator, n_samples=n, **kw))
+    ora.set_components(X[:, :k])
+    gpu = somf.Somf(p, k, eta, seed=4, debug=True, estimator=estimator, n_samples=n, **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    Xg = cuda(X[:, k:])
+    rng = np.random.default_rng(3)
+    for t in range(12):
+        ids = rng.permutation(n)[:eta] if t % 3 == 0 else np.arange((t % 3) * eta, (t % 3 + 1) * eta)
+        out = ora.partial_fit(X[:, k + ids], ids)
+        gpu.partial_fit_ids(Xg[:, torch.tensor(ids, device="cuda")].contiguous(), ids)
+        A = gpu.get_codes().cpu().numpy()
+        st = gpu.get_state()
+        errs = dict(alpha=rel(A, out["A"]), Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar),
+                    D=rel(st["D"], ora.D))
+        assert all(v <= TOL_STEP for v in errs.values()), (t, errs)
+        # continue from the GPU's float32 iterate (the per-sample caches are
+        # the GPU's own: each step pins the cache recursion over t steps)
+        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
+                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
+        if estimator == "c":
+            ora.G_exact = ora.D.T @ ora.D
+
+
+def test_estimator_repeated_id_rejected(somf):
+    p, k, eta, kw, kind = EST_CASES["ridge_l1"]
+    X = _vdata(kind, p, k + eta)
+    gpu = somf.Somf(p, k, eta, seed=4, estimator="c", n_samples=100, **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    ids = np.arange(eta)
+    ids[3] = ids[5]
+    gpu.partial_fit_ids(cuda(X[:, k:k + eta]), ids)
+    with pytest.raises(somf.SomfError):
+        gpu.get_state()
+
+
+# ---------------------------------------------------------------------------
+# time-to-1 % sweep harness (bench.py --sweeps; SURVEY §8(f) row 4)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("estimator,r", [("c", 1.0), ("c", 12.0), ("b", 4.0), ("a", 12.0)])
+def test_sweep_curve_matches_oracle(somf, estimator, r):
+    """The convergence curve the sweep reports (held-out objective at
+    checkpoints of a randomly cycled finite data set) vs the oracle on the
+    same ids: every checkpoint within 1e-3 relative."""
+    import bench
+    p, k, eta, n, iters, every = 3000, 24, 40, 400, 60, 15
+    X, _, _ = synth.fmri_matrix(shape=(20, 20, 20), p=p, k=16, n_records=1, T=1200, seed=8)
+    X = f32(X)
+    Xd, Xte, D0 = X[:, :n], X[:, n:n + 200], X[:, n + 200:n + 200 + k]
+    kw = dict(lam=1e-3, nu=1.0, mu=0.0, r=r, u=0.917)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=0, estimator=estimator,
+                                  n_samples=n if estimator != "a" else 0, **kw))
+    ora.set_components(D0)
+    ref = [ora.objective(Xte)]
+    for t in range(iters):
+        ids = ostreams.column_ids(11, n, t * eta, eta)
+        ora.partial_fit(Xd[:, ids], ids if estimator != "a" else None)
+        if (t + 1) % every == 0:
+            ref.append(ora.objective(Xte))
+    gpu = somf.Somf(p, k, eta, seed=0, estimator=estimator, n_samples=n if estimator != "a" else 0, **kw)
+    gpu.set_components(cuda(D0))
+    curve = bench.convergence_curve(gpu, cuda(Xd), lambda t: somf.column_ids(11, n, t * eta, eta), iters, every,
+                                    cuda(Xte), torch.cuda.current_stream(), use_ids=estimator != "a")
+    got = [f for _, _, f in curve]
+    assert len(got) == len(ref)
+    for a, b in zip(got, ref):
+        assert abs(a - b) <= TOL_OBJ * abs(b), (got, ref)
