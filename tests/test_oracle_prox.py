@@ -257,3 +257,28 @@ def test_codes_match_sklearn_elastic_net():
                         max_iter=200000, positive=positive)
         en.fit(D, x)
         np.testing.assert_allclose(a, en.coef_, atol=1e-7)
+
+
+def test_codes_ill_conditioned_nonneg_reach_the_minimiser():
+    """NMF-shaped Gram (cfgD: correlated nonnegative atoms, cond ~1e3-1e4):
+    plain CD stalls far from the minimiser at its sweep cap, so the oracle's
+    answer (reading R14b) is checked against the KKT conditions and against
+    scipy's NNLS (Lawson-Hanson) on the equivalent least-squares problem
+    min 1/2 |L^T a - L^-1 beta|^2, a >= 0, with L L^T = G + lam I."""
+    from scipy.optimize import nnls
+    rng = np.random.default_rng(12)
+    p, k = 1500, 64
+    W = np.abs(rng.standard_normal((p, 40))) * (rng.random((p, 40)) < 0.3)
+    X = W @ rng.exponential(1.0, (40, k + 6)) + np.abs(0.1 * rng.standard_normal((p, k + 6)))
+    D = X[:, :k] / np.linalg.norm(X[:, :k], axis=0)    # atoms = data columns (bench D0)
+    X = X[:, k:]
+    G, beta = 8.0 * D.T @ D, 8.0 * D.T @ X
+    lam = 0.05
+    ev = np.linalg.eigvalsh(G + lam * np.eye(k))
+    assert ev[-1] / ev[0] > 1e3                       # the hard regime
+    a = solve_codes(G, beta, lam, 1.0, positive=True, max_sweeps=40)   # CD alone stalls here
+    L = np.linalg.cholesky(G + lam * np.eye(k))
+    for s in range(beta.shape[1]):
+        assert _kkt_residual(G, beta[:, s], a[:, s], lam, 1.0, True) < 1e-8
+        ref, _ = nnls(L.T, np.linalg.solve(L, beta[:, s]))
+        np.testing.assert_allclose(a[:, s], ref, atol=1e-7 * max(1.0, np.abs(ref).max()))
