@@ -143,6 +143,45 @@ class NmfStreamGPU:
         return (self.W @ H + N).contiguous()
 
 
+class FmriEStreamGPU:
+    """cfgE stand-in on the GPU (harness only): the cfgC recipe
+    on a 126 x 160 x 100 grid masked to 2,000,000 voxels (synth.fmri_voxel_grid)
+    with 256 truncated Gaussian blobs (centres uniform over the voxels, sigma ~
+    U[2, 6], cut at 3 sigma, unit l2; built on the GPU: a dense float64 D* on
+    the host would be 4 GB), AR(1) rho = 0.8 codes (synth.fmri_codes), SNR 0.5."""
+
+    def __init__(self, eta: int, seed: int, device, k_true: int = 256, p: int = 2_000_000):
+        import torch
+        import synth
+        coords = torch.tensor(synth.fmri_voxel_grid((126, 160, 100), p), dtype=torch.float32, device=device)
+        self.p = coords.shape[0]
+        rng = np.random.default_rng(seed)
+        D = torch.zeros((self.p, k_true), dtype=torch.float32, device=device)
+        for j in range(k_true):
+            c = coords[int(rng.integers(self.p))]
+            sg = float(rng.uniform(2.0, 6.0))
+            d2 = ((coords - c) ** 2).sum(dim=1)
+            v = torch.exp(-d2 / (2.0 * sg * sg))
+            v[d2 > (3.0 * sg) ** 2] = 0.0
+            D[:, j] = v / v.norm()
+        self.Dstar = D
+        self.A = torch.tensor(synth.fmri_codes(k_true, 1, T=4096, seed=seed + 1), dtype=torch.float32,
+                              device=device)
+        self.g = torch.Generator(device=device)
+        self.g.manual_seed(seed + 2)
+        self.sigma = float(np.sqrt(k_true / self.p / 0.5))
+        self.eta, self.device, self.c0 = eta, device, 0
+
+    def batch(self, m: int | None = None):
+        import torch
+        m = m or self.eta
+        c0 = self.c0 % (self.A.shape[1] - m)
+        self.c0 += m
+        X = self.Dstar @ self.A[:, c0:c0 + m]
+        X += self.sigma * torch.randn(X.shape, generator=self.g, device=self.device)
+        return X.contiguous()
+
+
 def fmri_inputs_gpu(n_batches: int, eta: int, k: int, seed: int, device):
     """(list of p x eta float32 CUDA batches, D0 p x k) of FmriStreamGPU."""
     s = FmriStreamGPU(n_batches, eta, k, seed, device)
@@ -175,6 +214,17 @@ def phase_cost(phase: str, q: float, p: int, k: int, eta: int):
 def step_bytes(q: float, k: int, eta: int):
     """4q(4k + eta) + 8q bytes per iteration (masked modes)."""
     return 4 * q * (4 * k + eta) + 8 * q
+
+
+def step_roofline_us(q: float, k: int, eta: int, peaks: dict) -> float:
+    """SURVEY §8(d) step roofline: the slower of the algorithmic bytes over HBM
+    and the contractions on the tensor pipe (3xTF32: 3 x (4 q k eta + q k^2)
+    at the TF32 rate = measured bf16 / 2) plus the BCD recurrence on FFMA
+    (2 q k^2 + 10 q k at the fp32 CUDA-core peak)."""
+    t_hbm = step_bytes(q, k, eta) / (peaks["hbm"] * 1e9)
+    t_tc = 3.0 * (4 * q * k * eta + q * k * k) / (peaks["bf16"] / 2.0 * 1e12)
+    t_fma = (2 * q * k * k + 10 * q * k) / (alu_peak_tflops(peaks["sm_max_mhz"], fp64=False) * 1e12)
+    return 1e6 * max(t_hbm, t_tc + t_fma)
 
 
 def measured_peaks():
@@ -509,8 +559,10 @@ def run_somf(args):
         roof["bcd_frozen_prefix_per_round"] = [round(f / bcd_cyc["launches"], 2)
                                                for f in bcd_cyc["frozen_prefix_per_round"][:len(unc)]]
     sb = step_bytes(q, k, eta)
+    roof_us = step_roofline_us(q, k, eta, peaks)
     step_roof = {"bytes_per_step": sb, "achieved_gbs": sb / (step_ms * 1e-3) / 1e9,
-                 "frac_of_hbm": sb / (step_ms * 1e-3) / 1e9 / peaks["hbm"]}
+                 "frac_of_hbm": sb / (step_ms * 1e-3) / 1e9 / peaks["hbm"],
+                 "roofline_us": roof_us, "frac": roof_us / (step_ms * 1e3)}
 
     # --- end-to-end through the C ABI with host buffers ----------------------
     e2e = None
@@ -551,6 +603,8 @@ def run_somf(args):
             t3 = time_steps(m3, batches, 3, 5, flush, stream)
             sm = sum(t3) / len(t3)
             sweep[f"r={int(rr)}"] = {"columns_per_s": eta / (sm * 1e-3), "ms_per_step": sm,
+                                     "roofline_us": step_roofline_us(p / rr, k, eta, measured_peaks()),
+                                     "roofline_frac": step_roofline_us(p / rr, k, eta, measured_peaks()) / (sm * 1e3),
                                      "bcd_kernel": m3.bcd_variant,
                                      "bcd_grid_reductions": m3.last_step_info()["bcd_reductions"]}
             del m3
@@ -576,7 +630,9 @@ def run_somf(args):
         specs = [("cfgB-hyperspectral", HyperspectralStreamGPU, 256, 256,
                   dict(lam=0.1, nu=0.0, mu=1.0, pos_code=False, pos_dict=False), (1.0, 4.0, 12.0)),
                  ("cfgD-nmf", NmfStreamGPU, 128, 512,
-                  dict(lam=0.05, nu=1.0, mu=1.0, pos_code=True, pos_dict=True), (8.0,))]
+                  dict(lam=0.05, nu=1.0, mu=1.0, pos_code=True, pos_dict=True), (8.0,)),
+                 ("cfgE-fmri2M", FmriEStreamGPU, 256, 512,
+                  dict(lam=0.05, nu=0.0, mu=0.5, pos_code=False, pos_dict=False), (24.0, 12.0, 4.0))]
         for name, gen_cls, kk, ee, kw, rs in specs:
             gen = gen_cls(ee, seed=0, device=dev)
             pool = [gen.batch() for _ in range(8)]
@@ -596,7 +652,9 @@ def run_somf(args):
                 time_steps(m4, pool, 15, 3, flush, stream)
                 pr4 = m4.profile_read()
                 m4.profile_enable(False)
+                roof4 = step_roofline_us(gen.p / rr, kk, ee, measured_peaks())
                 res[f"r={int(rr)}"] = {"columns_per_s": ee / (sm4 * 1e-3), "ms_per_step": sm4,
+                                       "roofline_us": roof4, "roofline_frac": roof4 / (sm4 * 1e3),
                                        "bcd_kernel": m4.bcd_variant,
                                        "bcd_grid_reductions": info4["bcd_reductions"], "q": info4["q"],
                                        "phase_ms_per_step": {ph: v / max(pr4["steps"], 1)

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SOMF_ABI_VERSION 2
+#define SOMF_ABI_VERSION 3
 
 typedef struct somf_ctx* somf_handle;
 
@@ -92,9 +92,12 @@ typedef struct somf_config {
   int32_t debug;          /* 1: synchronise and check after every call          */
   int32_t bcd_kernel;     /* Alg. 4 kernel: 0 = auto (simultaneous-threshold
                              when k <= 128 and the masked rows fit on chip, else
-                             on-chip per-atom, else global), 1 = global-memory
+                             kernel 4, else on-chip per-atom, else global), 1 = global-memory
                              per-atom kernel, 2 = on-chip per-atom kernel,
-                             3 = simultaneous-threshold kernel
+                             3 = simultaneous-threshold kernel (k <= 128, rows
+                             on chip), 4 = simultaneous-threshold kernel for
+                             k <= 256 with streamed Cbar chunks and streamed
+                             row tiles (auto picks it when 3 does not fit)
                              (SOMF_E_UNSUPPORTED at create if it cannot fit)   */
   /* Kernel selection of the other phases (0 = auto everywhere).  Every value
    * computes the same step (parity tests force each one); a forced variant
@@ -130,6 +133,11 @@ typedef struct somf_config {
   int64_t n_samples;      /* n: sample ids of the stream lie in [0, n)        */
   double v;               /* gamma_c = c^-v of the per-sample averages,
                              v in (0, 1] (0.751 in P:1361)        */
+  int32_t bcd_tile_rows;  /* bcd_kernel 4 (k <= 256 / streamed rows): masked
+                             rows per on-chip tile (0 = as many as fit); a
+                             CTA with more rows streams its tiles from an
+                             L2 / HBM scratch every round.  Performance /
+                             test knob only: the result does not depend on it */
 } somf_config;
 
 /* Fills *cfg with defaults: u = 0.917, r = 1, nu = 1, mu = 0,

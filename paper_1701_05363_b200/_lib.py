@@ -23,6 +23,7 @@ def _sources():
 
 
 NT_KPTS = (16, 32, 48, 64, 72, 80, 96, 128)   # bcd_newton_inst.cu variants (one object each)
+NB_KPTS = (72, 128, 192, 256)                  # bcd_big_inst.cu variants
 
 
 def _units():
@@ -31,6 +32,7 @@ def _units():
              ("bcd_onchip_inst", os.path.join(CSRC, "bcd_onchip_inst.cu"), [])]
     units += [(f"bcd_newton_k{k}", os.path.join(CSRC, "bcd_newton_inst.cu"), [f"-DNT_KPT={k}"])
               for k in NT_KPTS]
+    units += [(f"bcd_big_k{k}", os.path.join(CSRC, "bcd_big_inst.cu"), [f"-DNB_KPT={k}"]) for k in NB_KPTS]
     return units
 
 
@@ -94,6 +96,7 @@ class SomfConfig(C.Structure):
         ("contract_kernel", C.c_int32), ("bbar_kernel", C.c_int32), ("codes_kernel", C.c_int32),
         ("bcd_lam_tol", C.c_double), ("bcd_copies", C.c_int32),
         ("estimator", C.c_int32), ("n_samples", C.c_int64), ("v", C.c_double),
+        ("bcd_tile_rows", C.c_int32),
     ]
 
 

@@ -1,0 +1,632 @@
+// bcd_big.cuh -- (a4) Alg. 4 with all k projection thresholds
+// solved SIMULTANEOUSLY (the rounds of bcd_newton.cuh) for the shapes the
+// on-chip kernel does not cover:
+//   * k up to 256 (cfgB hyperspectral, cfgE): the prescaled Cbar rows in pi
+//     order (256 KB at k = 256) no longer fit shared memory next to the rows,
+//     so they stream from L2 in chunks of CH positions (cp.async, double
+//     buffered, one CTA barrier per chunk);
+//   * masked rows that do not fit on chip (cfgC r <= 4, cfgE on one GPU):
+//     every CTA walks its rows in tiles of TR rows; the tile's d_old and its
+//     prescaled initial residual (pi order) are written once to an L2/HBM
+//     scratch at setup and re-read every round (they do not change over the
+//     rounds), the per-atom statistics are accumulated over the tiles in a
+//     fixed order, and the final D is written by one more pass with the
+//     converged thresholds.
+// Round structure, convergence test and the deterministic fixed-point grid
+// sums are the ones of k_bcd_newton (shared helpers in bcd_newton.cuh).
+#pragma once
+#include "bcd_newton.cuh"
+
+namespace somf {
+
+constexpr int kNbMaxK = 256;
+constexpr int kNbThreads = 384;
+
+// prescaled Cbar rows per thread parity: row PP of Ctg holds, for each parity
+// t < T, the KTS values c_{PP, iT+t} / c_{iT+t, iT+t} (i < KT, zero padded) at
+// stride CSTR floats (CSTR = 4 mod 8: the 16-byte loads of 8 consecutive
+// parities hit disjoint banks)
+__host__ __device__ constexpr int nb_kts(int kpt, int t) { return ((kpt / t) + 3) & ~3; }
+__host__ __device__ constexpr int nb_cstr(int kpt, int t) { return (nb_kts(kpt, t) % 8 == 0) ? nb_kts(kpt, t) + 4 : nb_kts(kpt, t); }
+
+struct NbArgs {
+  NtArgs nt;                // thresholds, records, barrier, draw-ahead (perm read from nt.perm)
+  const float* Cpi;         // k x KPT: Cbar in pi order (row p = atom pi(p)), zero padded
+  const float* Ctg;         // KPT x T x CSTR: prescaled Cbar rows per parity (k_nb_prep)
+  const float* invc;        // KPT: 1 / c_pp in pi order (0 for dead atoms)
+  float* scr;               // streamed tiles: per masked row 2 x KPT floats (d_old | R0), pi order
+  int tile_rows;            // TR: rows per tile (rows of a CTA beyond TR => streamed)
+  int ch;                   // positions per Cbar chunk (== KPT: resident)
+};
+
+// pi in the device array, Cbar permuted (k x KPT) and prescaled per parity
+// (KPT x T x CSTR), 1/c_pp; one CTA per position row.  Dead atoms (R10) get
+// 1/c = 0 (their residual is zero, so d stays d_old).
+struct NbPerm { int32_t v[kNbMaxK]; };
+static __global__ void k_nb_prep(NbPerm pi, int k, int kpt, int T, const float* __restrict__ C32,
+                          const double* __restrict__ C64, int32_t* __restrict__ perm, float* __restrict__ Cpi,
+                          float* __restrict__ Ctg, float* __restrict__ invc) {
+  const int p = blockIdx.x;                    // position (row of Cpi / Ctg)
+  const int kt = kpt / T, kts = nb_kts(kpt, T), cstr = nb_cstr(kpt, T);
+  __shared__ double dmax_s;
+  __shared__ float inv_s[kNbMaxK];
+  if (threadIdx.x < 32) {
+    double dm = 1.0;
+    for (int j = threadIdx.x; j < k; j += 32) dm = fmax(dm, C64[(int64_t)j * k + j]);
+    dm = warp_max(dm);
+    if (threadIdx.x == 0) dmax_s = dm;
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < kpt; l += blockDim.x) {
+    float iv = 0.f;
+    if (l < k) {
+      const double c = C64[(int64_t)pi.v[l] * k + pi.v[l]];
+      iv = c > 1e-12 * dmax_s ? (float)(1.0 / c) : 0.f;
+    }
+    inv_s[l] = iv;
+  }
+  __syncthreads();
+  if (p == 0)
+    for (int l = threadIdx.x; l < kpt; l += blockDim.x) {
+      if (l < k) perm[l] = pi.v[l];
+      invc[l] = inv_s[l];
+    }
+  const int jp = p < k ? pi.v[p] : 0;
+  for (int l = threadIdx.x; l < kpt; l += blockDim.x)
+    Cpi[(int64_t)p * kpt + l] = (p < k && l < k) ? C32[(int64_t)jp * k + pi.v[l]] : 0.f;
+  for (int e = threadIdx.x; e < T * cstr; e += blockDim.x) {
+    const int t = e / cstr, i = e % cstr;
+    const int l = i * T + t;
+    float v = 0.f;
+    if (p < k && i < kt && i < kts && l < k) v = C32[(int64_t)jp * k + pi.v[l]] * inv_s[l];
+    Ctg[(int64_t)p * T * cstr + e] = v;
+  }
+}
+
+__device__ __forceinline__ void nb_cp16(void* dst, const void* src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+
+// The recurrence of one tile (v5 layout: a group of T lanes owns M rows; R and
+// d_old in registers), with the prescaled Cbar rows either resident (CH =
+// KPT) or streamed in double-buffered chunks of CH positions (one CTA barrier
+// per chunk: every thread of the CTA runs this, rows past the tile on the
+// spare zero row).
+template <int KPT, int T, int M, bool kGen, int CH, int PP, int END>
+struct NbRec {
+  static constexpr int KT = KPT / T;
+  static constexpr int KTS = nb_kts(KPT, T);
+  static constexpr int CSTR = nb_cstr(KPT, T);
+  static constexpr int CHB = CH * T * CSTR;           // floats per chunk buffer
+  static __device__ __forceinline__ void run(float (&R)[M][KT], const float (&Do)[M][KT], int t, float* __restrict__ v0,
+                                             int vstride, float* __restrict__ cbuf, const float* __restrict__ Ctg,
+                                             const NtPar<kGen>* __restrict__ par) {
+    if constexpr (CH < KPT && PP % CH == 0) {
+      // chunk PP / CH is (being) loaded into buffer (PP / CH) & 1: wait for it;
+      // then every thread is past chunk PP / CH - 1, whose buffer takes the next
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+      if (PP + CH < KPT) {
+        float* dst = cbuf + (((PP / CH) + 1) & 1) * CHB;
+        const float* src = Ctg + (size_t)(PP + CH) * T * CSTR;
+        constexpr int n4 = CHB / 4;
+        for (int e = threadIdx.x; e < n4; e += blockDim.x) nb_cp16(dst + 4 * e, src + 4 * e);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+      }
+    }
+    constexpr int own = PP % T, ii = PP / T;
+    {
+      const NtPar<kGen> pr = par[PP];
+      float delta[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const float u = R[m][ii] + Do[m][ii];        // P:861 (valid in the owner)
+        const float v = pr.v_of(u);
+        const float d = pr.d_of(u);
+        if (t == own) v0[m * vstride + PP] = v;
+        delta[m] = __shfl_sync(0xffffffffu, d - Do[m][ii], own, T);
+      }
+      const float* crow = cbuf + ((PP / CH) & 1) * CHB + (PP % CH) * T * CSTR + t * CSTR;
+#pragma unroll
+      for (int j4 = ii / 4; j4 < KTS / 4; ++j4) {
+        const float4 c = *reinterpret_cast<const float4*>(crow + 4 * j4);
+        const float cc[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = 4 * j4 + e;
+          if (i < KT) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+              if (i > ii) {
+                R[m][i] = fmaf(-delta[m], cc[e], R[m][i]);
+              } else if (i == ii) {
+                const float up = fmaf(-delta[m], cc[e], R[m][i]);
+                R[m][i] = t > own ? up : R[m][i];
+              }
+            }
+          }
+        }
+      }
+    }
+    NbRec<KPT, T, M, kGen, CH, PP + 1, END>::run(R, Do, t, v0, vstride, cbuf, Ctg, par);
+  }
+};
+// (positions in runs of <= 128 template instantiations: nvcc's recursion limit)
+template <int KPT, int T, int M, bool kGen, int CH, int END>
+struct NbRec<KPT, T, M, kGen, CH, END, END> {
+  static __device__ __forceinline__ void run(float (&)[M][KPT / T], const float (&)[M][KPT / T], int, float*, int,
+                                             float*, const float*, const NtPar<kGen>*) {}
+};
+
+// shared-memory layout (floats unless noted), host mirror: nb_smem_bytes
+//   Dold, Rini, V   3 x (TR + 1) x LD     (LD = KPT + 1; row TR = spare zeros)
+//   cbuf            2 x CHB (streamed) or KPT x T x CSTR (resident)
+//   part            max(5 H KPT, 12 k) words (stats partials / record read)
+//   rows_s          TR ints; mbits: one byte per Philox block of my slice
+template <int KPT, int T>
+__host__ __device__ constexpr size_t nb_cbuf_floats(int ch) {
+  return ch >= KPT ? (size_t)KPT * T * nb_cstr(KPT, T) : (size_t)2 * ch * T * nb_cstr(KPT, T);
+}
+
+template <int KPT, int T, int M, bool kGen, int CH>
+__global__ void __launch_bounds__(kNbThreads, 1)
+k_bcd_big(NbArgs A) {
+  const NtArgs& P = A.nt;
+  constexpr int LD = KPT + 1;
+  constexpr int KT = KPT / T;
+  constexpr int CSTR = nb_cstr(KPT, T);
+  static_assert(KPT % T == 0 && M == 2, "groups of T lanes x 2 rows");
+  extern __shared__ __align__(16) float nb_smem[];
+  __shared__ __align__(16) NtPar<kGen> par_s[2][KPT];
+  __shared__ double lam_s[KPT], rho_s[KPT];
+  __shared__ double acc1_s[KPT], acc2_s[KPT];       // per-atom sums over my tiles (fixed order)
+  __shared__ unsigned acn_s[KPT], amn_s[KPT], amx_s[KPT];
+  __shared__ float vlo_s[KPT];
+  __shared__ int mode_s[KPT], jmap_s[KPT], pinv_s[KPT];
+  __shared__ int mcnt_s;
+  const int k = P.k, kp = P.kp;
+  const int nthr = blockDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x;
+  const int64_t q = *P.q_dev;
+  const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
+  const int nr_all = (int)(hi - lo);
+  const int TR = A.tile_rows;
+  const int ntile = nr_all > 0 ? (nr_all + TR - 1) / TR : 0;
+  const bool streamed = ntile > 1;
+  // host sizing errors (uniform over the CTAs: every CTA returns before any barrier)
+  if (T * ((TR + M - 1) / M) > nthr || nthr < k || ((q + G - 1) / G > TR && A.scr == nullptr)) {
+    if (tid == 0) atomicExch(P.err, 2);
+    return;
+  }
+  const size_t blk = ((size_t)(TR + 1) * LD + 3) & ~(size_t)3;
+  float* Dold = nb_smem;
+  float* Rini = Dold + blk;
+  float* V = Rini + blk;
+  float* cbuf = V + blk;
+  const size_t cbf = nb_cbuf_floats<KPT, T>(CH);
+  const int H = max(1, nthr / max(k, 1));
+  const size_t partw = (size_t)5 * H * KPT > (size_t)12 * k ? (size_t)5 * H * KPT : (size_t)12 * k;
+  unsigned* pcn = reinterpret_cast<unsigned*>(cbuf + cbf);
+  float* ps1 = reinterpret_cast<float*>(pcn + H * KPT);
+  float* ps2 = ps1 + H * KPT;
+  unsigned* pmn = reinterpret_cast<unsigned*>(ps2 + H * KPT);
+  unsigned* pmx = pmn + H * KPT;
+  int* rows_s = reinterpret_cast<int*>(cbuf + cbf + ((partw + 3) & ~(size_t)3));
+  uint8_t* mbits_s = reinterpret_cast<uint8_t*>(rows_s + ((TR + 3) & ~3));
+  const double a = P.a, b = P.b;
+  if (tid == 0) mcnt_s = 0;
+
+  // ---- setup: parameters, warm-start thresholds, M_{t+1} of my Philox slice --------
+  for (int p = tid; p < KPT; p += nthr) {
+    if (p < k) {
+      const int j = P.perm[p];
+      jmap_s[p] = j;
+      pinv_s[j] = p;
+      const bool dead = !(A.invc[p] > 0.f);                          // R10
+      const double lw = dead ? 0.0 : P.lam_ws[j];
+      lam_s[p] = lw;
+      rho_s[p] = P.nslack[j];
+      const int mode = dead ? kModeDead : (lw > 0.0 ? kModeShrink : kModeCopy);
+      mode_s[p] = mode;
+      vlo_s[p] = P.pos ? 0.f : -INFINITY;
+      par_s[0][p] = par_s[1][p] = nt_make_par<kGen>(mode, a, b, lw, vlo_s[p]);
+    } else {
+      jmap_s[p] = 0;
+      mode_s[p] = kModeDead;
+      lam_s[p] = 0.0;
+      rho_s[p] = 0.0;
+      vlo_s[p] = -INFINITY;
+      par_s[0][p] = par_s[1][p] = nt_make_par<kGen>(kModeDead, a, b, 0.0, -INFINITY);
+    }
+    acc1_s[p] = acc2_s[p] = 0.0;
+  }
+  // resident prescaled Cbar: staged once
+  if (CH >= KPT) {
+    const int n4 = (int)(cbf / 4);
+    for (int e = tid; e < n4; e += nthr) nb_cp16(cbuf + 4 * e, A.Ctg + 4 * e);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  int64_t mb0 = 0;
+  int nmb = 0;
+  if (P.idx_next) {
+    const int64_t b0 = P.row_lo >> 2, nb = ((P.row_hi - 1) >> 2) - b0 + 1;
+    mb0 = b0 + nb * blockIdx.x / G;
+    nmb = (int)(b0 + nb * (blockIdx.x + 1) / G - mb0);
+    int c = 0;
+    for (int i = tid; i < nmb; i += nthr) {
+      const uint32_t bits = mask_bits(P.seed, (uint64_t)P.tn, mb0 + i, P.row_lo, P.row_hi, P.Tthr);
+      mbits_s[i] = (uint8_t)bits;
+      c += __popc(bits);
+    }
+    c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+    if (lane == 0 && c) atomicAdd(&mcnt_s, c);
+  }
+  __syncthreads();
+
+  // ---- setup per tile: d_old and the prescaled residual in pi order ----------------
+  // R0 = (P Bbar - P D Cbar) / c_pp, radii sums ||P d_j|| (R9)
+  for (int e = tid; e < LD; e += nthr) {
+    Dold[(size_t)TR * LD + e] = 0.f;
+    Rini[(size_t)TR * LD + e] = 0.f;
+  }
+  for (int tl = 0; tl < ntile; ++tl) {
+    const int r0 = tl * TR, nr = min(TR, nr_all - r0);
+    for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + r0 + r];
+    __syncthreads();
+    // natural-order rows: D into V, Bbar into Rini (stride kp)
+    {
+      const int c4 = kp / 4;
+      for (int e = tid; e < nr * c4; e += nthr) {
+        const int row = e / c4, c = e % c4;
+        const int64_t goff = (int64_t)rows_s[row] * kp + 4 * c;
+        nb_cp16(V + (size_t)row * kp + 4 * c, P.D + goff);
+        nb_cp16(Rini + (size_t)row * kp + 4 * c, P.Bbar + goff);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
+    // d_old in pi order
+    for (int e = tid; e < nr * KPT; e += nthr) {
+      const int row = e / KPT, p = e % KPT;
+      Dold[(size_t)row * LD + p] = p < k ? V[(size_t)row * kp + jmap_s[p]] : 0.f;
+    }
+    __syncthreads();
+    // Bbar in pi order into V (row stride LD)
+    for (int e = tid; e < nr * KPT; e += nthr) {
+      const int row = e / KPT, p = e % KPT;
+      V[(size_t)row * LD + p] = p < k ? Rini[(size_t)row * kp + jmap_s[p]] : 0.f;
+    }
+    __syncthreads();
+    // R0 = (Bbar - Dold Cpi) * invc : RT rows x 8 positions per item
+    {
+      constexpr int RT = 4;
+      const int nrb = (nr + RT - 1) / RT, npb = (k + 7) / 8;
+      for (int it = tid; it < nrb * npb; it += nthr) {
+        const int rb = (it / npb) * RT, p0 = (it % npb) * 8;
+        float acc[RT][8];
+#pragma unroll
+        for (int i = 0; i < RT; ++i)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+        for (int l = 0; l < k; ++l) {
+          const float4 c0 = __ldg(reinterpret_cast<const float4*>(A.Cpi + (size_t)l * KPT + p0));
+          const float4 c1 = __ldg(reinterpret_cast<const float4*>(A.Cpi + (size_t)l * KPT + p0 + 4));
+          const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+#pragma unroll
+          for (int i = 0; i < RT; ++i) {
+            const float d = Dold[(size_t)min(rb + i, TR) * LD + l];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(d, cv[c], acc[i][c]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const int row = rb + i;
+          if (row >= nr) continue;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int p = p0 + c;
+            if (p < k) Rini[(size_t)row * LD + p] = (V[(size_t)row * LD + p] - acc[i][c]) * A.invc[p];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < nr * LD; e += nthr) {                 // padding positions of R0
+      const int row = e / LD, p = e % LD;
+      if (p >= k) Rini[(size_t)row * LD + p] = 0.f;
+    }
+    // radii sums of this tile (fp64, fixed order: tile by tile)
+    {
+      const int nwarp = nthr >> 5;
+      for (int p = wid; p < k; p += nwarp) {
+        double d1 = 0.0, d2 = 0.0;
+        for (int row = lane; row < nr; row += 32) {
+          const double d = Dold[(size_t)row * LD + p];
+          d1 += fabs(d);
+          d2 += d * d;
+        }
+        d1 = warp_sum(d1);
+        d2 = warp_sum(d2);
+        if (lane == 0) {
+          acc1_s[p] += d1;
+          acc2_s[p] += d2;
+        }
+      }
+    }
+    __syncthreads();
+    if (streamed) {
+      // the tile's d_old | R0 rows to the scratch (2 KPT floats per row)
+      float* sc = A.scr + (size_t)(lo + r0) * 2 * KPT;
+      for (int e = tid; e < nr * KPT; e += nthr) {
+        const int row = e / KPT, p = e % KPT;
+        sc[(size_t)row * 2 * KPT + p] = Dold[(size_t)row * LD + p];
+        sc[(size_t)row * 2 * KPT + KPT + p] = Rini[(size_t)row * LD + p];
+      }
+      __syncthreads();
+    }
+  }
+  if (nr_all > 0 && tid < k) {
+    unsigned long long* rr = P.rec + (((size_t)kNtRing * P.ncopy + blockIdx.x % P.ncopy) * k + tid) * kNtRec;
+    const bool ok = fx_red(rr + 1, acc1_s[tid]) & fx_red(rr + 3, acc2_s[tid]);
+    if (!ok) atomicExch(P.err, 6);
+  }
+  if (CH >= KPT) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  if (P.idx_next && tid == 0) P.cnt_next[blockIdx.x] = mcnt_s;   // before round 0's barrier
+
+  // my rows within a tile: M consecutive rows of group g; rows >= nr use the spare row
+  const int g = tid / T, tq = tid % T;
+  const int ngroups = (TR + M - 1) / M;
+
+  // one recurrence pass over tile tl (loads it first when streamed); leaves v in V
+  auto pass = [&](int tl, const NtPar<kGen>* par) {
+    const int r0 = tl * TR, nr = min(TR, nr_all - r0);
+    if (streamed) {
+      __syncthreads();                               // V / Dold / Rini of the previous tile consumed
+      const float* sc = A.scr + (size_t)(lo + r0) * 2 * KPT;
+      constexpr int q4 = KPT / 4;
+      for (int e = tid; e < nr * 2 * q4; e += nthr) {
+        const int row = e / (2 * q4), c = e % (2 * q4);
+        float* dst = c < q4 ? Dold + (size_t)row * LD + 4 * c : Rini + (size_t)row * LD + 4 * (c - q4);
+        const float4 v4 = __ldcg(reinterpret_cast<const float4*>(sc + (size_t)row * 2 * KPT + 4 * c));
+        dst[0] = v4.x;
+        dst[1] = v4.y;
+        dst[2] = v4.z;
+        dst[3] = v4.w;
+      }
+    }
+    if (CH < KPT) {
+      // chunk 0 of the prescaled Cbar into buffer 0
+      constexpr int n4 = CH * T * CSTR / 4;
+      for (int e = tid; e < n4; e += nthr) nb_cp16(cbuf + 4 * e, A.Ctg + 4 * e);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __syncthreads();
+    int rowx[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) rowx[m] = (g < ngroups && g * M + m < nr) ? g * M + m : TR;
+    const int vstride = rowx[M - 1] - rowx[0];
+    float Do[M][KT], R[M][KT];
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
+        R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
+      }
+    // threads past the groups: same code on the spare row (their v goes to the spare row)
+    constexpr int H1 = KPT > 128 ? 128 : KPT;
+    NbRec<KPT, T, M, kGen, CH, 0, H1>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, A.Ctg, par);
+    if constexpr (KPT > 128)
+      NbRec<KPT, T, M, kGen, CH, H1, KPT>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, A.Ctg, par);
+    __syncthreads();
+    return nr;
+  };
+
+  unsigned nbar = 0;
+  int round = 0, cur = 0;
+  bool done = q == 0;
+  if (done && P.idx_next) {
+    ++nbar;
+    nt_barrier(P.bar, nbar * G);
+  }
+#pragma unroll 1
+  while (!done) {
+    const int ring = round % kNtRing;
+    for (int p = tid; p < k; p += nthr) {
+      acn_s[p] = 0u;
+      amn_s[p] = 0xffffffffu;
+      amx_s[p] = 0u;
+      acc1_s[p] = acc2_s[p] = 0.0;
+    }
+    for (int tl = 0; tl < ntile; ++tl) {
+      const int nr = pass(tl, par_s[cur]);
+      // per-atom statistics of the tile, added to the CTA sums in tile order
+      if (tid < H * k) {
+        const int p = tid % k, h = tid / k;
+        const double th = a * lam_s[p];
+        const float thf = th > 0.0 ? __double2float_rd(th) : 0.f;
+        unsigned cnt = 0, mn = 0xffffffffu, mx = 0u;
+        float s1 = 0.f, s2 = 0.f;
+        for (int r = h; r < nr; r += H) {
+          const float av = fabsf(V[(size_t)r * LD + p]);
+          const bool above = av > thf;
+          cnt += above;
+          s1 += above ? av : 0.f;
+          s2 = fmaf(above ? av : 0.f, av, s2);
+          mn = above ? min(mn, __float_as_uint(av)) : mn;
+          mx = above ? mx : max(mx, __float_as_uint(av));
+        }
+        pcn[h * KPT + p] = cnt;
+        ps1[h * KPT + p] = s1;
+        ps2[h * KPT + p] = s2;
+        pmn[h * KPT + p] = mn;
+        pmx[h * KPT + p] = mx;
+      }
+      __syncthreads();
+      if (tid < k) {
+        const int p = tid;
+        unsigned cnt = acn_s[p], mn = amn_s[p], mx = amx_s[p];
+        double S1 = 0.0, S2 = 0.0;
+        for (int h = 0; h < H; ++h) {
+          cnt += pcn[h * KPT + p];
+          S1 += (double)ps1[h * KPT + p];
+          S2 += (double)ps2[h * KPT + p];
+          mn = min(mn, pmn[h * KPT + p]);
+          mx = max(mx, pmx[h * KPT + p]);
+        }
+        acn_s[p] = cnt;
+        amn_s[p] = mn;
+        amx_s[p] = mx;
+        acc1_s[p] += S1;
+        acc2_s[p] += S2;
+      }
+      __syncthreads();
+    }
+    if (nr_all > 0 && tid < k) {
+      const int p = tid;
+      unsigned long long* rc = P.rec + (((size_t)ring * P.ncopy + blockIdx.x % P.ncopy) * k + p) * kNtRec;
+      unsigned* mm = reinterpret_cast<unsigned*>(rc + 5);
+      if (acn_s[p] > 0) {
+        nt_red_u64(rc, (unsigned long long)acn_s[p]);
+        const bool ok = fx_red(rc + 1, acc1_s[p]) & fx_red(rc + 3, acc2_s[p]);
+        if (!ok) atomicExch(P.err, 6);
+        atomicMin(mm, amn_s[p]);
+      }
+      if (amx_s[p]) atomicMax(mm + 1, amx_s[p]);
+    }
+    ++nbar;
+    nt_barrier(P.bar, nbar * G);
+    if (blockIdx.x == 0) {
+      const int rz = (round + 2) % kNtRing;
+      for (int e = tid; e < P.ncopy * k; e += nthr) nt_rec_reset(P.rec + ((size_t)rz * P.ncopy * k + e) * kNtRec);
+    }
+    // ---- the same Michelot step for every atom in every CTA ----
+    int conv = 1, nmode = 0;
+    double nlam = 0.0, cnt = 0.0, S1 = 0.0, S2 = 0.0;
+    const int p = tid;
+    const bool act = tid < k;
+    unsigned long long* rdp = reinterpret_cast<unsigned long long*>(pcn);
+    if (round == 0) {
+      nt_read_coop(P.rec + (size_t)kNtRing * P.ncopy * k * kNtRec, P.ncopy, k, P.rd_h, rdp);
+      __syncthreads();
+      if (act) {
+        const NtSums rs = nt_combine(rdp, P.rd_h, k, p);
+        rho_s[p] = fmax(0.0, rho_s[p] + a * rs.S1 + 0.5 * b * rs.S2);     // P:860, R9
+      }
+      __syncthreads();
+    }
+    nt_read_coop(P.rec + (size_t)ring * P.ncopy * k * kNtRec, P.ncopy, k, P.rd_h, rdp);
+    __syncthreads();
+    if (act) {
+      const NtSums sm = nt_combine(rdp, P.rd_h, k, p);
+      cnt = sm.cnt;
+      S1 = sm.S1;
+      S2 = sm.S2;
+      const double mnv = cnt > 0.0 ? (double)__uint_as_float(sm.mn) : INFINITY;
+      const double mxv = (double)__uint_as_float(sm.mx);
+      conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol);
+    }
+    const bool all_conv = __syncthreads_and(conv);
+    const bool capped = round + 1 >= P.max_rounds && !all_conv;
+    if (act) {
+      if (all_conv || capped) {
+        if (mode_s[p] != kModeDead && blockIdx.x == 0) {
+          const int j = jmap_s[p];
+          P.nslack[j] = rho_s[p] - nt_norm_d(a, b, mode_s[p], lam_s[p], cnt, S1, S2);
+          P.lam_ws[j] = lam_s[p];
+        }
+        par_s[cur ^ 1][p] = par_s[cur][p];
+      } else {
+        lam_s[p] = nlam;
+        mode_s[p] = nmode;
+        par_s[cur ^ 1][p] = nt_make_par<kGen>(nmode, a, b, nlam, vlo_s[p]);
+      }
+    }
+    ++round;
+    if (all_conv) {
+      done = true;
+    } else if (capped) {
+      if (tid == 0 && blockIdx.x == 0) atomicExch(P.err, 4);
+      done = true;
+    }
+    if (!done) cur ^= 1;
+    __syncthreads();
+  }
+  // ---- final D: v of the final round through its parameters (streamed: one more
+  // pass per tile with the final parameters) ----
+  if (q > 0) {
+    const NtPar<kGen>* pr = par_s[cur];
+    for (int tl = 0; tl < ntile; ++tl) {
+      int nr = min(TR, nr_all - tl * TR);
+      if (streamed) nr = pass(tl, pr);
+      if (streamed || tl == 0) {
+        if (streamed) {
+          for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + tl * TR + r];
+          __syncthreads();
+        }
+        for (int r = wid; r < nr; r += (nthr >> 5)) {
+          float* dst = P.D + (int64_t)rows_s[r] * kp;
+          const float* src = V + (size_t)r * LD;
+          for (int j = lane; j < k; j += 32) {
+            const int pp = pinv_s[j];
+            dst[j] = pr[pp].d_of(src[pp]);
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  // ---- draw-ahead of t+1: scatter of my slice of M_{t+1}, t+1, w_{t+1} ----
+  if (P.idx_next) {
+    if (wid == 0) {
+      int64_t off = 0;
+      for (int i = lane; i < (int)blockIdx.x; i += 32) off += __ldcg(P.cnt_next + i);
+      off = warp_sum(off);
+      const int i0 = nmb * lane / 32, i1 = nmb * (lane + 1) / 32;
+      int c = 0;
+      for (int i = i0; i < i1; ++i) c += __popc((unsigned)mbits_s[i]);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int64_t pos = off + incl - c;
+      for (int i = i0; i < i1; ++i) {
+        const unsigned bits = mbits_s[i];
+        for (int l = 0; l < 4; ++l)
+          if (bits & (1u << l)) P.idx_next[pos++] = (int32_t)((mb0 + i) * 4 + l - P.row_lo);
+      }
+      if (blockIdx.x == G - 1 && lane == 31) *P.q_next = pos;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      *P.t_next = P.tn;
+      *P.w_next = pow((double)P.tn, -P.u);
+    }
+  }
+  // ---- exit: last CTA resets counters and accumulators ----
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(P.bar + 1, 1u);
+    mcnt_s = old == (unsigned)G - 1;
+  }
+  __syncthreads();
+  if (mcnt_s) {
+    __threadfence();
+    for (int e = tid; e < (kNtRing + 1) * P.ncopy * k; e += nthr) nt_rec_reset(P.rec + (size_t)e * kNtRec);
+    if (tid == 0) {
+      if (P.nred_out) *P.nred_out = nbar;
+      P.bar[0] = 0u;
+      P.bar[1] = 0u;
+    }
+    __threadfence();
+  }
+}
+
+}  // namespace somf

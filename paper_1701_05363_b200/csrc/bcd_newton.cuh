@@ -63,6 +63,8 @@ struct NtArgs {
   int cap_rows;             // rows per CTA the shared memory holds (T x cap_rows <= blockDim)
   int ct_in_w;               // Cbar per thread parity fits the staging buffer W
   int part_in_cpi;           // the stats partials (5 H KPT words) fit the Cbar staging area
+  int rd_h;                  // threads per atom of the cooperative record read (its 48 rd_h k bytes
+                             // reuse the stats partials' area, free after the barrier)
   int max_rounds;
   double lam_tol;           // convergence tolerance on lambda (kNtLamTol)
   // per-atom grid accumulators, 128-byte records (u64 words) so the atomics
@@ -220,6 +222,62 @@ __device__ __forceinline__ NtSums nt_read(const unsigned long long* slot0, int n
       mn = min(mn, (unsigned)(v45[h].y & 0xffffffffull));
       mx = max(mx, (unsigned)(v45[h].y >> 32));
     }
+  }
+  NtSums r;
+  r.cnt = (double)c;
+  r.S1 = fx_value(a1, a2);
+  r.S2 = fx_value(b1, b2);
+  r.mn = mn;
+  r.mx = mx;
+  return r;
+}
+
+// The same sums read COOPERATIVELY: H2 threads per atom each load a strided
+// subset of the copies (all of its loads in flight: one L2 round trip instead
+// of ncopy / 2), the raw integer partials go to shared memory (part: [H2][k][6]
+// u64) and nt_combine adds them (integers: the order does not matter).
+__device__ __forceinline__ void nt_read_coop(const unsigned long long* slot0, int ncopy, int k, int H2,
+                                             unsigned long long* part) {
+  const int tid = threadIdx.x;
+  if (tid < H2 * k) {
+    const int p = tid % k, h = tid / k;
+    unsigned long long c = 0, a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+    unsigned mn = 0xffffffffu, mx = 0u;
+#pragma unroll 4
+    for (int cc = h; cc < ncopy; cc += H2) {
+      const unsigned long long* rc = slot0 + ((size_t)cc * k + p) * kNtRec;
+      const ulonglong2 v01 = __ldcg(reinterpret_cast<const ulonglong2*>(rc));
+      const ulonglong2 v23 = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 2));
+      const ulonglong2 v45 = __ldcg(reinterpret_cast<const ulonglong2*>(rc + 4));
+      c += v01.x;
+      a1 += v01.y;
+      a2 += v23.x;
+      b1 += v23.y;
+      b2 += v45.x;
+      mn = min(mn, (unsigned)(v45.y & 0xffffffffull));
+      mx = max(mx, (unsigned)(v45.y >> 32));
+    }
+    unsigned long long* o = part + ((size_t)h * k + p) * 6;
+    o[0] = c;
+    o[1] = a1;
+    o[2] = a2;
+    o[3] = b1;
+    o[4] = b2;
+    o[5] = ((unsigned long long)mx << 32) | mn;
+  }
+}
+__device__ __forceinline__ NtSums nt_combine(const unsigned long long* part, int H2, int k, int p) {
+  unsigned long long c = 0, a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+  unsigned mn = 0xffffffffu, mx = 0u;
+  for (int h = 0; h < H2; ++h) {
+    const unsigned long long* o = part + ((size_t)h * k + p) * 6;
+    c += o[0];
+    a1 += o[1];
+    a2 += o[2];
+    b1 += o[3];
+    b2 += o[4];
+    mn = min(mn, (unsigned)(o[5] & 0xffffffffull));
+    mx = max(mx, (unsigned)(o[5] >> 32));
   }
   NtSums r;
   r.cnt = (double)c;
@@ -638,7 +696,8 @@ k_bcd_newton(NtArgs P) {
 
   // stats partials (H threads per atom) reuse the Cbar staging area (host checks the size)
   const int H = max(1, nthr / max(k, 1));
-  unsigned* pcn = reinterpret_cast<unsigned*>(P.part_in_cpi ? Cpi : reinterpret_cast<float*>(rows_s + cap));
+  unsigned* pcn = P.part_in_cpi ? reinterpret_cast<unsigned*>(Cpi)
+                                : reinterpret_cast<unsigned*>((reinterpret_cast<uintptr_t>(rows_s + cap) + 15) & ~(uintptr_t)15);
   float* ps1 = reinterpret_cast<float*>(pcn + H * KPT);
   float* ps2 = ps1 + H * KPT;
   unsigned* pmn = reinterpret_cast<unsigned*>(ps2 + H * KPT);
@@ -755,12 +814,20 @@ k_bcd_newton(NtArgs P) {
     double nlam = 0.0, cnt = 0.0, S1 = 0.0, S2 = 0.0;
     const int p = F + tid;
     const bool act = tid < nact;
-    if (act) {
-      if (round == 0) {
-        const NtSums rs = nt_read(P.rec + (size_t)kNtRing * P.ncopy * k * kNtRec, P.ncopy, k, p);
+    unsigned long long* rdp = reinterpret_cast<unsigned long long*>(pcn);
+    if (round == 0) {
+      nt_read_coop(P.rec + (size_t)kNtRing * P.ncopy * k * kNtRec, P.ncopy, k, P.rd_h, rdp);
+      __syncthreads();
+      if (act) {
+        const NtSums rs = nt_combine(rdp, P.rd_h, k, p);
         rho_s[p] = fmax(0.0, rho_s[p] + a * rs.S1 + 0.5 * b * rs.S2);     // P:860, R9
       }
-      const NtSums sm = nt_read(P.rec + (size_t)ring * P.ncopy * k * kNtRec, P.ncopy, k, p);
+      __syncthreads();
+    }
+    nt_read_coop(P.rec + (size_t)ring * P.ncopy * k * kNtRec, P.ncopy, k, P.rd_h, rdp);
+    __syncthreads();
+    if (act) {
+      const NtSums sm = nt_combine(rdp, P.rd_h, k, p);
       cnt = sm.cnt;
       S1 = sm.S1;
       S2 = sm.S2;

@@ -5,40 +5,48 @@
 //   minimise 1/2 a^T G a - beta^T a + l1 |a|_1 + l2/2 |a|^2  (a >= 0 if positive)
 //
 // The solution is unique (G + l2 I > 0 on the support), so any
-// convergent path gives the oracle's value (reading R14).  Plain cyclic CD
-// (k_cd) needs ~90 sweeps of k dependent coordinate steps at cfgB (k = 256);
-// here, after a few warm sweeps, every CD sweep is followed by a JUMP: with S
-// the current support and s its signs, solve the stationarity system of the
-// face exactly,
-//   (G_SS + l2 I) a_S = beta_S - l1 s_S                         (KKT on S)
-// by a warp Cholesky in fp64, and accept a_S if its signs agree with s (then
-// it is the minimiser over the orthant face containing the current point,
-// so the objective does not increase).  The next CD sweep either confirms
-// optimality (max |delta| <= tol, every off-support KKT condition holds) or
-// moves the support; convergence is CD's.  Supports larger than kAsMax skip
-// the jump (plain CD).  One warp per column, 4 warps per CTA; per warp the
-// face system (kAsMax^2 doubles) lives in shared memory next to the packed
-// fp32 Gram (k = 256 fits).
+// convergent path gives the oracle's value (readings R14, R14b).  Plain cyclic
+// CD (k_cd) needs ~90 sweeps of k dependent coordinate steps at cfgB (k = 256)
+// and ~700 at cfgD (nonneg ridge on an NMF Gram, cond ~5e3); here:
+//
+//  * each CD sweep is exact cyclic CD, but the coordinates whose update is
+//    zero (most of them: the codes are sparse) cost nothing: all 32 lanes of a
+//    slot compute their candidate update from the current gradient, a ballot
+//    finds the FIRST nonzero one in cyclic order, only that one is applied
+//    (broadcast + gradient update), and the lanes after it recompute;
+//  * after kAsWarm sweeps, every sweep is followed by a JUMP towards the
+//    minimiser of the current orthant face: with S the support and s its signs,
+//    solve (G_SS + l2 I) y = beta_S - l1 s_S (warp Cholesky, fp64).  If every
+//    sign of y agrees, a_S <- y.  Otherwise move a_S along the segment towards
+//    y up to the first coordinate that reaches zero, drop it, and solve again
+//    on the smaller face (the feature-sign / active-set line search: the
+//    objective is convex on the face, so it never increases).  The next CD
+//    sweep confirms optimality (max |delta| <= tol) or moves the support.
+//
+// One warp per column; `nw` warps per CTA share the packed Gram in shared
+// memory (fp64 when it fits, else fp32); each warp has a face scratch for
+// supports up to `nmax` coordinates (larger supports skip the jump: plain CD).
 #pragma once
 #include "common.cuh"
 #include "solve.cuh"
 
 namespace somf {
 
-constexpr int kAsThreads = 128;     // 4 warps = 4 columns per CTA
-constexpr int kAsMax = 48;          // largest support solved exactly
-constexpr int kAsWarm = 6;          // CD sweeps before the first jump
+constexpr int kAsWarm = 3;          // CD sweeps before the first jump
 
-// per-warp scratch: kAsMax x kAsMax doubles (A, then L) + kAsMax doubles (y) + kAsMax ints
-__host__ __device__ constexpr size_t cd_as_warp_bytes() {
-  return (size_t)kAsMax * kAsMax * 8 + (size_t)kAsMax * 8 + (size_t)kAsMax * 4;
+// per-warp scratch: packed lower face matrix, y, a_S, sidx, and a dense k-vector
+__host__ __device__ constexpr size_t cd_as_warp_bytes(int nmax, int k) {
+  return ((size_t)nmax * (nmax + 1) / 2 + 2 * (size_t)nmax + (size_t)((k + 1) & ~1)) * 8 +
+         (size_t)((nmax + 3) & ~3) * 4;
 }
+
+__device__ __forceinline__ int pl_idx(int r, int c) { return (r * (r + 1) >> 1) + c; }   // packed lower, c <= r
 
 // GT: the packed Gram's type in shared memory (double when it fits, else float)
 template <int KPL, typename GT>
-__global__ void __launch_bounds__(kAsThreads)
+__global__ void __launch_bounds__(128)
 k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
-        double l1, double l2, int positive, double tol, int max_sweeps,
+        double l1, double l2, int positive, double tol, int max_sweeps, int nmax,
         double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out,
         float* __restrict__ AT32, int ldt, int64_t gstride) {
   // the B-bar kernel may launch now (programmatic dependent launch); it reads
@@ -50,11 +58,14 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
   const int tid = threadIdx.x, nt = blockDim.x;
   const int np = k * (k + 1) / 2;
   const int lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  uint8_t* wbase = as_smem + (size_t)wid * cd_as_warp_bytes();
-  double* Af = reinterpret_cast<double*>(wbase);                  // kAsMax x kAsMax
-  double* yv = Af + kAsMax * kAsMax;                              // kAsMax
-  int* sidx = reinterpret_cast<int*>(yv + kAsMax);                // kAsMax
-  GT* Pk = reinterpret_cast<GT*>(as_smem + (size_t)nw * cd_as_warp_bytes());   // packed upper triangle
+  const size_t wbytes = cd_as_warp_bytes(nmax, k);
+  uint8_t* wbase = as_smem + (size_t)wid * wbytes;
+  double* Af = reinterpret_cast<double*>(wbase);                  // nmax (nmax+1)/2, packed lower
+  double* yv = Af + (size_t)nmax * (nmax + 1) / 2;                // nmax
+  double* av = yv + nmax;                                         // nmax: a_S in sidx order
+  double* anew = av + nmax;                                       // k: dense result of a jump
+  int* sidx = reinterpret_cast<int*>(anew + ((k + 1) & ~1));      // nmax
+  GT* Pk = reinterpret_cast<GT*>(as_smem + (size_t)nw * wbytes);  // packed upper triangle
   for (int e = tid; e < np; e += nt) {
     int lo = 0, hi = k - 1;
     while (lo < hi) {
@@ -80,35 +91,38 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
     }
     int sweep = 0;
     for (; sweep < max_sweeps; ++sweep) {
-      // ---- one cyclic CD sweep (as k_cd) ----
+      // ---- one cyclic CD sweep; zero updates skipped by ballot ----
       double maxd = 0.0;
 #pragma unroll
       for (int slot = 0; slot < KPL; ++slot) {
-        for (int ol = 0; ol < 32; ++ol) {
-          const int j = slot * 32 + ol;
-          if (j >= k) break;
-          double delta = 0.0;
-          if (lane == ol) {
+        const int jl = slot * 32 + lane;
+        int ol = 0;
+        while (ol < 32) {
+          // candidate update of my coordinate from the current gradient
+          double nv = 0.0, delta = 0.0;
+          if (jl < k && lane >= ol) {
             const double gjj = den[slot] - l2;
             const double z = g[slot] + gjj * alpha[slot];
-            double nv;
             if (!(den[slot] > 0.0)) nv = 0.0;                          // R12
             else if (positive) nv = fmax(z - l1, 0.0) * rden[slot];
             else nv = copysign(fmax(fabs(z) - l1, 0.0), z) * rden[slot];
             delta = nv - alpha[slot];
-            alpha[slot] = nv;
           }
-          delta = __shfl_sync(0xffffffffu, delta, ol);
-          if (delta != 0.0) {
-            maxd = fmax(maxd, fabs(delta));
-            const int joff = packed_off(j, k);
+          const unsigned bal = __ballot_sync(0xffffffffu, delta != 0.0);
+          if (bal == 0u) break;
+          const int o = __ffs(bal) - 1;                 // first nonzero update in cyclic order
+          const double dl = __shfl_sync(0xffffffffu, delta, o);
+          if (lane == o) alpha[slot] = nv;
+          maxd = fmax(maxd, fabs(dl));
+          const int j = slot * 32 + o;
+          const int joff = packed_off(j, k);
 #pragma unroll
-            for (int i = 0; i < KPL; ++i) {
-              const int row = lane + 32 * i;
-              const int a = row <= j ? roff[i] + (j - row) : joff + (row - j);
-              if (row < k) g[i] = fma(-(double)Pk[a], delta, g[i]);
-            }
+          for (int i = 0; i < KPL; ++i) {
+            const int row = lane + 32 * i;
+            const int a = row <= j ? roff[i] + (j - row) : joff + (row - j);
+            if (row < k) g[i] = fma(-(double)Pk[a], dl, g[i]);
           }
+          ol = o + 1;
         }
       }
       double amax = 0.0;
@@ -117,100 +131,144 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
       amax = warp_max(amax);
       if (maxd <= tol * fmax(1.0, amax)) { ++sweep; break; }
       if (sweep + 1 < kAsWarm) continue;
-      // ---- jump: exact solve on the current support ----
+      // ---- jump: exact solve on the current face, with line search ----
       int n = 0;
 #pragma unroll
       for (int slot = 0; slot < KPL; ++slot) {
         const unsigned msk = __ballot_sync(0xffffffffu, alpha[slot] != 0.0);
         const int pos = n + __popc(msk & ((1u << lane) - 1u));
-        if (alpha[slot] != 0.0 && pos < kAsMax) sidx[pos] = slot * 32 + lane;
+        if (alpha[slot] != 0.0 && pos < nmax) {
+          sidx[pos] = slot * 32 + lane;
+          av[pos] = alpha[slot];
+        }
         n += __popc(msk);
       }
-      if (n == 0 || n > kAsMax) continue;
+      if (n == 0 || n > nmax) continue;
+      for (int j = lane; j < k; j += 32) anew[j] = 0.0;
+      bool moved = false;
       __syncwarp();
-      // A = G_SS + l2 I (lower triangle), y = beta_S - l1 sign_S
-      for (int e = lane; e < n * n; e += 32) {
-        const int r = e / n, c = e % n;
-        if (c <= r) {
-          const int jr = sidx[r], jc = sidx[c];
-          Af[r * kAsMax + c] = (double)packed_get(Pk, jr, jc, k) + (r == c ? l2 : 0.0);
+      while (n > 0) {
+        // A = G_SS + l2 I (packed lower), y = beta_S - l1 sign(a_S)
+        for (int e = lane; e < n * (n + 1) / 2; e += 32) {
+          int r = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
+          while (pl_idx(r, 0) > e) --r;
+          while (pl_idx(r + 1, 0) <= e) ++r;
+          const int c = e - pl_idx(r, 0);
+          Af[e] = (double)packed_get(Pk, sidx[r], sidx[c], k) + (r == c ? l2 : 0.0);
         }
+        for (int r = lane; r < n; r += 32) {
+          const int j = sidx[r];
+          yv[r] = beta[(int64_t)j * m + s] - l1 * (av[r] > 0.0 ? 1.0 : -1.0);
+        }
+        __syncwarp();
+        // Cholesky (right-looking, column by column; rows by lane); the
+        // diagonal holds 1 / L_cc (the substitutions multiply)
+        bool ok = true;
+        for (int c = 0; c < n; ++c) {
+          const double d = Af[pl_idx(c, c)];
+          if (!(d > 0.0)) { ok = false; break; }
+          const double il = rsqrt(d);
+          __syncwarp();
+          for (int r = c + 1 + lane; r < n; r += 32) Af[pl_idx(r, c)] *= il;
+          __syncwarp();
+          if (lane == 0) Af[pl_idx(c, c)] = il;
+          for (int r = c + 1 + lane; r < n; r += 32) {
+            const int rb = pl_idx(r, 0);
+            const double lrc = Af[rb + c];
+#pragma unroll 4
+            for (int q = c + 1; q <= r; ++q) Af[rb + q] = fma(-lrc, Af[pl_idx(q, c)], Af[rb + q]);
+          }
+          __syncwarp();
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok) break;
+        // L z = y, then L^T x = z, both column-oriented (rows by lane, no reductions)
+        for (int c = 0; c < n; ++c) {
+          const double zc = yv[c] * Af[pl_idx(c, c)];
+          __syncwarp();
+          if (lane == 0) yv[c] = zc;
+          for (int r = c + 1 + lane; r < n; r += 32) yv[r] = fma(-Af[pl_idx(r, c)], zc, yv[r]);
+          __syncwarp();
+        }
+        for (int c = n - 1; c >= 0; --c) {
+          const int cb = pl_idx(c, 0);
+          const double xc = yv[c] * Af[cb + c];
+          __syncwarp();
+          if (lane == 0) yv[c] = xc;
+          for (int r = lane; r < c; r += 32) yv[r] = fma(-Af[cb + r], xc, yv[r]);      // L^T[r][c] = L[c][r]
+          __syncwarp();
+        }
+        // signs agree: the face minimiser is the new point
+        bool agree = true;
+        double tau = 2.0;
+        int rmin = n;
+        for (int r = lane; r < n; r += 32) {
+          const double a0 = av[r], y = yv[r];
+          const bool same = a0 > 0.0 ? y > 0.0 : y < 0.0;
+          agree &= same;
+          if (!same) {
+            const double tr = a0 / (a0 - y);                 // in (0, 1]: where a0 + tr (y - a0) = 0
+            if (tr < tau || (tr == tau && r < rmin)) { tau = tr; rmin = r; }
+          }
+        }
+        agree = __all_sync(0xffffffffu, agree);
+        moved = true;
+        if (agree) {
+          for (int r = lane; r < n; r += 32) av[r] = yv[r];
+          break;
+        }
+        // line search: a_S <- a_S + tau (y - a_S), the first zero crossing
+        // (smallest tau, lowest position on ties) leaves the support
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double t2 = __shfl_xor_sync(0xffffffffu, tau, o);
+          const int r2 = __shfl_xor_sync(0xffffffffu, rmin, o);
+          if (t2 < tau || (t2 == tau && r2 < rmin)) { tau = t2; rmin = r2; }
+        }
+        __syncwarp();
+        for (int r = lane; r < n; r += 32) {
+          const double a0 = av[r];
+          double na = r == rmin ? 0.0 : fma(tau, yv[r] - a0, a0);
+          if (a0 > 0.0 ? !(na > 0.0) : !(na < 0.0)) na = 0.0;   // rounding past zero
+          av[r] = na;
+        }
+        __syncwarp();
+        // compact the support (order kept)
+        int nn = 0;
+        for (int r0 = 0; r0 < n; r0 += 32) {
+          const int r = r0 + lane;
+          const bool keep = r < n && av[r] != 0.0;
+          const double va = keep ? av[r] : 0.0;
+          const int ja = keep ? sidx[r] : 0;
+          const unsigned msk = __ballot_sync(0xffffffffu, keep);
+          __syncwarp();
+          if (keep) {
+            const int pos = nn + __popc(msk & ((1u << lane) - 1u));
+            av[pos] = va;
+            sidx[pos] = ja;
+          }
+          nn += __popc(msk);
+          __syncwarp();
+        }
+        n = nn;
       }
-      for (int r = lane; r < n; r += 32) yv[r] = 0.0;
+      if (!moved) continue;
+      // the jump's point (zeros off the final support) back into the registers
+      for (int r = lane; r < n; r += 32) anew[sidx[r]] = av[r];
       __syncwarp();
-      // beta_S and signs: the owner lane of coordinate j writes y
 #pragma unroll
       for (int slot = 0; slot < KPL; ++slot) {
-        if (alpha[slot] != 0.0) {
-          // position of coordinate (slot, lane) in sidx: recount (cheap, n <= 48)
-          const int j = slot * 32 + lane;
-          for (int r = 0; r < n; ++r)
-            if (sidx[r] == j) yv[r] = b[slot] - l1 * (alpha[slot] > 0.0 ? 1.0 : -1.0);
-        }
+        const int j = slot * 32 + lane;
+        if (j < k) alpha[slot] = anew[j];
       }
       __syncwarp();
-      // Cholesky (right-looking, column by column; rows by lane)
-      bool ok = true;
-      for (int c = 0; c < n; ++c) {
-        const double d = Af[c * kAsMax + c];
-        if (!(d > 0.0)) { ok = false; break; }
-        const double ld = sqrt(d), il = 1.0 / ld;
-        __syncwarp();
-        for (int r = c + 1 + lane; r < n; r += 32) Af[r * kAsMax + c] *= il;
-        __syncwarp();
-        if (lane == 0) Af[c * kAsMax + c] = ld;
-        for (int r = c + 1 + lane; r < n; r += 32) {
-          const double lrc = Af[r * kAsMax + c];
-          for (int q = c + 1; q <= r; ++q) Af[r * kAsMax + q] = fma(-lrc, Af[q * kAsMax + c], Af[r * kAsMax + q]);
-        }
-        __syncwarp();
-      }
-      ok = __all_sync(0xffffffffu, ok);
-      if (!ok) continue;
-      // L z = y (column-oriented), then L^T x = z
-      for (int c = 0; c < n; ++c) {
-        const double zc = yv[c] / Af[c * kAsMax + c];
-        __syncwarp();
-        if (lane == 0) yv[c] = zc;
-        for (int r = c + 1 + lane; r < n; r += 32) yv[r] = fma(-Af[r * kAsMax + c], zc, yv[r]);
-        __syncwarp();
-      }
-      for (int c = n - 1; c >= 0; --c) {
-        double acc = 0.0;
-        for (int r = c + 1 + lane; r < n; r += 32) acc = fma(Af[r * kAsMax + c], yv[r], acc);
-        acc = warp_sum(acc);
-        const double xc = (yv[c] - acc) / Af[c * kAsMax + c];
-        __syncwarp();
-        if (lane == 0) yv[c] = xc;
-        __syncwarp();
-      }
-      // accept only if every sign agrees (then the face minimiser is feasible)
-      bool agree = true;
-#pragma unroll
-      for (int slot = 0; slot < KPL; ++slot) {
-        if (alpha[slot] != 0.0) {
-          const int j = slot * 32 + lane;
-          for (int r = 0; r < n; ++r)
-            if (sidx[r] == j) agree &= (alpha[slot] > 0.0) ? (yv[r] > 0.0) : (yv[r] < 0.0);
-        }
-      }
-      agree = __all_sync(0xffffffffu, agree);
-      if (!agree) continue;
-#pragma unroll
-      for (int slot = 0; slot < KPL; ++slot) {
-        if (alpha[slot] != 0.0) {
-          const int j = slot * 32 + lane;
-          for (int r = 0; r < n; ++r)
-            if (sidx[r] == j) alpha[slot] = yv[r];
-        }
-      }
       // g = beta - G alpha (alpha supported on S)
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int row = lane + 32 * i;
         double acc = 0.0;
         if (row < k) {
-          for (int r = 0; r < n; ++r) acc = fma((double)packed_get(Pk, row, sidx[r], k), yv[r], acc);
+          for (int r = 0; r < n; ++r) acc = fma((double)packed_get(Pk, row, sidx[r], k), av[r], acc);
         }
         g[i] = b[i] - acc;
       }

@@ -33,6 +33,7 @@
 #include "bcd.cuh"
 #include "bcd_onchip.cuh"
 #include "bcd_newton.cuh"
+#include "bcd_big.cuh"
 #include "bcd_shard.cuh"
 #include "bbar_tc.cuh"
 #include "contract_tc.cuh"
@@ -153,11 +154,16 @@ struct somf_ctx {
   double* theta_ws = nullptr;
   const void* nt_fn = nullptr;   // simultaneous-threshold BCD (bcd_newton.cuh)
   double nt_lam_tol = kNtLamTol;
-  int nt_cap_rows = 0, nt_kpt = 0, nt_threads = 0, nt_ct_in_w = 0, nt_part_in_cpi = 0, nt_T = 0, nt_M = 0;
+  int nt_rd_h = 1, nt_cap_rows = 0, nt_kpt = 0, nt_threads = 0, nt_ct_in_w = 0, nt_part_in_cpi = 0, nt_T = 0, nt_M = 0;
   size_t nt_smem = 0;
   double* lam_ws = nullptr;
   unsigned long long* nt_acc = nullptr;
   int nt_ncopy = 8;
+  // simultaneous-threshold BCD for k <= 256 / streamed rows (bcd_big.cuh)
+  const void* nb_fn = nullptr;
+  int nb_kpt = 0, nb_T = 0, nb_ch = 0, nb_tr = 0, nb_threads = 0, nb_rd_h = 1;
+  size_t nb_smem = 0;
+  float *nb_cpi = nullptr, *nb_ctg = nullptr, *nb_invc = nullptr, *nb_scr = nullptr;
   long long* bcd_prof = nullptr;   // SM cycles per BCD phase (somf_bcd_phase_cycles)
   // row sharding (somf_set_reducer): the caller's allreduce over the ranks
   somf_reduce_fn reducer = nullptr;
@@ -665,28 +671,51 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     return SOMF_OK;
   }
   const double l1 = c.lambda * (1.0 - c.nu), l2 = c.lambda * c.nu;
-  // the packed Gram in fp64 when it fits next to the face scratch (k <= 160),
-  // else fp32 (k = 256: 132 KB)
+  // the packed Gram in fp64 when it fits next to the face scratch, else fp32
+  // (k = 256: 132 KB); face capacity nmax = min(k, 128) (a column whose support
+  // outgrows it runs plain CD), as many warps (columns) per CTA as fit, <= 4
   const size_t np = (size_t)k * (k + 1) / 2;
   const int kpl = (int)ceil_div(k, 32);
-  const size_t warps_as = (size_t)(kAsThreads / 32) * cd_as_warp_bytes();
-  const bool g64 = warps_as + np * sizeof(double) <= 200 * 1024;
-  const size_t smem = np * (g64 ? sizeof(double) : sizeof(float));
-  const size_t smem_as = warps_as + smem;
-  const bool as_ok = k >= 32 && smem_as <= 220 * 1024;
+  // Policy: enough warps per CTA that the columns fill the SMs in one wave
+  // (<= 4), with the largest face that still leaves them room, but a face of
+  // at least min(k, 96) (the supports at cfgB / cfgE reach ~40 / ~90); fp64
+  // Gram first.
+  const size_t budget = 220 * 1024;
+  const int nw_want = (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(m, h->nsm)));
+  const int nm_floor = std::min(k, 96);
+  bool g64 = true;
+  int nmax = 0, nw_as = 0;
+  for (int gi = 0; gi < 2; ++gi) {
+    const bool g = gi == 0;
+    const size_t gb = np * (g ? sizeof(double) : sizeof(float));
+    if (gb >= budget) continue;
+    for (int nw = nw_want; nw >= 1; --nw) {
+      int best = 0;
+      for (int nm = std::min(k, 128); nm >= nm_floor; nm -= 8)
+        if ((size_t)nw * cd_as_warp_bytes(nm, k) + gb <= budget) { best = nm; break; }
+      if (best && nw > nw_as) { nmax = best; nw_as = nw; g64 = g; }
+      if (best) break;
+    }
+    if (nw_as == nw_want) break;
+  }
+  if (gstride > 0) nw_as = std::min(nw_as, 1);      // a Gram per column: one column per CTA
+  const size_t smem_as = nw_as > 0 ? (size_t)nw_as * cd_as_warp_bytes(nmax, k) +
+                                         np * (g64 ? sizeof(double) : sizeof(float))
+                                   : 0;
+  const bool as_ok = k >= 8 && nw_as > 0;
   if (sel == 2 && !as_ok) {
-    set_err(h, "codes_kernel = cd_jump requires k >= 32");
+    set_err(h, "codes_kernel = cd_jump does not fit k = %d", k);
     return SOMF_E_UNSUPPORTED;
   }
   if (as_ok && (sel == 0 || sel == 2)) {
-    // CD with exact support jumps (cd_as.cuh), 4 columns per CTA (1 with a Gram per column)
-    const int tas = gstride > 0 ? 32 : kAsThreads;
-    const int gas = (int)ceil_div(m, tas / 32);
+    // CD with exact support jumps and line search (cd_as.cuh)
+    const int tas = 32 * nw_as;
+    const int gas = (int)ceil_div(m, nw_as);
 #define LAUNCH_AS(N, GT)                                                                               \
   {                                                                                                    \
     CK(cudaFuncSetAttribute(k_cd_as<N, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_as)); \
     k_cd_as<N, GT><<<gas, tas, smem_as, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,              \
-                                                 c.cd_max_sweeps, A64, A32, h->sweeps_dev,            \
+                                                 c.cd_max_sweeps, nmax, A64, A32, h->sweeps_dev,      \
                                                  want_cpart ? h->AT32 : nullptr, h->kp, gstride);     \
   }
 #define CASE_AS(N) \
@@ -794,8 +823,13 @@ static void choose_newton(somf_ctx* h) {
       const size_t ct = (size_t)Tv * ((((size_t)v.kpt * KTS + 31) & ~(size_t)31) + 8);   // T x CTS (bcd_newton.cuh)
       const int ct_in_w = ct <= blk;
       const size_t H = std::max(1, nthr / k);
-      const size_t part = 5 * H * v.kpt;             // stats partials (words)
+      // stats partials (words); after the barrier the same area holds the
+      // cooperative record read's partials (12 rd_h k words)
+      const size_t part = std::max<size_t>(5 * H * v.kpt, (size_t)12 * k);
       const int part_in_cpi = part <= (size_t)k * v.kpt;
+      const size_t avail = part_in_cpi ? (size_t)k * v.kpt : part;
+      const int rd_h = (int)std::max<size_t>(1, std::min<size_t>({avail / (12 * (size_t)k), (size_t)h->nt_ncopy,
+                                                                    (size_t)nthr / k}));
       const size_t base = ((size_t)4 * blk + (size_t)k * v.kpt + (ct_in_w ? 0 : ct) + (part_in_cpi ? 0 : part)) *
                               sizeof(float) + (size_t)cap * sizeof(int) + 16;
       // mask-bit scratch of the draw-ahead: one byte per Philox block of my slice
@@ -823,10 +857,79 @@ static void choose_newton(somf_ctx* h) {
       h->nt_mbits_off = (int)mb_off;
       if (h->cfg.bcd_lam_tol > 0.0) h->nt_lam_tol = h->cfg.bcd_lam_tol;
       h->nt_part_in_cpi = part_in_cpi;
+      h->nt_rd_h = rd_h;
       return;
     }
     return;     // the smallest KPT >= k did not fit: no simultaneous-threshold kernel
   }
+}
+
+#define NB_DECL(K) const void* somf_nb_kernel_##K(int gen, int* T, int* ch);
+NB_DECL(72) NB_DECL(128) NB_DECL(192) NB_DECL(256)
+#undef NB_DECL
+struct NbVariant { int kpt; const void* (*get)(int, int*, int*); };
+static const NbVariant kNbVariants[] = {{72, somf_nb_kernel_72}, {128, somf_nb_kernel_128},
+                                        {192, somf_nb_kernel_192}, {256, somf_nb_kernel_256}};
+
+// The simultaneous-threshold kernel for k <= 256 and for masked rows that do
+// not fit on chip (bcd_big.cuh): the smallest KPT >= k; tile rows TR as many
+// as the shared memory and the 384 threads hold (streamed when a CTA has more).
+static bool choose_big(somf_ctx* h) {
+  const int k = h->cfg.k;
+  const int cap = (int)ceil_div(h->q_cap, h->nsm);
+  const int gen = h->cfg.mu > 0.0 || h->cfg.pos_dict;
+  const int64_t nb = ((h->cfg.row_hi - 1) >> 2) - (h->cfg.row_lo >> 2) + 1;
+  const size_t mb = (size_t)ceil_div(nb, h->nsm) + 16;
+  for (const NbVariant& v : kNbVariants) {
+    if (v.kpt < k) continue;
+    int T = 0, ch = 0;
+    const void* fn = v.get(gen, &T, &ch);
+    cudaFuncAttributes fa{};
+    if (!fn || cudaFuncGetAttributes(&fa, fn) != cudaSuccess) { cudaGetLastError(); return false; }
+    const int kpt = v.kpt, LD = kpt + 1;
+    const size_t cstr = (size_t)nb_cstr(kpt, T);
+    const size_t cbf = ch >= kpt ? (size_t)kpt * T * cstr : (size_t)2 * ch * T * cstr;
+    const size_t limit = 227 * 1024 - fa.sharedSizeBytes - 512;
+    int TR = std::min(cap, 2 * (kNbThreads / T));
+    if (h->cfg.bcd_tile_rows > 0) TR = std::max(2, std::min(TR, (int)h->cfg.bcd_tile_rows));
+    size_t smem = 0;
+    int nthr = 0;
+    for (; TR >= 2; --TR) {
+      nthr = (int)std::max<int64_t>(ceil_div((int64_t)T * ceil_div(TR, 2), 32) * 32, ceil_div(k, 32) * 32);
+      const size_t H = std::max(1, nthr / k);
+      const size_t partw = std::max<size_t>(5 * H * kpt, (size_t)12 * k);
+      const size_t blk = ((size_t)(TR + 1) * LD + 3) & ~(size_t)3;
+      smem = (3 * blk + cbf + ((partw + 3) & ~(size_t)3) + (size_t)((TR + 3) & ~3)) * sizeof(float) + mb;
+      if (smem <= limit && nthr <= kNbThreads) break;
+    }
+    if (TR < 2) return false;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, nthr, smem) != cudaSuccess || occ < 1) {
+      cudaGetLastError();
+      return false;
+    }
+    if (dalloc(&h->nb_cpi, (size_t)kpt * kpt) != cudaSuccess || dalloc(&h->nb_ctg, (size_t)kpt * T * cstr) != cudaSuccess ||
+        dalloc(&h->nb_invc, (size_t)kpt) != cudaSuccess)
+      return false;
+    if (cap > TR && dalloc(&h->nb_scr, (size_t)h->q_cap * 2 * kpt) != cudaSuccess) return false;
+    const int H = std::max(1, nthr / k);
+    const size_t partw = std::max<size_t>(5 * (size_t)H * kpt, (size_t)12 * k);
+    h->nb_rd_h = (int)std::max<size_t>(1, std::min<size_t>({partw / (12 * (size_t)k), (size_t)h->nt_ncopy,
+                                                              (size_t)nthr / k}));
+    h->nb_fn = fn;
+    h->nb_kpt = kpt;
+    h->nb_T = T;
+    h->nb_ch = ch;
+    h->nb_tr = TR;
+    h->nb_threads = nthr;
+    h->nb_smem = smem;
+    return true;
+  }
+  return false;
 }
 
 // Picks the on-chip variant for this handle (h->oc_fn stays null when the
@@ -1043,9 +1146,10 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       !(c.cd_tol > 0.0) || c.cd_max_sweeps < 1 || c.row_hi - c.row_lo > (int64_t)INT32_MAX;
   if (bad) return SOMF_E_ARG;
   if (c.b_mode == SOMF_B_UNBIASED) return SOMF_E_UNSUPPORTED;
-  if (c.bcd_kernel < 0 || c.bcd_kernel > 3) return SOMF_E_ARG;
+  if (c.bcd_kernel < 0 || c.bcd_kernel > 4) return SOMF_E_ARG;
   if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL) return SOMF_E_ARG;
   if (c.estimator < 0 || c.estimator > 2) return SOMF_E_ARG;
+  if (c.bcd_tile_rows < 0) return SOMF_E_ARG;
   if (c.estimator != 0 && (c.n_samples < 1 || !(c.v > 0.0 && c.v <= 1.0))) return SOMF_E_ARG;
   somf_ctx* h = new somf_ctx();
   h->cfg = c;
@@ -1138,8 +1242,9 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
     }
   }
   if (c.bcd_kernel == 0 || c.bcd_kernel == 3) choose_newton(h);
-  if (c.bcd_kernel == 0 ? !h->nt_fn : c.bcd_kernel == 2) choose_onchip(h);
-  if ((c.bcd_kernel == 2 && !h->oc_fn) || (c.bcd_kernel == 3 && !h->nt_fn)) {
+  if ((c.bcd_kernel == 0 && !h->nt_fn) || c.bcd_kernel == 4) choose_big(h);
+  if (c.bcd_kernel == 0 ? (!h->nt_fn && !h->nb_fn) : c.bcd_kernel == 2) choose_onchip(h);
+  if ((c.bcd_kernel == 2 && !h->oc_fn) || (c.bcd_kernel == 3 && !h->nt_fn) || (c.bcd_kernel == 4 && !h->nb_fn)) {
     set_err(h, "requested BCD kernel does not fit: %lld masked rows x k = %d", (long long)h->q_cap, k);
     return fail(SOMF_E_UNSUPPORTED);
   }
@@ -1179,7 +1284,7 @@ SOMF_EXPORT somf_status somf_destroy(somf_handle h) {
                   h->theta_ws, h->oc_acc, h->oc_accmin, h->oc_rho, h->oc_bar,
                   h->lam_ws, h->nt_acc, h->bcd_prof, h->idx_next, h->cnt_next, h->q_next, h->t_next, h->w_next, h->ct_bar, h->cpart, h->AT32,
                   h->ids_dev, h->est_cnt, h->est_stamp, h->est_bcache, h->est_gcache, h->est_beta, h->est_G,
-                  h->Gex, h->gnew};
+                  h->Gex, h->gnew, h->nb_cpi, h->nb_ctg, h->nb_invc, h->nb_scr};
   if (h->st2) cudaStreamDestroy(h->st2);
   if (h->ev_codes) cudaEventDestroy(h->ev_codes);
   if (h->ev_comp) cudaEventDestroy(h->ev_comp);
@@ -1467,12 +1572,12 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   }
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
-    h->kern[3] = h->reducer ? 4 : h->nt_fn ? 3 : h->oc_fn ? 2 : 1;
+    h->kern[3] = h->reducer ? 4 : h->nt_fn ? 3 : h->nb_fn ? 5 : h->oc_fn ? 2 : 1;
     h->kern[5] = h->kern[3] == 3 ? h->nt_T : 0;
     h->kern[6] = h->kern[3] == 3 ? h->nt_M : 0;
     if (h->reducer) {
       if (somf_status s = bcd_sharded(h)) return s;
-    } else if (h->nt_fn) {
+    } else if (h->nt_fn || h->nb_fn) {
       NtArgs na{};
       na.idx = h->idx;
       na.q_dev = h->q_dev;
@@ -1484,8 +1589,8 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.lam_ws = h->lam_ws;
       na.perm = h->perm;
       // pi_t drawn on the host (same Philox words and swaps as atom_perm_cta, R13)
-      host_atom_perm(c.seed, (uint64_t)h->t_host, k, c.perm_cyclic, na.perm_v);
-      na.perm_by_value = 1;
+      if (h->nt_fn) host_atom_perm(c.seed, (uint64_t)h->t_host, k, c.perm_cyclic, na.perm_v);   // (k <= 128)
+      na.perm_by_value = h->nt_fn ? 1 : 0;
       na.k = k;
       na.kp = h->kp;
       na.a = 1.0 - c.mu;
@@ -1512,12 +1617,37 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.rec = h->nt_acc;
       na.ncopy = h->nt_ncopy;
       na.part_in_cpi = h->nt_part_in_cpi;
+      na.rd_h = h->nt_rd_h;
       na.bar = h->oc_bar;
       na.nred_out = h->nred_dev;
       na.err = h->err_dev;
       na.prof = h->prof_on ? h->bcd_prof : nullptr;
-      void* kargs[] = {&na};
-      CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(h->nt_threads), kargs, h->nt_smem, h->st));
+      if (h->nt_fn) {
+        void* kargs[] = {&na};
+        CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(h->nt_threads), kargs, h->nt_smem, h->st));
+      } else {
+        // pi, Cbar in pi order and prescaled per thread parity, then the rounds
+        NbPerm pv{};
+        host_atom_perm(c.seed, (uint64_t)h->t_host, k, c.perm_cyclic, pv.v);
+        k_nb_prep<<<h->nb_kpt, 256, 0, h->st>>>(pv, k, h->nb_kpt, h->nb_T, h->C32, h->C64, h->perm, h->nb_cpi,
+                                                  h->nb_ctg, h->nb_invc);
+        CKL();
+        h->launches[SOMF_PH_BCD] += 1;
+        na.perm = h->perm;
+        na.perm_by_value = 0;
+        na.rd_h = h->nb_rd_h;
+        na.cap_rows = h->nb_tr;
+        NbArgs nba{};
+        nba.nt = na;
+        nba.Cpi = h->nb_cpi;
+        nba.Ctg = h->nb_ctg;
+        nba.invc = h->nb_invc;
+        nba.scr = h->nb_scr;
+        nba.tile_rows = h->nb_tr;
+        nba.ch = h->nb_ch;
+        void* kargs[] = {&nba};
+        CK(cudaLaunchCooperativeKernel(h->nb_fn, dim3(h->nsm), dim3(h->nb_threads), kargs, h->nb_smem, h->st));
+      }
       h->ahead_ready = true;
     } else if (h->oc_fn) {
       OcArgs oa{};
@@ -1790,7 +1920,7 @@ SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {
   return SOMF_OK;
 }
 
-SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->nt_fn ? 3 : h->oc_fn ? 2 : 1) : 0; }
+SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->nt_fn ? 3 : h->nb_fn ? 5 : h->oc_fn ? 2 : 1) : 0; }
 
 SOMF_EXPORT somf_status somf_last_kernels(somf_handle h, int32_t* out) {
   if (!h || !out) return SOMF_E_ARG;

@@ -92,7 +92,7 @@ class Somf:
                  stream=None, debug: bool = False, bcd_kernel: str = "auto",
                  contract_kernel: str = "auto", bbar_kernel: str = "auto", codes_kernel: str = "auto",
                  bcd_lam_tol: float = 0.0, bcd_copies: int = 0,
-                 estimator: str = "a", n_samples: int = 0, v: float = 0.751):
+                 estimator: str = "a", n_samples: int = 0, v: float = 0.751, bcd_tile_rows: int = 0):
         L = lib()
         cfg = _lib.SomfConfig()
         L.somf_config_default(C.byref(cfg))
@@ -111,7 +111,7 @@ class Somf:
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         cfg.stream = _stream_ptr(self.stream)
         cfg.debug = int(debug)
-        cfg.bcd_kernel = {"auto": 0, "global": 1, "onchip": 2, "newton": 3}[bcd_kernel]
+        cfg.bcd_kernel = {"auto": 0, "global": 1, "onchip": 2, "newton": 3, "big": 4}[bcd_kernel]
         cfg.contract_kernel = CONTRACT_KERNELS[contract_kernel]
         cfg.bbar_kernel = BBAR_KERNELS[bbar_kernel]
         cfg.codes_kernel = CODES_KERNELS[codes_kernel]
@@ -120,6 +120,7 @@ class Somf:
         cfg.estimator = {"a": 0, "b": 1, "c": 2}[estimator]
         cfg.n_samples = n_samples
         cfg.v = v
+        cfg.bcd_tile_rows = bcd_tile_rows
         h = C.c_void_p()
         st = L.somf_create(C.byref(cfg), C.byref(h))
         if st != 0:
@@ -286,7 +287,7 @@ class Somf:
 
     @property
     def bcd_variant(self) -> str:
-        return {1: "global", 2: "onchip", 3: "newton"}.get(lib().somf_bcd_variant(self._h), "?")
+        return {1: "global", 2: "onchip", 3: "newton", 5: "big"}.get(lib().somf_bcd_variant(self._h), "?")
 
     def last_kernels(self):
         """Kernel variants of the last partial_fit (somf_last_kernels): names
@@ -296,7 +297,7 @@ class Somf:
         inv = lambda d, x: {i: n for n, i in d.items()}.get(int(x), "none")  # noqa: E731
         return dict(contract=inv(CONTRACT_KERNELS, v[0]), codes=inv(CODES_KERNELS, v[1]),
                     bbar=inv(BBAR_KERNELS, v[2]),
-                    bcd={1: "global", 2: "onchip", 3: "newton", 4: "sharded"}.get(int(v[3]), "none"),
+                    bcd={1: "global", 2: "onchip", 3: "newton", 4: "sharded", 5: "big"}.get(int(v[3]), "none"),
                     bbar_complement=bool(v[4]), bcd_group=(int(v[5]), int(v[6])))
 
     def last_step_info(self):

@@ -46,7 +46,7 @@ def test_sass_is_sm100a(libpath):
 def test_library_loads_and_binding_matches(libpath):
     from paper_1701_05363_b200 import _lib
     L = _lib.load(libpath)
-    assert L.somf_abi_version() == 2
+    assert L.somf_abi_version() == 3
     names = {n for n, _, _ in _lib.SIGNATURES}
     assert names == set(_declared())
     import ctypes as C

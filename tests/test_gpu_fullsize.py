@@ -237,7 +237,11 @@ def test_bbar_variants(somf, name, variant):
 @pytest.mark.parametrize("variant", ["ridge", "cd_jump", "cd"])
 @pytest.mark.parametrize("name", list(VARIANT_CASES))
 def test_codes_variants(somf, name, variant):
-    ora, gpu, batch, _ = _vpair(somf, name, codes_kernel=variant)
+    # plain CD stops on max |delta| <= cd_tol; on the ill-conditioned NMF Gram
+    # (cond ~1e4) its contraction is ~1 - 1e-3 per sweep, so the forced plain
+    # variant runs with a tolerance that bounds the error at that rate
+    extra = dict(cd_tol=1e-11, cd_max_sweeps=50000) if variant == "cd" and "k128" in name else {}
+    ora, gpu, batch, _ = _vpair(somf, name, codes_kernel=variant, **extra)
     out, _ = _forced_step(somf, ora, gpu, batch)
     assert gpu.last_kernels()["codes"] == variant
     p, k, eta, kw, _ = VARIANT_CASES[name]
@@ -277,7 +281,7 @@ def test_forced_variant_that_does_not_apply_fails_loudly(somf):
 # ---------------------------------------------------------------------------
 # determinism: fixed-point grid sums => bit-identical reruns, any copy count
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("bcd_kernel", ["newton", "onchip"])
+@pytest.mark.parametrize("bcd_kernel", ["newton", "onchip", "big"])
 def test_bcd_bitwise_deterministic(somf, bcd_kernel):
     p, k, eta, kw, kind = VARIANT_CASES["ridge_l1"]
     X = _vdata(kind, p, k + 6 * eta)
@@ -298,11 +302,11 @@ def test_bcd_bitwise_deterministic(somf, bcd_kernel):
 # ---------------------------------------------------------------------------
 def test_recurring_empty_masks(somf):
     p, k, eta = 64, 4, 5
-    kw = dict(lam=0.1, nu=1.0, mu=0.0, r=64.0)       # P(S_t empty) = (63/64)^64 ~ 0.37
+    kw = dict(lam=0.1, nu=1.0, mu=0.0, r=64.0)       # P(S_t empty) = (63/64)^64 ~ 0.37; seed 3: 14 of 40
     X = f32(synth.tiny_dictionary_learning(p=p, n=k + 40 * eta, seed=2)[0])
-    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=1, **kw))
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=3, **kw))
     ora.set_components(X[:, :k])
-    gpu = somf.Somf(p, k, eta, seed=1, debug=True, bcd_kernel="newton", **kw)
+    gpu = somf.Somf(p, k, eta, seed=3, debug=True, bcd_kernel="newton", **kw)
     gpu.set_components(cuda(X[:, :k]))
     n_empty = 0
     for t in range(40):
@@ -318,7 +322,7 @@ def test_recurring_empty_masks(somf):
                                             st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
     assert n_empty >= 5
     q, idx = gpu.next_mask()
-    assert np.array_equal(idx, ostreams.mask_rows(1, ora.t + 1, p, 64.0))
+    assert np.array_equal(idx, ostreams.mask_rows(3, ora.t + 1, p, 64.0))
 
 
 # ---------------------------------------------------------------------------

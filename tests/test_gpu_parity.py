@@ -122,6 +122,10 @@ def _data(kind, p, n, seed=0):
 
 def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
     p, k, eta, kw, kind = CASES[name]
+    gkw = {}
+    if bcd_kernel == "big_streamed":
+        # the k <= 256 kernel with 4-row tiles: every CTA streams its rows
+        bcd_kernel, gkw = "big", dict(bcd_tile_rows=4)
     X = _data(kind, p, k + (t0 + 3) * eta)
     ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=seed, **kw))
     ora.set_components(X[:, :k])
@@ -129,18 +133,18 @@ def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
         ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
     # the oracle continues from the float32-rounded state the GPU holds
     ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
-    gpu = somf.Somf(p, k, eta, seed=seed, debug=True, bcd_kernel=bcd_kernel, **kw)
+    gpu = somf.Somf(p, k, eta, seed=seed, debug=True, bcd_kernel=bcd_kernel, **kw, **gkw)
     gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
     return ora, gpu, X, (p, k, eta)
 
 
-@pytest.mark.parametrize("bcd_kernel", ["global", "onchip", "newton"])
+@pytest.mark.parametrize("bcd_kernel", ["global", "onchip", "newton", "big", "big_streamed"])
 @pytest.mark.parametrize("name", list(CASES))
 def test_one_step_parity(somf, name, bcd_kernel):
     if bcd_kernel == "newton" and CASES[name][1] > 128:
         pytest.skip("simultaneous-threshold kernel covers k <= 128")
     ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel=bcd_kernel)
-    assert gpu.bcd_variant == bcd_kernel
+    assert gpu.bcd_variant == bcd_kernel.replace("_streamed", "")
     batch = X[:, k + 5 * eta:k + 6 * eta]
     out = ora.partial_fit(batch)
     gpu.partial_fit(cuda(batch))
@@ -243,15 +247,16 @@ def test_set_components_projects_and_slacks(somf):
         assert st["t"] == 0 and np.abs(st["Cbar"]).max() == 0 and np.abs(st["Bbar"]).max() == 0
 
 
+@pytest.mark.parametrize("bcd_kernel", ["newton", "big", "big_streamed"])
 @pytest.mark.parametrize("name", ["ridge_l1_fmri_small", "enet_enet", "nmf_small"])
-def test_draw_ahead_multi_step(somf, name):
+def test_draw_ahead_multi_step(somf, name, bcd_kernel):
     """The simultaneous-threshold BCD kernel draws M_{t+1}, pi_{t+1}, t+1 and
     w_{t+1} while it runs; the next step consumes them.  Three
     consecutive steps from a loaded state: after each, the mask the handle
     reports for t+1 is the oracle's bit for bit, and the state after the
     three steps matches the oracle (each step is pinned one by one in
     test_one_step_parity)."""
-    ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel="newton")
+    ora, gpu, X, (p, k, eta) = _pair(somf, name, bcd_kernel=bcd_kernel)
     r = CASES[name][3]["r"]
     for s in range(3):
         batch = X[:, k + (5 + s) * eta:k + (6 + s) * eta]
@@ -275,8 +280,9 @@ def test_draw_ahead_multi_step(somf, name):
 # trajectory: objective after 100 iterations
 # ---------------------------------------------------------------------------
 @pytest.mark.parametrize("name,iters", [("cfgA_ridge_l1", 100), ("ridge_l1_fmri_small", 100),
-                                        ("nmf_small", 100), ("enet_enet", 60)])
-@pytest.mark.parametrize("bcd_kernel", ["onchip", "newton"])
+                                        ("nmf_small", 100), ("enet_enet", 100),
+                                        ("lasso_l2_hyper_small", 100)])
+@pytest.mark.parametrize("bcd_kernel", ["onchip", "newton", "big"])
 def test_trajectory_objective(somf, name, iters, bcd_kernel):
     p, k, eta, kw, kind = CASES[name]
     X = _data(kind, p, k + iters * eta + 200, seed=1)
