@@ -549,7 +549,8 @@ def run_somf(args):
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
         roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
                                          if ph not in ("launches", "unconverged_per_round", "frozen_prefix_per_round", "ridge",
-                                                       "setup_split")}
+                                                       "setup_split", "update_split")}
+        roof["bcd_update_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["update_split"].items()}
         roof["ridge_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["ridge"].items()}
         roof["bcd_setup_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["setup_split"].items()}
         unc = [u / bcd_cyc["launches"] for u in bcd_cyc["unconverged_per_round"]]

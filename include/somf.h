@@ -120,7 +120,7 @@ typedef struct somf_config {
                              tolerance on each projection multiplier between
                              two rounds (0 = default 1e-5)     */
   int32_t bcd_copies;     /* simultaneous-threshold Alg. 4: copies of each
-                             per-atom grid accumulator (1..16, 0 = 8); a
+                             per-atom grid accumulator (1..16, 0 = 2); a
                              performance knob only: the sums are fixed-point
                              integers, so results are bit-identical for any
                              value and any CTA arrival order                 */

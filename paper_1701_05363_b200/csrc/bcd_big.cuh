@@ -30,24 +30,25 @@ __host__ __device__ constexpr int nb_kts(int kpt, int t) { return ((kpt / t) + 3
 __host__ __device__ constexpr int nb_cstr(int kpt, int t) { return (nb_kts(kpt, t) % 8 == 0) ? nb_kts(kpt, t) + 4 : nb_kts(kpt, t); }
 
 struct NbArgs {
-  NtArgs nt;                // thresholds, records, barrier, draw-ahead (perm read from nt.perm)
-  const float* Cpi;         // k x KPT: Cbar in pi order (row p = atom pi(p)), zero padded
-  const float* Ctg;         // KPT x T x CSTR: prescaled Cbar rows per parity (k_nb_prep)
+  const float* Cpi;         // KPT x KPT, pi order: Cbar (NbRec mode) or Cbar prescaled by
+                            // 1 / c_ll per column l (blocked mode)
+  const float* Ctg;         // KPT x T x CSTR: prescaled Cbar rows per parity (NbRec mode)
   const float* invc;        // KPT: 1 / c_pp in pi order (0 for dead atoms)
-  float* scr;               // streamed tiles: per masked row 2 x KPT floats (d_old | R0), pi order
-  int tile_rows;            // TR: rows per tile (rows of a CTA beyond TR => streamed)
+  float* scr;               // per masked row 2 x KPT floats (d_old | R0), pi order: streamed
+                            // tiles (NbRec mode) / every tile (blocked mode)
+  int tile_rows;            // TR: rows per tile (rows of a CTA beyond TR => several tiles)
   int ch;                   // positions per Cbar chunk (== KPT: resident)
 };
 
-// pi in the device array, Cbar permuted (k x KPT) and prescaled per parity
-// (KPT x T x CSTR), 1/c_pp; one CTA per position row.  Dead atoms (R10) get
-// 1/c = 0 (their residual is zero, so d stays d_old).
+// pi in the device array, Cbar permuted and prescaled, 1/c_pp; one CTA per
+// position row.  Dead atoms (R10) get 1/c = 0 (their residual is zero, so d
+// stays d_old).  blocked: Cpi[p][l] = c_{pi p, pi l} / c_{pi l, pi l} and no
+// Ctg; else Cpi unscaled and Ctg = the parity layout of the prescaled rows.
 struct NbPerm { int32_t v[kNbMaxK]; };
-static __global__ void k_nb_prep(NbPerm pi, int k, int kpt, int T, const float* __restrict__ C32,
-                          const double* __restrict__ C64, int32_t* __restrict__ perm, float* __restrict__ Cpi,
-                          float* __restrict__ Ctg, float* __restrict__ invc) {
+static __global__ void k_nb_prep(NbPerm pi, int k, int kpt, int T, int blocked, const float* __restrict__ C32,
+                                 const double* __restrict__ C64, int32_t* __restrict__ perm, float* __restrict__ Cpi,
+                                 float* __restrict__ Ctg, float* __restrict__ invc) {
   const int p = blockIdx.x;                    // position (row of Cpi / Ctg)
-  const int kt = kpt / T, kts = nb_kts(kpt, T), cstr = nb_cstr(kpt, T);
   __shared__ double dmax_s;
   __shared__ float inv_s[kNbMaxK];
   if (threadIdx.x < 32) {
@@ -72,8 +73,12 @@ static __global__ void k_nb_prep(NbPerm pi, int k, int kpt, int T, const float* 
       invc[l] = inv_s[l];
     }
   const int jp = p < k ? pi.v[p] : 0;
-  for (int l = threadIdx.x; l < kpt; l += blockDim.x)
-    Cpi[(int64_t)p * kpt + l] = (p < k && l < k) ? C32[(int64_t)jp * k + pi.v[l]] : 0.f;
+  for (int l = threadIdx.x; l < kpt; l += blockDim.x) {
+    const float c = (p < k && l < k) ? C32[(int64_t)jp * k + pi.v[l]] : 0.f;
+    Cpi[(int64_t)p * kpt + l] = blocked ? c * inv_s[l] : c;
+  }
+  if (blocked) return;
+  const int kt = kpt / T, kts = nb_kts(kpt, T), cstr = nb_cstr(kpt, T);
   for (int e = threadIdx.x; e < T * cstr; e += blockDim.x) {
     const int t = e / cstr, i = e % cstr;
     const int l = i * T + t;
@@ -159,24 +164,204 @@ struct NbRec<KPT, T, M, kGen, CH, END, END> {
                                              float*, const float*, const NtPar<kGen>*) {}
 };
 
-// shared-memory layout (floats unless noted), host mirror: nb_smem_bytes
-//   Dold, Rini, V   3 x (TR + 1) x LD     (LD = KPT + 1; row TR = spare zeros)
-//   cbuf            2 x CHB (streamed) or KPT x T x CSTR (resident)
-//   part            max(5 H KPT, 12 k) words (stats partials / record read)
-//   rows_s          TR ints; mbits: one byte per Philox block of my slice
-template <int KPT, int T>
-__host__ __device__ constexpr size_t nb_cbuf_floats(int ch) {
-  return ch >= KPT ? (size_t)KPT * T * nb_cstr(KPT, T) : (size_t)2 * ch * T * nb_cstr(KPT, T);
+// ---------------------------------------------------------------------------
+// Blocked recurrence (k > 128: the unrolled per-position code of NbRec would
+// not fit the instruction cache).  Positions in chunks of 16:
+//   (a) one thread per masked row runs the chunk's 16 positions in order (its
+//       16 residuals and d_old in registers, the chunk's 16 x 16 block of the
+//       prescaled Cbar broadcast from shared memory), writes v and
+//       delta = d - d_old of the 16 positions;
+//   (b) the rows' later residuals take the chunk's rank-16 update
+//       R[:, l] -= delta[:, chunk] Cpre[chunk, l] (l past the chunk), register
+//       tiles of 2 rows x 4 positions over all threads.
+// Same arithmetic as the sequential recurrence, grouped.
+// ---------------------------------------------------------------------------
+constexpr int kNbCB = 16;        // positions per chunk
+
+// R[r][l] -= sum_j S[r][j] C[j][l]  for r < nr, l in [l0, l1) (multiples of 4),
+// j < 16; S rows at stride lds (16-byte aligned), C the 16 chunk rows (stride
+// KPT).  tid / nthr: this thread's share of the (row pair, 4 positions) items.
+template <int KPT>
+__device__ __forceinline__ void nb_rank16(float* __restrict__ R, int ldr, const float* __restrict__ S, int lds,
+                                          const float* __restrict__ C, int nr, int l0, int l1, int tid, int nthr) {
+  const int nq = (l1 - l0) >> 2, npair = (nr + 1) >> 1;
+  for (int it = tid; it < npair * nq; it += nthr) {
+    const int r0 = 2 * (it / nq), lq = l0 + 4 * (it % nq);
+    const bool two = r0 + 1 < nr;
+    float4 a0 = *reinterpret_cast<const float4*>(R + (size_t)r0 * ldr + lq);
+    float4 a1 = two ? *reinterpret_cast<const float4*>(R + (size_t)(r0 + 1) * ldr + lq) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const float4 s0 = *reinterpret_cast<const float4*>(S + (size_t)r0 * lds + 4 * j4);
+      const float4 s1 = two ? *reinterpret_cast<const float4*>(S + (size_t)(r0 + 1) * lds + 4 * j4)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float sv0[4] = {s0.x, s0.y, s0.z, s0.w}, sv1[4] = {s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 c = *reinterpret_cast<const float4*>(C + (size_t)(4 * j4 + e) * KPT + lq);
+        a0.x = fmaf(-sv0[e], c.x, a0.x);
+        a0.y = fmaf(-sv0[e], c.y, a0.y);
+        a0.z = fmaf(-sv0[e], c.z, a0.z);
+        a0.w = fmaf(-sv0[e], c.w, a0.w);
+        a1.x = fmaf(-sv1[e], c.x, a1.x);
+        a1.y = fmaf(-sv1[e], c.y, a1.y);
+        a1.z = fmaf(-sv1[e], c.z, a1.z);
+        a1.w = fmaf(-sv1[e], c.w, a1.w);
+      }
+    }
+    *reinterpret_cast<float4*>(R + (size_t)r0 * ldr + lq) = a0;
+    if (two) *reinterpret_cast<float4*>(R + (size_t)(r0 + 1) * ldr + lq) = a1;
+  }
 }
 
-template <int KPT, int T, int M, bool kGen, int CH>
+// chunk c of the prescaled Cbar (16 rows x KPT) into buffer c & 1 (cp.async)
+template <int KPT>
+__device__ __forceinline__ void nb_load_chunk(float* cbuf, const float* __restrict__ Cpre, int c, int tid, int nthr) {
+  float* dst = cbuf + (c & 1) * kNbCB * KPT;
+  const float* src = Cpre + (size_t)c * kNbCB * KPT;
+  for (int e = tid; e < kNbCB * KPT / 4; e += nthr) nb_cp16(dst + 4 * e, src + 4 * e);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// one recurrence pass of the blocked mode over the tile's rows (R: the
+// tile's R0, overwritten; Dold; V receives v; Dl: nr x 16 deltas)
+template <int KPT, bool kGen>
+__device__ __forceinline__ void nb_blk_pass(float* R, const float* Dold, float* V, float* Dl, float* cbuf,
+                                            const float* __restrict__ Cpre, const NtPar<kGen>* par, int nr,
+                                            int tid, int nthr) {
+  constexpr int LDB = KPT + 4, NC = KPT / kNbCB;
+  nb_load_chunk<KPT>(cbuf, Cpre, 0, tid, nthr);
+#pragma unroll 1
+  for (int c = 0; c < NC; ++c) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();                                   // chunk c landed; chunk c - 1 consumed
+    if (c + 1 < NC) nb_load_chunk<KPT>(cbuf, Cpre, c + 1, tid, nthr);
+    const float* Cb = cbuf + (c & 1) * kNbCB * KPT;
+    const int p0 = c * kNbCB;
+    if (tid < nr) {
+      float rr[kNbCB], dd[kNbCB], vv[kNbCB], dl[kNbCB];
+      const float* Rr = R + (size_t)tid * LDB + p0;
+      const float* Dr = Dold + (size_t)tid * LDB + p0;
+#pragma unroll
+      for (int i4 = 0; i4 < kNbCB / 4; ++i4) {
+        const float4 x = *reinterpret_cast<const float4*>(Rr + 4 * i4);
+        const float4 y = *reinterpret_cast<const float4*>(Dr + 4 * i4);
+        rr[4 * i4] = x.x; rr[4 * i4 + 1] = x.y; rr[4 * i4 + 2] = x.z; rr[4 * i4 + 3] = x.w;
+        dd[4 * i4] = y.x; dd[4 * i4 + 1] = y.y; dd[4 * i4 + 2] = y.z; dd[4 * i4 + 3] = y.w;
+      }
+#pragma unroll
+      for (int j = 0; j < kNbCB; ++j) {
+        const NtPar<kGen> pr = par[p0 + j];
+        const float u = rr[j] + dd[j];
+        vv[j] = pr.v_of(u);
+        const float delta = pr.d_of(u) - dd[j];
+        dl[j] = delta;
+        const float* crow = Cb + (size_t)j * KPT + p0;
+#pragma unroll
+        for (int i4 = (j + 1) / 4; i4 < kNbCB / 4; ++i4) {
+          const float4 cc = *reinterpret_cast<const float4*>(crow + 4 * i4);
+          const float cv[4] = {cc.x, cc.y, cc.z, cc.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (4 * i4 + e > j) rr[4 * i4 + e] = fmaf(-delta, cv[e], rr[4 * i4 + e]);
+        }
+      }
+      float* Vr = V + (size_t)tid * LDB + p0;
+      float* Dlr = Dl + (size_t)tid * kNbCB;
+#pragma unroll
+      for (int i4 = 0; i4 < kNbCB / 4; ++i4) {
+        *reinterpret_cast<float4*>(Vr + 4 * i4) = make_float4(vv[4 * i4], vv[4 * i4 + 1], vv[4 * i4 + 2], vv[4 * i4 + 3]);
+        *reinterpret_cast<float4*>(Dlr + 4 * i4) = make_float4(dl[4 * i4], dl[4 * i4 + 1], dl[4 * i4 + 2], dl[4 * i4 + 3]);
+      }
+    }
+    __syncthreads();
+    if (c + 1 < NC) nb_rank16<KPT>(R, LDB, Dl, kNbCB, Cb, nr, p0 + kNbCB, KPT, tid, nthr);
+  }
+  __syncthreads();
+}
+
+// shared-memory layout (floats unless noted), host mirror in somf_capi.cu
+//   NbRec mode:   Dold, Rini, V   3 x (TR + 1) x (KPT + 1); cbuf 2 x CHB or KPT x T x CSTR
+//   blocked mode: Dold, R, V      3 x (TR + 1) x (KPT + 4); cbuf 2 x 16 x KPT; Dl (TR + 1) x 16
+//   part          max(5 H KPT, 12 k) words (stats partials / record read)
+//   rows_s        TR ints; mbits: one byte per Philox block of my slice
+template <int KPT, int T>
+__host__ __device__ constexpr size_t nb_cbuf_floats(int ch, bool blk) {
+  return blk ? (size_t)2 * kNbCB * KPT
+             : ch >= KPT ? (size_t)KPT * T * nb_cstr(KPT, T) : (size_t)2 * ch * T * nb_cstr(KPT, T);
+}
+
+// One recurrence pass over tile tl: loads it from the scratch when streamed,
+// leaves v in V; returns the tile's row count.
+template <int KPT, int T, int M, bool kGen, int CH, bool kBlk>
+__device__ __forceinline__ int nb_tile_pass(const float* __restrict__ scr, const float* __restrict__ Cpi,
+                                            const float* __restrict__ Ctg, int tl, int TR, int nr_all, int64_t lo,
+                                            bool streamed, float* Dold, float* Rini, float* V, float* cbuf, float* Dl,
+                                            const NtPar<kGen>* par, int g, int tq, int ngroups, int tid, int nthr) {
+  constexpr int LD = kBlk ? KPT + 4 : KPT + 1;
+  constexpr int KT = KPT / T;
+  constexpr int CSTR = nb_cstr(KPT, T);
+  const int r0 = tl * TR, nr = min(TR, nr_all - r0);
+  if (streamed) {
+    __syncthreads();                               // V / Dold / Rini of the previous tile consumed
+    const float* sc = scr + (size_t)(lo + r0) * 2 * KPT;
+    constexpr int q4 = KPT / 4;
+    for (int e = tid; e < nr * 2 * q4; e += nthr) {
+      const int row = e / (2 * q4), c = e % (2 * q4);
+      float* dst = c < q4 ? Dold + (size_t)row * LD + 4 * c : Rini + (size_t)row * LD + 4 * (c - q4);
+      const float4 v4 = __ldcg(reinterpret_cast<const float4*>(sc + (size_t)row * 2 * KPT + 4 * c));
+      if constexpr (kBlk) {
+        *reinterpret_cast<float4*>(dst) = v4;
+      } else {
+        dst[0] = v4.x;
+        dst[1] = v4.y;
+        dst[2] = v4.z;
+        dst[3] = v4.w;
+      }
+    }
+  }
+  if constexpr (kBlk) {
+    __syncthreads();
+    nb_blk_pass<KPT, kGen>(Rini, Dold, V, Dl, cbuf, Cpi, par, nr, tid, nthr);
+    return nr;
+  } else {
+    if (CH < KPT) {
+      // chunk 0 of the prescaled Cbar into buffer 0
+      constexpr int n4 = CH * T * CSTR / 4;
+      for (int e = tid; e < n4; e += nthr) nb_cp16(cbuf + 4 * e, Ctg + 4 * e);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    __syncthreads();
+    int rowx[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) rowx[m] = (g < ngroups && g * M + m < nr) ? g * M + m : TR;
+    const int vstride = rowx[M - 1] - rowx[0];
+    float Do[M][KT], R[M][KT];
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
+        R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
+      }
+    // threads past the groups: same code on the spare row (their v goes to the spare row)
+    constexpr int H1 = KPT > 128 ? 128 : KPT;
+    NbRec<KPT, T, M, kGen, CH, 0, H1>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, Ctg, par);
+    if constexpr (KPT > 128)
+      NbRec<KPT, T, M, kGen, CH, H1, KPT>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, Ctg, par);
+    __syncthreads();
+    return nr;
+  }
+}
+
+template <int KPT, int T, int M, bool kGen, int CH, bool kBlk>
 __global__ void __launch_bounds__(kNbThreads, 1)
-k_bcd_big(NbArgs A) {
-  const NtArgs& P = A.nt;
-  constexpr int LD = KPT + 1;
+k_bcd_big(NtArgs P, NbArgs A) {
+  constexpr int LD = kBlk ? KPT + 4 : KPT + 1;
   constexpr int KT = KPT / T;
   constexpr int CSTR = nb_cstr(KPT, T);
   static_assert(KPT % T == 0 && M == 2, "groups of T lanes x 2 rows");
+  static_assert(!kBlk || KPT % kNbCB == 0, "blocked mode: KPT a multiple of 16");
   extern __shared__ __align__(16) float nb_smem[];
   __shared__ __align__(16) NtPar<kGen> par_s[2][KPT];
   __shared__ double lam_s[KPT], rho_s[KPT];
@@ -194,9 +379,10 @@ k_bcd_big(NbArgs A) {
   const int nr_all = (int)(hi - lo);
   const int TR = A.tile_rows;
   const int ntile = nr_all > 0 ? (nr_all + TR - 1) / TR : 0;
-  const bool streamed = ntile > 1;
+  const bool streamed = kBlk || ntile > 1;          // tiles re-read from the scratch every round
   // host sizing errors (uniform over the CTAs: every CTA returns before any barrier)
-  if (T * ((TR + M - 1) / M) > nthr || nthr < k || ((q + G - 1) / G > TR && A.scr == nullptr)) {
+  if ((!kBlk && T * ((TR + M - 1) / M) > nthr) || (kBlk && TR > nthr) || nthr < k ||
+      ((kBlk || (q + G - 1) / G > TR) && A.scr == nullptr)) {
     if (tid == 0) atomicExch(P.err, 2);
     return;
   }
@@ -205,15 +391,17 @@ k_bcd_big(NbArgs A) {
   float* Rini = Dold + blk;
   float* V = Rini + blk;
   float* cbuf = V + blk;
-  const size_t cbf = nb_cbuf_floats<KPT, T>(CH);
+  const size_t cbf = nb_cbuf_floats<KPT, T>(CH, kBlk);
+  float* Dl = cbuf + cbf;                                       // blocked mode: (TR + 1) x 16
+  const size_t dlf = kBlk ? (size_t)(TR + 1) * kNbCB : 0;
   const int H = max(1, nthr / max(k, 1));
   const size_t partw = (size_t)5 * H * KPT > (size_t)12 * k ? (size_t)5 * H * KPT : (size_t)12 * k;
-  unsigned* pcn = reinterpret_cast<unsigned*>(cbuf + cbf);
+  unsigned* pcn = reinterpret_cast<unsigned*>(Dl + dlf);
   float* ps1 = reinterpret_cast<float*>(pcn + H * KPT);
   float* ps2 = ps1 + H * KPT;
   unsigned* pmn = reinterpret_cast<unsigned*>(ps2 + H * KPT);
   unsigned* pmx = pmn + H * KPT;
-  int* rows_s = reinterpret_cast<int*>(cbuf + cbf + ((partw + 3) & ~(size_t)3));
+  int* rows_s = reinterpret_cast<int*>(Dl + dlf + ((partw + 3) & ~(size_t)3));
   uint8_t* mbits_s = reinterpret_cast<uint8_t*>(rows_s + ((TR + 3) & ~3));
   const double a = P.a, b = P.b;
   if (tid == 0) mcnt_s = 0;
@@ -242,8 +430,8 @@ k_bcd_big(NbArgs A) {
     }
     acc1_s[p] = acc2_s[p] = 0.0;
   }
-  // resident prescaled Cbar: staged once
-  if (CH >= KPT) {
+  // resident prescaled Cbar (NbRec mode): staged once
+  if (!kBlk && CH >= KPT) {
     const int n4 = (int)(cbf / 4);
     for (int e = tid; e < n4; e += nthr) nb_cp16(cbuf + 4 * e, A.Ctg + 4 * e);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -294,14 +482,28 @@ k_bcd_big(NbArgs A) {
       Dold[(size_t)row * LD + p] = p < k ? V[(size_t)row * kp + jmap_s[p]] : 0.f;
     }
     __syncthreads();
-    // Bbar in pi order into V (row stride LD)
+    // Bbar in pi order into V (row stride LD); blocked mode: prescaled by 1 / c_pp
     for (int e = tid; e < nr * KPT; e += nthr) {
       const int row = e / KPT, p = e % KPT;
-      V[(size_t)row * LD + p] = p < k ? Rini[(size_t)row * kp + jmap_s[p]] : 0.f;
+      const float bb = p < k ? Rini[(size_t)row * kp + jmap_s[p]] : 0.f;
+      V[(size_t)row * LD + p] = kBlk ? bb * A.invc[p] : bb;
     }
     __syncthreads();
-    // R0 = (Bbar - Dold Cpi) * invc : RT rows x 8 positions per item
-    {
+    if constexpr (kBlk) {
+      // R0 = Bbar / c - Dold Cpre: rank-16 updates over every chunk of positions
+      for (int e = tid; e < nr * LD; e += nthr) Rini[e] = V[e];
+      int c = 0;
+      nb_load_chunk<KPT>(cbuf, A.Cpi, 0, tid, nthr);
+#pragma unroll 1
+      for (; c < KPT / kNbCB; ++c) {
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        if (c + 1 < KPT / kNbCB) nb_load_chunk<KPT>(cbuf, A.Cpi, c + 1, tid, nthr);
+        nb_rank16<KPT>(Rini, LD, Dold + c * kNbCB, LD, cbuf + (c & 1) * kNbCB * KPT, nr, 0, KPT, tid, nthr);
+      }
+      __syncthreads();
+    } else {
+      // R0 = (Bbar - Dold Cpi) * invc : RT rows x 8 positions per item
       constexpr int RT = 4;
       const int nrb = (nr + RT - 1) / RT, npb = (k + 7) / 8;
       for (int it = tid; it < nrb * npb; it += nthr) {
@@ -333,11 +535,11 @@ k_bcd_big(NbArgs A) {
           }
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
     for (int e = tid; e < nr * LD; e += nthr) {                 // padding positions of R0
-      const int row = e / LD, p = e % LD;
-      if (p >= k) Rini[(size_t)row * LD + p] = 0.f;
+      const int p = e % LD;
+      if (p >= k) Rini[e] = 0.f;
     }
     // radii sums of this tile (fp64, fixed order: tile by tile)
     {
@@ -374,58 +576,13 @@ k_bcd_big(NbArgs A) {
     const bool ok = fx_red(rr + 1, acc1_s[tid]) & fx_red(rr + 3, acc2_s[tid]);
     if (!ok) atomicExch(P.err, 6);
   }
-  if (CH >= KPT) asm volatile("cp.async.wait_all;" ::: "memory");
+  if (!kBlk && CH >= KPT) asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   if (P.idx_next && tid == 0) P.cnt_next[blockIdx.x] = mcnt_s;   // before round 0's barrier
 
-  // my rows within a tile: M consecutive rows of group g; rows >= nr use the spare row
+  // my rows within a tile (NbRec mode): M consecutive rows of group g; rows >= nr use the spare row
   const int g = tid / T, tq = tid % T;
   const int ngroups = (TR + M - 1) / M;
-
-  // one recurrence pass over tile tl (loads it first when streamed); leaves v in V
-  auto pass = [&](int tl, const NtPar<kGen>* par) {
-    const int r0 = tl * TR, nr = min(TR, nr_all - r0);
-    if (streamed) {
-      __syncthreads();                               // V / Dold / Rini of the previous tile consumed
-      const float* sc = A.scr + (size_t)(lo + r0) * 2 * KPT;
-      constexpr int q4 = KPT / 4;
-      for (int e = tid; e < nr * 2 * q4; e += nthr) {
-        const int row = e / (2 * q4), c = e % (2 * q4);
-        float* dst = c < q4 ? Dold + (size_t)row * LD + 4 * c : Rini + (size_t)row * LD + 4 * (c - q4);
-        const float4 v4 = __ldcg(reinterpret_cast<const float4*>(sc + (size_t)row * 2 * KPT + 4 * c));
-        dst[0] = v4.x;
-        dst[1] = v4.y;
-        dst[2] = v4.z;
-        dst[3] = v4.w;
-      }
-    }
-    if (CH < KPT) {
-      // chunk 0 of the prescaled Cbar into buffer 0
-      constexpr int n4 = CH * T * CSTR / 4;
-      for (int e = tid; e < n4; e += nthr) nb_cp16(cbuf + 4 * e, A.Ctg + 4 * e);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    __syncthreads();
-    int rowx[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) rowx[m] = (g < ngroups && g * M + m < nr) ? g * M + m : TR;
-    const int vstride = rowx[M - 1] - rowx[0];
-    float Do[M][KT], R[M][KT];
-#pragma unroll
-    for (int m = 0; m < M; ++m)
-#pragma unroll
-      for (int i = 0; i < KT; ++i) {
-        Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
-        R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
-      }
-    // threads past the groups: same code on the spare row (their v goes to the spare row)
-    constexpr int H1 = KPT > 128 ? 128 : KPT;
-    NbRec<KPT, T, M, kGen, CH, 0, H1>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, A.Ctg, par);
-    if constexpr (KPT > 128)
-      NbRec<KPT, T, M, kGen, CH, H1, KPT>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, A.Ctg, par);
-    __syncthreads();
-    return nr;
-  };
 
   unsigned nbar = 0;
   int round = 0, cur = 0;
@@ -444,7 +601,8 @@ k_bcd_big(NbArgs A) {
       acc1_s[p] = acc2_s[p] = 0.0;
     }
     for (int tl = 0; tl < ntile; ++tl) {
-      const int nr = pass(tl, par_s[cur]);
+      const int nr = nb_tile_pass<KPT, T, M, kGen, CH, kBlk>(A.scr, A.Cpi, A.Ctg, tl, TR, nr_all, lo, streamed, Dold, Rini, V, cbuf,
+                                                            Dl, par_s[cur], g, tq, ngroups, tid, nthr);
       // per-atom statistics of the tile, added to the CTA sums in tile order
       if (tid < H * k) {
         const int p = tid % k, h = tid / k;
@@ -501,9 +659,10 @@ k_bcd_big(NbArgs A) {
     }
     ++nbar;
     nt_barrier(P.bar, nbar * G);
-    if (blockIdx.x == 0) {
-      const int rz = (round + 2) % kNtRing;
-      for (int e = tid; e < P.ncopy * k; e += nthr) nt_rec_reset(P.rec + ((size_t)rz * P.ncopy * k + e) * kNtRec);
+    {
+      const int rz = (round + 2) % kNtRing;          // (see k_bcd_newton)
+      for (int e = blockIdx.x + G * tid; e < P.ncopy * k; e += G * nthr)
+        nt_rec_reset(P.rec + ((size_t)rz * P.ncopy * k + e) * kNtRec);
     }
     // ---- the same Michelot step for every atom in every CTA ----
     int conv = 1, nmode = 0;
@@ -557,28 +716,27 @@ k_bcd_big(NbArgs A) {
     if (!done) cur ^= 1;
     __syncthreads();
   }
-  // ---- final D: v of the final round through its parameters (streamed: one more
-  // pass per tile with the final parameters) ----
+  // ---- final D: v of the final round through its parameters (several tiles: one
+  // more pass per tile with the final parameters) ----
   if (q > 0) {
     const NtPar<kGen>* pr = par_s[cur];
     for (int tl = 0; tl < ntile; ++tl) {
       int nr = min(TR, nr_all - tl * TR);
-      if (streamed) nr = pass(tl, pr);
-      if (streamed || tl == 0) {
-        if (streamed) {
-          for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + tl * TR + r];
-          __syncthreads();
-        }
-        for (int r = wid; r < nr; r += (nthr >> 5)) {
-          float* dst = P.D + (int64_t)rows_s[r] * kp;
-          const float* src = V + (size_t)r * LD;
-          for (int j = lane; j < k; j += 32) {
-            const int pp = pinv_s[j];
-            dst[j] = pr[pp].d_of(src[pp]);
-          }
-        }
+      if (ntile > 1) nr = nb_tile_pass<KPT, T, M, kGen, CH, kBlk>(A.scr, A.Cpi, A.Ctg, tl, TR, nr_all, lo, streamed, Dold, Rini, V,
+                                                                cbuf, Dl, pr, g, tq, ngroups, tid, nthr);
+      if (ntile > 1) {
+        for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + tl * TR + r];
         __syncthreads();
       }
+      for (int r = wid; r < nr; r += (nthr >> 5)) {
+        float* dst = P.D + (int64_t)rows_s[r] * kp;
+        const float* src = V + (size_t)r * LD;
+        for (int j = lane; j < k; j += 32) {
+          const int pp = pinv_s[j];
+          dst[j] = pr[pp].d_of(src[pp]);
+        }
+      }
+      __syncthreads();
     }
   }
   // ---- draw-ahead of t+1: scatter of my slice of M_{t+1}, t+1, w_{t+1} ----

@@ -31,6 +31,7 @@
 namespace somf {
 
 constexpr int kNtRing = 3;
+constexpr int kProfSlots = 96;      // BCD / ridge profile slots (somf_bcd_phase_cycles)
 constexpr int kNtMaxK = 128;        // largest k of the simultaneous-threshold kernel
 constexpr int kNtRec = 16;          // 64-bit words per accumulator record (128 bytes)
 constexpr int kNtMaxCopies = 16;    // copies of each record (CTA b adds into copy b % ncopy)
@@ -97,11 +98,14 @@ struct NtArgs {
 };
 
 // phase clock of CTA 0 (diagnostics only; prof == nullptr disables it)
+// (accumulated in shared memory: a global read-modify-write per mark would put
+// an L2 round trip on CTA 0's path and distort what it measures; flushed once
+// at the end of the kernel)
 #define NT_MARK(slot)                                                              \
   do {                                                                             \
     if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {                           \
       const long long now_ = clock64();                                            \
-      P.prof[slot] += now_ - t_mark;                                               \
+      prof_s[slot] += now_ - t_mark;                                               \
       t_mark = now_;                                                               \
     }                                                                              \
   } while (0)
@@ -494,7 +498,10 @@ k_bcd_newton(NtArgs P) {
   __shared__ double dmax_s;
   __shared__ double diag_s[KPT], lws_s[KPT], ns_s[KPT];
   __shared__ int mcnt_s;      // selected rows of M_{t+1} in my slice
+  __shared__ long long prof_s[kProfSlots];
   const int k = P.k, kp = P.kp;
+  if (P.prof && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < kProfSlots; i += blockDim.x) prof_s[i] = 0;
   const int nthr = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int G = gridDim.x;
@@ -804,11 +811,15 @@ k_bcd_newton(NtArgs P) {
     ++nbar;
     nt_barrier(P.bar, nbar * G);
     NT_MARK(3);
-    if (blockIdx.x == 0) {
-      // recycle the ring slot of the NEXT-but-one round (its readers are done)
+    {
+      // recycle the ring slot of the NEXT-but-one round (every CTA read it in
+      // the previous round, before this barrier; it is written again only after
+      // the next one): record e by CTA e % G, spread over the grid
       const int rz = (round + 2) % kNtRing;
-      for (int e = tid; e < P.ncopy * k; e += nthr) nt_rec_reset(P.rec + ((size_t)rz * P.ncopy * k + e) * kNtRec);
+      for (int e = blockIdx.x + G * tid; e < P.ncopy * k; e += G * nthr)
+        nt_rec_reset(P.rec + ((size_t)rz * P.ncopy * k + e) * kNtRec);
     }
+    NT_MARK(80);
     // ---- 3. the same Michelot step for every unfrozen atom in every CTA ----------
     int conv = 1, nmode = 0;
     double nlam = 0.0, cnt = 0.0, S1 = 0.0, S2 = 0.0;
@@ -826,6 +837,7 @@ k_bcd_newton(NtArgs P) {
     }
     nt_read_coop(P.rec + (size_t)ring * P.ncopy * k * kNtRec, P.ncopy, k, P.rd_h, rdp);
     __syncthreads();
+    NT_MARK(81);
     if (act) {
       const NtSums sm = nt_combine(rdp, P.rd_h, k, p);
       cnt = sm.cnt;
@@ -859,7 +871,7 @@ k_bcd_newton(NtArgs P) {
     if (P.prof && blockIdx.x == 0) {
       // convergence profile: unconverged atoms per round (slots 8..71)
       const int nun = __syncthreads_count(act && !conv);
-      if (tid == 0 && round < 64) P.prof[8 + round] += nun + ((long long)F << 16);   // (F << 16) + unconverged
+      if (tid == 0 && round < 64) prof_s[8 + round] += nun + ((long long)F << 16);   // (F << 16) + unconverged
     }
     NT_MARK(4);
     ++round;
@@ -924,7 +936,13 @@ k_bcd_newton(NtArgs P) {
   // ---- exit: last CTA resets counters and accumulators ------------------------------
   __syncthreads();
   NT_MARK(6);
-  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) P.prof[7] += 1;
+  if (P.prof && blockIdx.x == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) prof_s[7] += 1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kProfSlots; i += blockDim.x)
+      if (i < 72 || i >= 76) P.prof[i] += prof_s[i];              // (72..75: the ridge solver's)
+  }
   if (tid == 0) {
     __threadfence();
     const unsigned old = atomicAdd(P.bar + 1, 1u);

@@ -158,10 +158,10 @@ struct somf_ctx {
   size_t nt_smem = 0;
   double* lam_ws = nullptr;
   unsigned long long* nt_acc = nullptr;
-  int nt_ncopy = 8;
+  int nt_ncopy = 2;
   // simultaneous-threshold BCD for k <= 256 / streamed rows (bcd_big.cuh)
   const void* nb_fn = nullptr;
-  int nb_kpt = 0, nb_T = 0, nb_ch = 0, nb_tr = 0, nb_threads = 0, nb_rd_h = 1;
+  int nb_kpt = 0, nb_T = 0, nb_ch = 0, nb_blk = 0, nb_tr = 0, nb_threads = 0, nb_rd_h = 1;
   size_t nb_smem = 0;
   float *nb_cpi = nullptr, *nb_ctg = nullptr, *nb_invc = nullptr, *nb_scr = nullptr;
   long long* bcd_prof = nullptr;   // SM cycles per BCD phase (somf_bcd_phase_cycles)
@@ -864,16 +864,17 @@ static void choose_newton(somf_ctx* h) {
   }
 }
 
-#define NB_DECL(K) const void* somf_nb_kernel_##K(int gen, int* T, int* ch);
+#define NB_DECL(K) const void* somf_nb_kernel_##K(int gen, int* T, int* ch, int* blk);
 NB_DECL(72) NB_DECL(128) NB_DECL(192) NB_DECL(256)
 #undef NB_DECL
-struct NbVariant { int kpt; const void* (*get)(int, int*, int*); };
+struct NbVariant { int kpt; const void* (*get)(int, int*, int*, int*); };
 static const NbVariant kNbVariants[] = {{72, somf_nb_kernel_72}, {128, somf_nb_kernel_128},
                                         {192, somf_nb_kernel_192}, {256, somf_nb_kernel_256}};
 
 // The simultaneous-threshold kernel for k <= 256 and for masked rows that do
 // not fit on chip (bcd_big.cuh): the smallest KPT >= k; tile rows TR as many
-// as the shared memory and the 384 threads hold (streamed when a CTA has more).
+// as the shared memory and the 384 threads hold (several tiles per CTA:
+// streamed from the scratch).  Shared-memory layout: bcd_big.cuh.
 static bool choose_big(somf_ctx* h) {
   const int k = h->cfg.k;
   const int cap = (int)ceil_div(h->q_cap, h->nsm);
@@ -882,24 +883,27 @@ static bool choose_big(somf_ctx* h) {
   const size_t mb = (size_t)ceil_div(nb, h->nsm) + 16;
   for (const NbVariant& v : kNbVariants) {
     if (v.kpt < k) continue;
-    int T = 0, ch = 0;
-    const void* fn = v.get(gen, &T, &ch);
+    int T = 0, ch = 0, blk = 0;
+    const void* fn = v.get(gen, &T, &ch, &blk);
     cudaFuncAttributes fa{};
     if (!fn || cudaFuncGetAttributes(&fa, fn) != cudaSuccess) { cudaGetLastError(); return false; }
-    const int kpt = v.kpt, LD = kpt + 1;
+    const int kpt = v.kpt, LD = blk ? kpt + 4 : kpt + 1;
     const size_t cstr = (size_t)nb_cstr(kpt, T);
-    const size_t cbf = ch >= kpt ? (size_t)kpt * T * cstr : (size_t)2 * ch * T * cstr;
+    const size_t cbf = blk ? (size_t)2 * kNbCB * kpt
+                           : ch >= kpt ? (size_t)kpt * T * cstr : (size_t)2 * ch * T * cstr;
     const size_t limit = 227 * 1024 - fa.sharedSizeBytes - 512;
-    int TR = std::min(cap, 2 * (kNbThreads / T));
+    int TR = std::min(cap, blk ? kNbThreads : 2 * (kNbThreads / T));
     if (h->cfg.bcd_tile_rows > 0) TR = std::max(2, std::min(TR, (int)h->cfg.bcd_tile_rows));
     size_t smem = 0;
     int nthr = 0;
     for (; TR >= 2; --TR) {
-      nthr = (int)std::max<int64_t>(ceil_div((int64_t)T * ceil_div(TR, 2), 32) * 32, ceil_div(k, 32) * 32);
+      nthr = blk ? kNbThreads
+                 : (int)std::max<int64_t>(ceil_div((int64_t)T * ceil_div(TR, 2), 32) * 32, ceil_div(k, 32) * 32);
       const size_t H = std::max(1, nthr / k);
       const size_t partw = std::max<size_t>(5 * H * kpt, (size_t)12 * k);
-      const size_t blk = ((size_t)(TR + 1) * LD + 3) & ~(size_t)3;
-      smem = (3 * blk + cbf + ((partw + 3) & ~(size_t)3) + (size_t)((TR + 3) & ~3)) * sizeof(float) + mb;
+      const size_t blkf = ((size_t)(TR + 1) * LD + 3) & ~(size_t)3;
+      const size_t dlf = blk ? (size_t)(TR + 1) * kNbCB : 0;
+      smem = (3 * blkf + cbf + dlf + ((partw + 3) & ~(size_t)3) + (size_t)((TR + 3) & ~3)) * sizeof(float) + mb;
       if (smem <= limit && nthr <= kNbThreads) break;
     }
     if (TR < 2) return false;
@@ -912,10 +916,10 @@ static bool choose_big(somf_ctx* h) {
       cudaGetLastError();
       return false;
     }
-    if (dalloc(&h->nb_cpi, (size_t)kpt * kpt) != cudaSuccess || dalloc(&h->nb_ctg, (size_t)kpt * T * cstr) != cudaSuccess ||
-        dalloc(&h->nb_invc, (size_t)kpt) != cudaSuccess)
+    if (dalloc(&h->nb_cpi, (size_t)kpt * kpt) != cudaSuccess || dalloc(&h->nb_invc, (size_t)kpt) != cudaSuccess ||
+        (!blk && dalloc(&h->nb_ctg, (size_t)kpt * T * cstr) != cudaSuccess))
       return false;
-    if (cap > TR && dalloc(&h->nb_scr, (size_t)h->q_cap * 2 * kpt) != cudaSuccess) return false;
+    if ((blk || cap > TR) && dalloc(&h->nb_scr, (size_t)h->q_cap * 2 * kpt) != cudaSuccess) return false;
     const int H = std::max(1, nthr / k);
     const size_t partw = std::max<size_t>(5 * (size_t)H * kpt, (size_t)12 * k);
     h->nb_rd_h = (int)std::max<size_t>(1, std::min<size_t>({partw / (12 * (size_t)k), (size_t)h->nt_ncopy,
@@ -924,6 +928,7 @@ static bool choose_big(somf_ctx* h) {
     h->nb_kpt = kpt;
     h->nb_T = T;
     h->nb_ch = ch;
+    h->nb_blk = blk;
     h->nb_tr = TR;
     h->nb_threads = nthr;
     h->nb_smem = smem;
@@ -1223,8 +1228,8 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->oc_rho, (size_t)4 * k));
   A(dalloc(&h->oc_bar, 4));
   A(dalloc(&h->lam_ws, (size_t)k));
-  A(dalloc(&h->bcd_prof, 80));
-  h->nt_ncopy = c.bcd_copies > 0 ? std::min(c.bcd_copies, kNtMaxCopies) : 8;
+  A(dalloc(&h->bcd_prof, kProfSlots));
+  h->nt_ncopy = c.bcd_copies > 0 ? std::min(c.bcd_copies, kNtMaxCopies) : 2;
   A(dalloc(&h->nt_acc, (size_t)(kNtRing + 1) * h->nt_ncopy * k * kNtRec));
   if (c.estimator != 0) {
     const size_t n = (size_t)c.n_samples;
@@ -1257,7 +1262,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       cudaMemset(h->theta_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->lam_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->AT32, 0, (size_t)c.eta * ((k + 3) & ~3) * sizeof(float)) != cudaSuccess ||
-      cudaMemset(h->bcd_prof, 0, 80 * sizeof(long long)) != cudaSuccess ||
+      cudaMemset(h->bcd_prof, 0, kProfSlots * sizeof(long long)) != cudaSuccess ||
       init_nt_rec(h->nt_acc, (kNtRing + 1) * h->nt_ncopy * k) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
@@ -1629,8 +1634,8 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
         // pi, Cbar in pi order and prescaled per thread parity, then the rounds
         NbPerm pv{};
         host_atom_perm(c.seed, (uint64_t)h->t_host, k, c.perm_cyclic, pv.v);
-        k_nb_prep<<<h->nb_kpt, 256, 0, h->st>>>(pv, k, h->nb_kpt, h->nb_T, h->C32, h->C64, h->perm, h->nb_cpi,
-                                                  h->nb_ctg, h->nb_invc);
+        k_nb_prep<<<h->nb_kpt, 256, 0, h->st>>>(pv, k, h->nb_kpt, h->nb_T, h->nb_blk, h->C32, h->C64, h->perm,
+                                                  h->nb_cpi, h->nb_ctg, h->nb_invc);
         CKL();
         h->launches[SOMF_PH_BCD] += 1;
         na.perm = h->perm;
@@ -1638,14 +1643,13 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
         na.rd_h = h->nb_rd_h;
         na.cap_rows = h->nb_tr;
         NbArgs nba{};
-        nba.nt = na;
         nba.Cpi = h->nb_cpi;
         nba.Ctg = h->nb_ctg;
         nba.invc = h->nb_invc;
         nba.scr = h->nb_scr;
         nba.tile_rows = h->nb_tr;
         nba.ch = h->nb_ch;
-        void* kargs[] = {&nba};
+        void* kargs[] = {&na, &nba};
         CK(cudaLaunchCooperativeKernel(h->nb_fn, dim3(h->nsm), dim3(h->nb_threads), kargs, h->nb_smem, h->st));
       }
       h->ahead_ready = true;
@@ -1913,10 +1917,10 @@ SOMF_EXPORT somf_status somf_set_reducer(somf_handle h, somf_reduce_fn fn, void*
 SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {
   if (!h || !cycles) return SOMF_E_ARG;
   CK(cudaStreamSynchronize(h->st));
-  long long v[80];
+  long long v[kProfSlots];
   CK(cudaMemcpy(v, h->bcd_prof, sizeof(v), cudaMemcpyDeviceToHost));
   CK(cudaMemset(h->bcd_prof, 0, sizeof(v)));
-  for (int i = 0; i < 80; ++i) cycles[i] = v[i];
+  for (int i = 0; i < kProfSlots; ++i) cycles[i] = v[i];
   return SOMF_OK;
 }
 

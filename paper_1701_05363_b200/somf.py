@@ -250,7 +250,7 @@ class Somf:
     BCD_PHASES = ("setup", "recurrence", "stats", "barrier", "update", "finish", "writeback")
 
     def bcd_phase_cycles(self):
-        v = np.zeros(80, np.int64)
+        v = np.zeros(96, np.int64)
         _check(lib().somf_bcd_phase_cycles(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
         out = dict(zip(self.BCD_PHASES, v[:7].tolist()), launches=int(v[7]))
         # slot 8 + r: (frozen prefix F << 16) + unconverged atoms, summed over launches
@@ -258,6 +258,7 @@ class Somf:
         out["frozen_prefix_per_round"] = (v[8:72] >> 16).tolist()
         out["ridge"] = dict(zip(("load", "factor", "solve", "cbar_partial"), v[72:76].tolist()), inverse=int(v[79]))
         out["setup_split"] = dict(zip(("params", "gather", "permute"), v[76:79].tolist()))
+        out["update_split"] = dict(zip(("ring_reset", "record_read"), v[80:82].tolist()))
         return out
 
     def set_reducer(self, fn):
