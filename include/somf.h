@@ -63,7 +63,11 @@ typedef enum {
  * and Alg. 3's last line P:612). */
 typedef enum {
   SOMF_B_MASKED = 0,      /* P_t Bbar only: BASELINE north star (hot path)      */
-  SOMF_B_UNBIASED = 1,    /* reserved (reading R6); returns SOMF_E_UNSUPPORTED  */
+  SOMF_B_UNBIASED = 1,    /* unbiased masked update (reading R6):
+                           Bbar <- (1-w) Bbar on every row, kept lazily as
+                           one scale sigma_t, plus (w r / eta) X_M A^T on the
+                           masked rows; same bytes as MASKED, tracks FULL.
+                           somf_get_state returns the true (scaled) Bbar, Cbar */
   SOMF_B_FULL = 2         /* P_t Bbar and P_t^perp Bbar: Alg. 3 as printed      */
 } somf_bmode;
 
@@ -173,7 +177,8 @@ somf_status somf_set_components(somf_handle h, const float* D0, int64_t ld);
  * beta = D^T M_t X, G = D^T M_t D (Eq. a), codes (Eq. somf_alpha: ridge closed
  * form by Cholesky when nu = 1 and no positivity and k <= 160, coordinate
  * descent otherwise), Cbar and Bbar (Eq. somf_partial; b_mode), then Alg. 4 on
- * the selected rows.  Only the selected rows of X are read (b_mode MASKED):
+ * the selected rows.  Only the selected rows of X are read (b_mode MASKED or
+ * UNBIASED):
  * X may be mapped pinned host memory, in which case the q selected rows are
  * first gathered into device memory (phase SOMF_PH_STAGE), each crossing the
  * host link once.  SOMF_E_STATE before somf_set_components / somf_set_state. */
@@ -201,7 +206,7 @@ somf_status somf_next_mask(somf_handle h, int64_t* q_out, int32_t* idx_out);
 /* Like somf_partial_fit, but X_M (device, q x eta row-major, ld >= eta) holds
  * only the q selected rows of the batch, in ascending row order, where q and
  * the rows are those returned by the preceding somf_next_mask.  Requires
- * b_mode MASKED.  SOMF_E_STATE without a preceding somf_next_mask. */
+ * b_mode MASKED or UNBIASED (FULL reads every row: SOMF_E_STATE).  SOMF_E_STATE without a preceding somf_next_mask. */
 somf_status somf_partial_fit_masked(somf_handle h, const float* X_M, int64_t ld);
 
 /* Codes alpha_t of the last iteration's batch, k x eta row-major float32,

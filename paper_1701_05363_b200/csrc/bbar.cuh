@@ -42,8 +42,8 @@ k_bbar_v2(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, co
   float* As = bb_smem + 2 * TR * SC;            // [2][SC][KA]
   __shared__ int grow[TR];
   const int64_t q = *q_dev;
-  const double w = *w_dev;
-  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const double keepd = w_dev[kCoefKeep], gb = w_dev[kCoefGainB];
+  const float keep = (float)keepd, add = (float)(gb / eta);
   const int G = gridDim.x;
   const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -159,8 +159,8 @@ k_bbar_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, co
   float* Xs = ATs + (size_t)eta * KA;                 // SEG x eta (rows >= n zero)
   __shared__ int grow[SEG];
   const int64_t q = *q_dev;
-  const double w = *w_dev;
-  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const double keepd = w_dev[kCoefKeep], gb = w_dev[kCoefGainB], gc = w_dev[kCoefGainC];
+  const float keep = (float)keepd, add = (float)(gb / eta);
   const int G = gridDim.x;
   const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -175,7 +175,7 @@ k_bbar_v3(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev, co
     for (int e = e0 + tid; e < e1; e += kBbThreads) {
       double s = 0.0;
       for (int bq = 0; bq < cf.nparts; ++bq) s += cf.cpart[(size_t)bq * cf.kk + e];
-      const double c = (1.0 - w) * cf.C64[e] + (w / eta) * s;
+      const double c = keepd * cf.C64[e] + (gc / eta) * s;
       cf.C64[e] = c;
       cf.C32[e] = (float)c;
     }

@@ -87,8 +87,8 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
   const int eta = P.eta, k = P.k, kp = P.kp, np = P.np, ep = P.ep, nch = ep / 8;
   const int G = gridDim.x;
   const int64_t q = *P.q_dev;
-  const double w = *P.w_dev;
-  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const double keepd = P.w_dev[kCoefKeep], gb = P.w_dev[kCoefGainB], gc = P.w_dev[kCoefGainC];
+  const float keep = (float)keepd, add = (float)(gb / eta);
   const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
   const size_t a_bytes = (size_t)kBtM * ep * 2, b_bytes = (size_t)np * ep * 2;
   uint8_t* Ahi = bt_smem;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
         s += __shfl_xor_sync(0xffffffffu, s, 2);
         s += __shfl_xor_sync(0xffffffffu, s, 4);
         if (e < e1 && h == 0) {
-          const double c = (1.0 - w) * P.cf.C64[e] + (w / eta) * s;
+          const double c = keepd * P.cf.C64[e] + (gc / eta) * s;
           P.cf.C64[e] = c;
           P.cf.C32[e] = (float)c;
         }
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
       for (int e = e0 + tid; e < e1; e += kBtThreads) {
         double s = 0.0;
         for (int bq = 0; bq < P.cf.nparts; ++bq) s += P.cf.cpart[(size_t)bq * P.cf.kk + e];
-        const double c = (1.0 - w) * P.cf.C64[e] + (w / eta) * s;
+        const double c = keepd * P.cf.C64[e] + (gc / eta) * s;
         P.cf.C64[e] = c;
         P.cf.C32[e] = (float)c;
       }

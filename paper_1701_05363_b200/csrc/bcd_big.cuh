@@ -764,7 +764,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
     }
     if (blockIdx.x == 0 && tid == 0) {
       *P.t_next = P.tn;
-      *P.w_next = pow((double)P.tn, -P.u);
+      store_coef(P.w_next, P.cf_next);
     }
   }
   // ---- exit: last CTA resets counters and accumulators ----

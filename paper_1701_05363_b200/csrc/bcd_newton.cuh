@@ -79,8 +79,8 @@ struct NtArgs {
   int ncopy;
   // draw-ahead of iteration t+1 while the CTAs wait on the rounds (null idx_next
   // = off): M_{t+1} (Eq. mt) into idx_next / q_next (per-CTA counts through
-  // cnt_next, published before round 0's barrier), t+1 and w_{t+1} = (t+1)^-u
-  // into t_next / w_next.  (pi_{t+1} is drawn on the host: perm_v.)
+  // cnt_next, published before round 0's barrier), t+1 and the coefficients of
+  // w_{t+1} = (t+1)^-u into t_next / w_next.  (pi_{t+1} is drawn on the host: perm_v.)
   int32_t* idx_next;
   int64_t* q_next;
   int* cnt_next;            // gridDim.x
@@ -88,7 +88,7 @@ struct NtArgs {
   double* w_next;
   uint64_t seed, Tthr;
   int64_t tn, row_lo, row_hi;
-  double u;
+  StepCoef cf_next;         // coefficients of iteration t+1 (w_{t+1} = (t+1)^-u; common.cuh)
   int cyclic;
   int mbits_off;            // byte offset of the mask-bit scratch in dynamic smem
   unsigned* bar;            // [0] arrivals [1] exits [2] watchdog
@@ -930,7 +930,7 @@ k_bcd_newton(NtArgs P) {
     }
     if (blockIdx.x == 0 && wid == 0 && lane == 0) {
       *P.t_next = P.tn;
-      *P.w_next = pow((double)P.tn, -P.u);
+      store_coef(P.w_next, P.cf_next);
     }
   }
   // ---- exit: last CTA resets counters and accumulators ------------------------------

@@ -334,10 +334,10 @@ __global__ void k_cbar_finalize(const double* __restrict__ cpart, int nparts, in
                                 float* __restrict__ C32) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
-  const double w = *w_dev;
+  const double keepd = w_dev[kCoefKeep], gc = w_dev[kCoefGainC];
   double s = 0.0;
   for (int b = 0; b < nparts; ++b) s += cpart[(size_t)b * k * k + e];
-  const double c = (1.0 - w) * C64[e] + (w / eta) * s;
+  const double c = keepd * C64[e] + (gc / eta) * s;
   C64[e] = c;
   C32[e] = (float)c;
 }

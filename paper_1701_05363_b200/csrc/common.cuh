@@ -42,6 +42,22 @@ __host__ __device__ __forceinline__ uint32_t u4_word(const U4& v, int lane) {
 
 enum : uint32_t { kStreamMask = 1, kStreamPerm = 2, kStreamCols = 3 };
 
+// Aggregation coefficients of iteration t (Eq. somf_partial, R6),
+// kept on the device next to t (w_dev[0..3]) and written by whichever kernel
+// begins the iteration (k_step_mask_count or the previous BCD's draw-ahead):
+//   Cbar <- keep Cbar + (gc / eta) A A^T ,  P_t Bbar <- keep P_t Bbar + (gb / eta) X_M A^T
+// modes M / F: keep = 1 - w_t, gb = gc = w_t.  Mode U stores Bbar / sigma_t and
+// Cbar / sigma_t (sigma_t = prod (1 - w_s), the lazy global decay of R6):
+// keep = 1, gb = w_t r / sigma_t, gc = w_t / sigma_t.  Alg. 4 is invariant to
+// the joint scale of (Bbar, Cbar), so the BCD kernels read the stored values.
+enum : int { kCoefW = 0, kCoefKeep = 1, kCoefGainB = 2, kCoefGainC = 3, kCoefN = 4 };
+struct StepCoef { double v[kCoefN]; };
+
+__device__ __forceinline__ void store_coef(double* dst, const StepCoef& c) {
+#pragma unroll
+  for (int i = 0; i < kCoefN; ++i) dst[i] = c.v[i];
+}
+
 // Selection bits of the 4 rows of Philox block blk (rows 4 blk .. 4 blk + 3)
 // in M_t (Eq. mt; R1, R2): row i selected iff word_{i&3} < T(r).
 __device__ __forceinline__ uint32_t mask_bits(uint64_t seed, uint64_t t, int64_t blk,

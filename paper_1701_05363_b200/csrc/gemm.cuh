@@ -122,8 +122,8 @@ k_bbar_update(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev
   __shared__ __align__(16) float Xs[TK][TM + 4];   // [s][row]
   __shared__ __align__(16) float As[TK][TN + 4];   // [s][atom]
   const int64_t q = *q_dev;
-  const double w = *w_dev;
-  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const double keepd = w_dev[kCoefKeep], gb = w_dev[kCoefGainB];
+  const float keep = (float)keepd, add = (float)(gb / eta);
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
   const int a0 = blockIdx.y * TN;
   for (int64_t m0 = (int64_t)blockIdx.x * TM; m0 < q; m0 += (int64_t)gridDim.x * TM) {
@@ -183,9 +183,9 @@ k_bbar_comp(const float* __restrict__ X, int64_t ldx, int eta, const float* __re
             uint64_t seed, const int64_t* __restrict__ t_dev, uint64_t T) {
   __shared__ __align__(16) float Xs[TK][TM + 4];   // [s][row]
   __shared__ __align__(16) float As[TK][TN + 4];   // [s][atom]
-  const double w = *w_dev;
+  const double keepd = w_dev[kCoefKeep], gb = w_dev[kCoefGainB];
   const uint64_t t = (uint64_t)*t_dev;
-  const float keep = (float)(1.0 - w), add = (float)(w / eta);
+  const float keep = (float)keepd, add = (float)(gb / eta);
   const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
   const int a0 = blockIdx.y * TN;
   for (int64_t m0 = (int64_t)blockIdx.x * TM; m0 < rows; m0 += (int64_t)gridDim.x * TM) {

@@ -111,10 +111,10 @@ __device__ __forceinline__ void atom_perm_cta(uint64_t seed, uint64_t t, int k, 
 
 // One launch for the start of an iteration: CTAs 0 .. ntiles-1 count the
 // selected rows of M_t per tile (as k_mask_count); the extra last CTA writes
-// t and w_t = t^-u and draws the atom order (R13).
+// t and the coefficients of w_t = t^-u (computed on the host) and draws the atom order (R13).
 // t is passed by value (the host tracks it), so no CTA reads t_dev.
 __global__ void __launch_bounds__(kMaskThreads)
-k_step_mask_count(uint64_t seed, int64_t t, double u, int64_t row_lo, int64_t row_hi, uint64_t T, int ntiles,
+k_step_mask_count(uint64_t seed, int64_t t, StepCoef cf, int64_t row_lo, int64_t row_hi, uint64_t T, int ntiles,
                   int32_t* __restrict__ tile_counts, int64_t* __restrict__ t_dev, double* __restrict__ w_dev,
                   int k, int cyclic, int32_t* __restrict__ perm) {
   __shared__ uint32_t sh[2 * 256 + 8];
@@ -122,7 +122,7 @@ k_step_mask_count(uint64_t seed, int64_t t, double u, int64_t row_lo, int64_t ro
   if ((int)blockIdx.x == ntiles) {
     if (threadIdx.x == 0) {
       *t_dev = t;
-      *w_dev = pow((double)t, -u);
+      store_coef(w_dev, cf);          // w_t = t^-u and the mode's coefficients
     }
     atom_perm_cta(seed, (uint64_t)t, k, cyclic, perm, sh);
     return;

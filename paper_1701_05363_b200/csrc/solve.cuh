@@ -125,12 +125,12 @@ __global__ void k_cbar_update(const double* __restrict__ A64, int k, int eta,
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
   const int a = e / k, b = e % k;
-  const double w = *w_dev;
+  const double keepd = w_dev[kCoefKeep], gc = w_dev[kCoefGainC];
   double s = 0.0;
   const double* ra = A64 + (int64_t)a * eta;
   const double* rb = A64 + (int64_t)b * eta;
   for (int t = 0; t < eta; ++t) s += ra[t] * rb[t];
-  const double c = (1.0 - w) * C64[e] + (w / eta) * s;
+  const double c = keepd * C64[e] + (gc / eta) * s;
   C64[e] = c;
   C32[e] = (float)c;
 }

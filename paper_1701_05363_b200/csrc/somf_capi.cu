@@ -115,6 +115,7 @@ struct somf_ctx {
   double* w_next = nullptr;
   int nt_mbits_off = 0;
   int64_t t_host = 0;
+  double sig = 1.0;          // mode U: sigma_{t_host}, the lazy scale of the stored Bbar / Cbar (R6)
   // iterate
   float* D = nullptr;
   float* Bbar = nullptr;
@@ -1150,9 +1151,8 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       !(c.u > 0.0 && c.u <= 1.0) || c.row_lo < 0 || c.row_hi > c.p || c.row_lo >= c.row_hi ||
       !(c.cd_tol > 0.0) || c.cd_max_sweeps < 1 || c.row_hi - c.row_lo > (int64_t)INT32_MAX;
   if (bad) return SOMF_E_ARG;
-  if (c.b_mode == SOMF_B_UNBIASED) return SOMF_E_UNSUPPORTED;
   if (c.bcd_kernel < 0 || c.bcd_kernel > 4) return SOMF_E_ARG;
-  if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL) return SOMF_E_ARG;
+  if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL && c.b_mode != SOMF_B_UNBIASED) return SOMF_E_ARG;
   if (c.estimator < 0 || c.estimator > 2) return SOMF_E_ARG;
   if (c.bcd_tile_rows < 0) return SOMF_E_ARG;
   if (c.estimator != 0 && (c.n_samples < 1 || !(c.v > 0.0 && c.v <= 1.0))) return SOMF_E_ARG;
@@ -1181,7 +1181,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->C32, (size_t)k * k + 4));   // +4: 16-byte staging reads in the BCD
   A(dalloc(&h->nslack, (size_t)k));
   A(dalloc(&h->t_dev, 1));
-  A(dalloc(&h->w_dev, 1));
+  A(dalloc(&h->w_dev, kCoefN));
   A(dalloc(&h->q_dev, 1));
   A(dalloc(&h->nred_dev, 1));
   A(dalloc(&h->err_dev, 1));
@@ -1190,7 +1190,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->idx_next, (size_t)rows));
   A(dalloc(&h->q_next, 1));
   A(dalloc(&h->t_next, 1));
-  A(dalloc(&h->w_next, 1));
+  A(dalloc(&h->w_next, kCoefN));
   h->ntiles = (int)ceil_div(((c.row_hi - 1) >> 2) - (c.row_lo >> 2) + 1, kMaskThreads);
   A(dalloc(&h->tile_counts, (size_t)h->ntiles));
   A(dalloc(&h->perm, (size_t)k));
@@ -1354,6 +1354,7 @@ SOMF_EXPORT somf_status somf_set_components(somf_handle h, const float* D0, int6
   CK(cudaMemsetAsync(h->theta_ws, 0, (size_t)k * sizeof(double), h->st));
   CK(cudaMemsetAsync(h->lam_ws, 0, (size_t)k * sizeof(double), h->st));
   h->t_host = 0;
+  h->sig = 1.0;
   h->mask_ready = h->begin_ready = h->ahead_ready = false;
   h->initialized = true;
   if (somf_status s = reset_estimator(h)) return s;
@@ -1396,6 +1397,73 @@ static void host_atom_perm(uint64_t seed, uint64_t t, int k, int cyclic, int32_t
 }
 
 // the draw-ahead buffers of the BCD kernel become the current ones
+// Aggregation coefficients of iteration t (common.cuh StepCoef), from
+// sigma_{t-1} = h->sig (mode U; a stored scale below kURenorm is folded back
+// into Bbar / Cbar by u_renorm before iteration t aggregates, so t's
+// coefficients start from sigma = 1 then).  *sig_t = sigma_t.
+constexpr double kURenorm = 1e-20;
+static StepCoef step_coef(const somf_ctx* h, int64_t t, double* sig_t = nullptr) {
+  const somf_config& c = h->cfg;
+  const double w = std::pow((double)t, -c.u);
+  StepCoef cf{};
+  cf.v[kCoefW] = w;
+  double sg = 1.0;
+  if (c.b_mode != SOMF_B_UNBIASED) {
+    cf.v[kCoefKeep] = 1.0 - w;                                               // Eq. somf_partial
+    cf.v[kCoefGainB] = w;
+    cf.v[kCoefGainC] = w;
+  } else {
+    // R6: Bbar = sigma Btilde, Cbar = sigma Ctilde, sigma_t = sigma_{t-1} (1 - w_t);
+    // Btilde[S] += (w r / (eta sigma_t)) X_S A^T, Ctilde += (w / (eta sigma_t)) A A^T
+    const double base = h->sig < kURenorm ? 1.0 : h->sig;
+    sg = base * (1.0 - w);
+    if (!(sg > 0.0)) {
+      // w_t = 1 (t = 1): Bbar <- 0 on every row (u_begin zeroes the stored
+      // rows), Cbar <- A A^T / eta, sigma restarts at 1
+      sg = 1.0;
+      cf.v[kCoefKeep] = 0.0;
+      cf.v[kCoefGainB] = w * c.r;
+      cf.v[kCoefGainC] = w;
+    } else {
+      cf.v[kCoefKeep] = 1.0;
+      cf.v[kCoefGainB] = w * c.r / sg;
+      cf.v[kCoefGainC] = w / sg;
+    }
+  }
+  if (sig_t) *sig_t = sg;
+  return cf;
+}
+
+__global__ void k_set_coef(double* dst, StepCoef cf) { store_coef(dst, cf); }
+
+__global__ void k_scale_state(float* __restrict__ Bbar, int64_t n, double* __restrict__ C64,
+                              float* __restrict__ C32, int kk, double s) {
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = i0; i < n; i += st) Bbar[i] = (float)(s * (double)Bbar[i]);
+  for (int64_t i = i0; i < kk; i += st) {
+    const double c = s * C64[i];
+    C64[i] = c;
+    C32[i] = (float)c;
+  }
+}
+
+// Mode U: fold the stored scale back (Bbar <- sigma Btilde, Cbar <- sigma Ctilde,
+// sigma <- 1) and rewrite the coefficients already drawn for iteration t+1.
+static somf_status u_renorm(somf_ctx* h) {
+  if (h->cfg.b_mode != SOMF_B_UNBIASED || h->sig == 1.0) return SOMF_OK;
+  const int64_t n = h->rows * h->kp;
+  const int kk = h->cfg.k * h->cfg.k;
+  k_scale_state<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 8 * h->nsm), 256, 0, h->st>>>(
+      h->Bbar, n, h->C64, h->C32, kk, h->sig);
+  CKL();
+  h->sig = 1.0;
+  if (h->ahead_ready || h->begin_ready) {
+    k_set_coef<<<1, 1, 0, h->st>>>(h->ahead_ready ? h->w_next : h->w_dev, step_coef(h, h->t_host + 1));
+    CKL();
+  }
+  return SOMF_OK;
+}
+
 static void swap_ahead(somf_ctx* h) {
   std::swap(h->idx, h->idx_next);
   std::swap(h->q_dev, h->q_next);
@@ -1437,9 +1505,21 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       swap_ahead(h);
       h->begin_ready = h->mask_ready = true;
     }
+    double sig_t = 1.0;
+    if (c.b_mode == SOMF_B_UNBIASED && h->sig < kURenorm) {
+      // (t's coefficients, drawn ahead or not, were computed from sigma = 1)
+      const bool br = h->begin_ready;
+      h->begin_ready = false;
+      if (somf_status s = u_renorm(h)) return s;
+      h->begin_ready = br;
+    }
+    const StepCoef cf = step_coef(h, h->t_host, &sig_t);
+    if (c.b_mode == SOMF_B_UNBIASED && cf.v[kCoefKeep] == 0.0)                 // w_t = 1: Bbar <- 0 (R6)
+      CK(cudaMemsetAsync(h->Bbar, 0, (size_t)h->rows * h->kp * sizeof(float), h->st));
+    h->sig = sig_t;
     const int nt = h->mask_ready ? 0 : h->ntiles;
     if (!h->begin_ready) {
-      k_step_mask_count<<<nt + 1, kMaskThreads, 0, h->st>>>(c.seed, h->t_host, c.u, c.row_lo, c.row_hi, h->T, nt,
+      k_step_mask_count<<<nt + 1, kMaskThreads, 0, h->st>>>(c.seed, h->t_host, cf, c.row_lo, c.row_hi, h->T, nt,
                                                             h->tile_counts, h->t_dev, h->w_dev, k, c.perm_cyclic,
                                                             h->perm);
       CKL();
@@ -1454,7 +1534,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
     }
     h->mask_ready = false;
   }
-  if (host && !compact && c.b_mode == SOMF_B_MASKED) {
+  if (host && !compact && c.b_mode != SOMF_B_FULL) {
     // the selected rows of a host-resident batch cross the link once
     PhaseScope ps(h, SOMF_PH_STAGE);
     if (!h->Xstage) CK(dalloc(&h->Xstage, (size_t)h->rows * eta));
@@ -1616,7 +1696,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.tn = h->t_host + 1;
       na.row_lo = c.row_lo;
       na.row_hi = c.row_hi;
-      na.u = c.u;
+      na.cf_next = step_coef(h, h->t_host + 1);
       na.cyclic = c.perm_cyclic;
       na.mbits_off = h->nt_mbits_off;
       na.rec = h->nt_acc;
@@ -1766,7 +1846,7 @@ SOMF_EXPORT somf_status somf_next_mask(somf_handle h, int64_t* q_out, int32_t* i
 SOMF_EXPORT somf_status somf_partial_fit_masked(somf_handle h, const float* X_M, int64_t ld) {
   if (!h || !X_M) return SOMF_E_ARG;
   if (!h->mask_ready) { set_err(h, "partial_fit_masked without a preceding somf_next_mask"); return SOMF_E_STATE; }
-  if (h->cfg.b_mode != SOMF_B_MASKED) { set_err(h, "partial_fit_masked requires b_mode MASKED"); return SOMF_E_STATE; }
+  if (h->cfg.b_mode == SOMF_B_FULL) { set_err(h, "partial_fit_masked: b_mode FULL reads every row"); return SOMF_E_STATE; }
   return partial_fit_impl(h, X_M, ld, true);
 }
 
@@ -1850,6 +1930,7 @@ SOMF_EXPORT somf_status somf_get_state(somf_handle h, float* D, float* Bbar, dou
                                        int64_t* t) {
   if (!h) return SOMF_E_ARG;
   const int k = h->cfg.k;
+  if (somf_status s = u_renorm(h)) return s;      // mode U: the true Bbar / Cbar (R6)
   if (D)
     CK(cudaMemcpy2DAsync(D, k * sizeof(float), h->D, h->kp * sizeof(float), k * sizeof(float), h->rows,
                          cudaMemcpyDefault, h->st));
@@ -1889,6 +1970,7 @@ SOMF_EXPORT somf_status somf_set_state(somf_handle h, const float* D, const floa
   CK(cudaMemsetAsync(h->lam_ws, 0, (size_t)k * sizeof(double), h->st));
   CK(cudaStreamSynchronize(h->st));
   h->t_host = t;
+  h->sig = 1.0;
   h->mask_ready = h->begin_ready = h->ahead_ready = false;
   h->initialized = true;
   if (somf_status s = reset_estimator(h)) return s;

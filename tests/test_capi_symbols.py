@@ -70,5 +70,3 @@ def test_invalid_config_rejected_without_gpu(libpath):
         setattr(cfg, field, bad)
         assert L.somf_create(C.byref(cfg), C.byref(h)) == 1, field
         setattr(cfg, field, old)
-    cfg.b_mode = 1
-    assert L.somf_create(C.byref(cfg), C.byref(h)) == 8

@@ -190,6 +190,62 @@ def test_one_step_parity_full_mode(somf, name):
                                             st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
 
 
+@pytest.mark.parametrize("bcd_kernel", ["auto", "onchip", "big"])
+@pytest.mark.parametrize("name", ["ridge_l1_fmri_small", "lasso_l2_hyper_small", "nmf_k128", "lasso_k256_ragged"])
+def test_one_step_parity_unbiased_mode(somf, name, bcd_kernel):
+    """Mode U (reading R6): every Bbar row decays by (1 - w) -- kept on the
+    GPU as one lazy scale sigma_t -- and the masked rows add (w r / eta) X_M A^T.
+    Three consecutive steps (drawn-ahead coefficients included) from a loaded
+    state vs the oracle's mode U, every row of Bbar compared."""
+    p, k, eta, kw, kind = CASES[name]
+    if bcd_kernel == "big" and k <= 128 and name != "nmf_k128":
+        pytest.skip("one k <= 128 case is enough for the k <= 256 kernel")
+    X = _data(kind, p, k + 9 * eta)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=3, b_mode="U", **kw))
+    ora.set_components(X[:, :k])
+    for t in range(5):
+        ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
+    ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
+    gpu = somf.Somf(p, k, eta, seed=3, debug=True, b_mode="unbiased", bcd_kernel=bcd_kernel, **kw)
+    gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
+    for s in range(3):
+        batch = X[:, k + (5 + s) * eta:k + (6 + s) * eta]
+        out = ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+        A = gpu.get_codes().cpu().numpy()
+        st = gpu.get_state()
+        errs = dict(alpha=rel(A, out["A"]), Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar),
+                    D=rel(st["D"], ora.D))
+        assert all(v <= TOL_STEP for v in errs.values()), (s, errs)
+        notS = np.setdiff1d(np.arange(p), out["S"])
+        assert rel(st["Bbar"][notS], ora.Bbar[notS]) <= TOL_STEP
+        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
+                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
+
+
+def test_unbiased_mode_from_scratch_and_renormalised(somf):
+    """Mode U from t = 0 (w_1 = 1 zeroes every Bbar row, R6) with u = 0.05 so
+    that sigma_t = prod (1 - w_s) falls below 1e-20 within ~20 steps and the
+    library folds its lazy scale back into Bbar / Cbar (also on get_state, in
+    the middle of the run); 40 steps vs the oracle."""
+    p, k, eta, kw, kind = CASES["ridge_l1_fmri_small"]
+    kw = dict(kw, u=0.05)
+    X = _data(kind, p, k + 40 * eta)
+    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=5, b_mode="U", **kw))
+    ora.set_components(X[:, :k])
+    gpu = somf.Somf(p, k, eta, seed=5, debug=True, b_mode="unbiased", **kw)
+    gpu.set_components(cuda(X[:, :k]))
+    ora.D = f32(ora.D)
+    for t in range(40):
+        batch = X[:, k + t * eta:k + (t + 1) * eta]
+        ora.partial_fit(batch)
+        gpu.partial_fit(cuda(batch))
+        if t in (0, 13, 39):
+            st = gpu.get_state()
+            errs = dict(Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar), D=rel(st["D"], ora.D))
+            assert all(v <= 1e-3 for v in errs.values()), (t, errs)
+
+
 @pytest.mark.parametrize("name", ["cfgA_ridge_l1", "lasso_l2_hyper_small", "nmf_small"])
 def test_masked_api_and_pinned_input_match(somf, name):
     ora, gpu, X, (p, k, eta) = _pair(somf, name)

@@ -5,7 +5,8 @@ What the paper fixes, and the pin used:
     unbiasedness E[G] = D^T D, E[beta] = D^T x.
   * Cbar: symmetric PSD; w_t = 1/t gives the running mean.
   * Bbar modes: M leaves unmasked rows untouched; F equals the full OMF rule
-    (partition identity, P:602 + P:612).
+    (partition identity, P:602 + P:612); U (R6) is unbiased for F over the
+    masks (Monte Carlo, E[M_t] = I) and equals F and M at r = 1.
   * Alg. 4: freezing of unmasked rows (P:840-842); feasibility (Eq. 2);
     n_j = 1 - ||d_j||; surrogate non-increase on the masked rows
     (P:1175-1186); k = 1 and Cbar = I interior cases; full mask => radius 1.
@@ -108,6 +109,61 @@ def test_bbar_modes(mode):
         np.testing.assert_allclose(o.Bbar[notS], (1 - w) * B0[notS], rtol=1e-14)
         np.testing.assert_allclose(o.Bbar[S], (1 - w) * B0[S] + (w * 3.0 / eta) * X[S] @ A.T,
                                    rtol=1e-13, atol=1e-15)
+
+
+def test_bbar_mode_u_reduces_to_f_at_r1():
+    """r = 1 selects every row (Eq. mt): the unbiased mode U, the masked mode M
+    and Alg. 3's full mode F are then one rule (reading R5/R6) -- whole
+    trajectories, dictionary updates included, agree to rounding."""
+    p, k, eta = 40, 3, 5
+    rng = np.random.default_rng(12)
+    X = rng.standard_normal((p, 200))
+    outs = {}
+    for mode in ("U", "M", "F"):
+        o = SomfOracle(OracleConfig(p=p, k=k, eta=eta, lam=0.1, nu=1.0, mu=0.0, r=1.0, b_mode=mode, seed=4))
+        o.set_components(X[:, :k])
+        for t in range(12):
+            o.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
+        outs[mode] = (o.D.copy(), o.Bbar.copy(), o.Cbar.copy())
+    for mode in ("M", "F"):
+        for a, b in zip(outs["U"], outs[mode]):
+            np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-14)
+
+
+def test_bbar_mode_u_unbiased_monte_carlo(monkeypatch):
+    """Mode U's point (SURVEY 8c ledger 5-6): E over masks of its Bbar equals
+    Alg. 3's full-mode Bbar (P:602 + P:612), because E[M_t] = I.
+    With the codes held fixed (so they do not depend on the mask) and Alg. 4
+    frozen, the mean of mode-U Bbar over 3000 independent mask streams must
+    equal the deterministic mode-F Bbar within 4 standard errors; a dropped r,
+    a missing decay of the unmasked rows or a wrong weight fails it."""
+    import oracle.somf as osomf
+    p, k, eta, r, steps = 24, 2, 3, 3.0, 4
+    rng = np.random.default_rng(21)
+    D0 = rng.standard_normal((p, k))
+    Xs = [rng.standard_normal((p, eta)) for _ in range(steps)]
+    As = [rng.standard_normal((k, eta)) for _ in range(steps)]
+    it = {"i": 0}
+
+    def fixed_codes(G, beta, *a, **kw):
+        return As[it["i"]].copy()
+    monkeypatch.setattr(osomf, "solve_codes", fixed_codes)
+
+    def run(mode, seed):
+        o = SomfOracle(OracleConfig(p=p, k=k, eta=eta, lam=0.1, nu=1.0, mu=1.0, r=r, b_mode=mode, seed=seed))
+        o.set_components(D0)
+        o._partial_dictionary_update = lambda S, perm: None
+        for t in range(steps):
+            it["i"] = t
+            o.partial_fit(Xs[t])
+        return o.Bbar
+    ref = run("F", 0)
+    draws = np.stack([run("U", 1000 + s) for s in range(3000)])
+    mean = draws.mean(axis=0)
+    se = draws.std(axis=0, ddof=1) / np.sqrt(draws.shape[0])
+    assert np.all(np.abs(mean - ref) <= 4.0 * se + 1e-12), np.max(np.abs(mean - ref) / (se + 1e-30))
+    # and the estimator is not degenerate: single draws differ from F
+    assert np.max(np.abs(draws[0] - ref)) > 1e-3
 
 
 @pytest.mark.parametrize("mu,pos", [(0.0, False), (1.0, False), (0.5, False), (1.0, True), (0.0, True)])
