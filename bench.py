@@ -640,27 +640,32 @@ def run_somf(args):
             d0 = gen.batch(kk)
             res = {}
             for rr in rs:
-                m4 = somf_pkg.Somf(gen.p, kk, ee, r=rr, u=w["u"], seed=0, device=dev.index, stream=stream, **kw)
-                m4.set_components(d0)
-                for i in range(10):
-                    m4.partial_fit(pool[i % len(pool)])
-                torch.cuda.synchronize()
-                t4 = time_steps(m4, pool, 10, 5, flush, stream)
-                sm4 = sum(t4) / len(t4)
-                info4 = m4.last_step_info()
-                m4.profile_read()
-                m4.profile_enable(True)
-                time_steps(m4, pool, 15, 3, flush, stream)
-                pr4 = m4.profile_read()
-                m4.profile_enable(False)
-                roof4 = step_roofline_us(gen.p / rr, kk, ee, measured_peaks())
-                res[f"r={int(rr)}"] = {"columns_per_s": ee / (sm4 * 1e-3), "ms_per_step": sm4,
-                                       "roofline_us": roof4, "roofline_frac": roof4 / (sm4 * 1e3),
-                                       "bcd_kernel": m4.bcd_variant,
-                                       "bcd_grid_reductions": info4["bcd_reductions"], "q": info4["q"],
-                                       "phase_ms_per_step": {ph: v / max(pr4["steps"], 1)
-                                                             for ph, v in pr4["ms"].items() if v > 0}}
-                del m4
+                try:
+                    m4 = somf_pkg.Somf(gen.p, kk, ee, r=rr, u=w["u"], seed=0, device=dev.index, stream=stream, **kw)
+                    m4.set_components(d0)
+                    for i in range(10):
+                        m4.partial_fit(pool[i % len(pool)])
+                    torch.cuda.synchronize()
+                    t4 = time_steps(m4, pool, 10, 5, flush, stream)
+                    sm4 = sum(t4) / len(t4)
+                    info4 = m4.last_step_info()
+                    m4.profile_read()
+                    m4.profile_enable(True)
+                    time_steps(m4, pool, 15, 3, flush, stream)
+                    pr4 = m4.profile_read()
+                    m4.profile_enable(False)
+                    roof4 = step_roofline_us(gen.p / rr, kk, ee, measured_peaks())
+                    res[f"r={int(rr)}"] = {"columns_per_s": ee / (sm4 * 1e-3), "ms_per_step": sm4,
+                                           "roofline_us": roof4, "roofline_frac": roof4 / (sm4 * 1e3),
+                                           "bcd_kernel": m4.bcd_variant,
+                                           "bcd_grid_reductions": info4["bcd_reductions"], "q": info4["q"],
+                                           "phase_ms_per_step": {ph: v / max(pr4["steps"], 1)
+                                                                 for ph, v in pr4["ms"].items() if v > 0}}
+                    del m4
+                except somf_pkg.SomfError as e:
+                    # a secondary line must not take the headline down: record the failure
+                    res[f"r={int(rr)}"] = {"error": str(e)}
+                    print(f"bench: workload {name} r={rr} failed: {e}", file=sys.stderr, flush=True)
             workloads[name] = {"p": gen.p, "k": kk, "eta": ee, **{k_: v for k_, v in kw.items()}, "results": res}
 
     # --- CPU oracle baseline (rank 0, N = 1) ----------------------------------------

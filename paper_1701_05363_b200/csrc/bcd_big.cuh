@@ -688,7 +688,8 @@ k_bcd_big(NtArgs P, NbArgs A) {
       S2 = sm.S2;
       const double mnv = cnt > 0.0 ? (double)__uint_as_float(sm.mn) : INFINITY;
       const double mxv = (double)__uint_as_float(sm.mx);
-      conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol);
+      conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol,
+                            round >= kNtRelaxRound);
     }
     const bool all_conv = __syncthreads_and(conv);
     const bool capped = round + 1 >= P.max_rounds && !all_conv;

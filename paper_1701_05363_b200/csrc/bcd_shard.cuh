@@ -202,7 +202,7 @@ __global__ void k_shard_round(ShState S, const int64_t* __restrict__ q_dev, int 
 }
 
 // the Michelot step of every atom (identical on every rank); convergence flag
-__global__ void k_shard_update(ShState S, int k, double a, double b) {
+__global__ void k_shard_update(ShState S, int k, double a, double b, int round) {
   int conv = 1;
   for (int p = threadIdx.x; p < k; p += blockDim.x) {
     const double cnt = S.acc[3 * p], S1 = S.acc[3 * p + 1], S2 = S.acc[3 * p + 2];
@@ -210,7 +210,8 @@ __global__ void k_shard_update(ShState S, int k, double a, double b) {
     const double mxv = (double)__uint_as_float(S.mx[p]);
     int nmode;
     double nlam;
-    conv &= nt_atom_update(a, b, S.rho[p], cnt, S1, S2, mnv, mxv, S.mode[p], S.lam[p], &nmode, &nlam);
+    conv &= nt_atom_update(a, b, S.rho[p], cnt, S1, S2, mnv, mxv, S.mode[p], S.lam[p], &nmode, &nlam, kNtLamTol,
+                          round >= kNtRelaxRound);
     S.last[3 * p] = cnt;
     S.last[3 * p + 1] = S1;
     S.last[3 * p + 2] = S2;

@@ -1029,7 +1029,7 @@ static somf_status project_sharded(somf_ctx* h) {
     if (somf_status s = reduce(h, S.acc, 3 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
     if (somf_status s = reduce(h, S.mn, k, SOMF_DT_I32, SOMF_OP_MIN)) return s;
     if (somf_status s = reduce(h, S.mx, k, SOMF_DT_I32, SOMF_OP_MAX)) return s;
-    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b);
+    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b, it);
     CKL();
     CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, sizeof(int), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
@@ -1073,7 +1073,7 @@ static somf_status bcd_sharded(somf_ctx* h) {
     if (somf_status s = reduce(h, S.acc, 3 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
     if (somf_status s = reduce(h, S.mn, k, SOMF_DT_I32, SOMF_OP_MIN)) return s;
     if (somf_status s = reduce(h, S.mx, k, SOMF_DT_I32, SOMF_OP_MAX)) return s;
-    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b);
+    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b, r);
     CKL();
     CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, sizeof(int), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
