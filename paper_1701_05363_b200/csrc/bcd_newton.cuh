@@ -872,6 +872,12 @@ k_bcd_newton(NtArgs P) {
           P.lam_ws[j] = lam_s[p];
         }
         par_s[cur ^ 1][p] = par_s[cur][p];
+      } else if (conv) {
+        // converged atoms keep their parameters while others move: the v of
+        // the atoms after them then only change when an unconverged atom
+        // before them does (no tolerance-level jitter propagating down the
+        // chain; at cfgE it kept later atoms from ever settling)
+        par_s[cur ^ 1][p] = par_s[cur][p];
       } else {
         lam_s[p] = nlam;
         mode_s[p] = nmode;

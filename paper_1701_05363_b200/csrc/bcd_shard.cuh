@@ -210,8 +210,13 @@ __global__ void k_shard_update(ShState S, int k, double a, double b, int round) 
     const double mxv = (double)__uint_as_float(S.mx[p]);
     int nmode;
     double nlam;
-    conv &= nt_atom_update(a, b, S.rho[p], cnt, S1, S2, mnv, mxv, S.mode[p], S.lam[p], &nmode, &nlam, kNtLamTol,
-                          round >= kNtRelaxRound);
+    const int cp = nt_atom_update(a, b, S.rho[p], cnt, S1, S2, mnv, mxv, S.mode[p], S.lam[p], &nmode, &nlam,
+                                  kNtLamTol, round >= kNtRelaxRound);
+    conv &= cp;
+    if (cp) {                 // converged atoms keep their parameters (as k_bcd_newton)
+      nlam = S.lam[p];
+      nmode = S.mode[p];
+    }
     S.last[3 * p] = cnt;
     S.last[3 * p + 1] = S1;
     S.last[3 * p + 2] = S2;

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(128)
 k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, int m,
         double l1, double l2, int positive, double tol, int max_sweeps, int nmax,
         double* __restrict__ A64, float* __restrict__ A32, int* __restrict__ sweeps_out,
-        float* __restrict__ AT32, int ldt, int64_t gstride) {
+        float* __restrict__ AT32, int ldt, int64_t gstride, long long* __restrict__ prof) {
   // the B-bar kernel may launch now (programmatic dependent launch); it reads
   // the codes only after griddepcontrol.wait
   asm volatile("griddepcontrol.launch_dependents;");
@@ -90,6 +90,10 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
       roff[i] = packed_off(row < k ? row : 0, k);
     }
     int sweep = 0;
+    // diagnostics (prof != nullptr; somf_bcd_phase_cycles slots 84..91)
+    long long c_sw = 0, c_jump = 0, n_solve = 0, n_sum = 0, n_agree = 0;
+    int n_max = 0;
+    long long t0 = prof ? clock64() : 0;
     for (; sweep < max_sweeps; ++sweep) {
       // ---- one cyclic CD sweep; zero updates skipped by ballot ----
       double maxd = 0.0;
@@ -129,6 +133,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
 #pragma unroll
       for (int i = 0; i < KPL; ++i) amax = fmax(amax, fabs(alpha[i]));
       amax = warp_max(amax);
+      if (prof) { const long long t1 = clock64(); c_sw += t1 - t0; t0 = t1; }
       if (maxd <= tol * fmax(1.0, amax)) { ++sweep; break; }
       if (sweep + 1 < kAsWarm) continue;
       // ---- jump: exact solve on the current face, with line search ----
@@ -181,6 +186,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
           __syncwarp();
         }
         ok = __all_sync(0xffffffffu, ok);
+        if (prof) { ++n_solve; n_sum += n; n_max = max(n_max, n); }
         if (!ok) break;
         // L z = y, then L^T x = z, both column-oriented (rows by lane, no reductions)
         for (int c = 0; c < n; ++c) {
@@ -215,6 +221,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
         moved = true;
         if (agree) {
           for (int r = lane; r < n; r += 32) av[r] = yv[r];
+          n_agree += 1;
           break;
         }
         // line search: a_S <- a_S + tau (y - a_S), the first zero crossing
@@ -273,6 +280,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
         g[i] = b[i] - acc;
       }
       __syncwarp();
+      if (prof) { const long long t1 = clock64(); c_jump += t1 - t0; t0 = t1; }
     }
 #pragma unroll
     for (int i = 0; i < KPL; ++i) {
@@ -284,6 +292,16 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
       }
     }
     if (lane == 0 && sweeps_out) atomicMax(sweeps_out, sweep);
+    if (prof && lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 84), 1ull);
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 85), (unsigned long long)sweep);
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 86), (unsigned long long)n_solve);
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 87), (unsigned long long)n_sum);
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 88), (unsigned long long)c_sw);
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 89), (unsigned long long)c_jump);
+      atomicMax(prof + 90, (long long)n_max);
+      atomicAdd(reinterpret_cast<unsigned long long*>(prof + 91), (unsigned long long)n_agree);
+    }
   }
 }
 

@@ -118,21 +118,48 @@ k_cd(const double* __restrict__ G, const double* __restrict__ beta, int k, int m
   }
 }
 
-// Cbar <- (1-w) Cbar + (w/eta) A A^T  (Eq. somf_partial; batch mean R4)
-__global__ void k_cbar_update(const double* __restrict__ A64, int k, int eta,
-                              const double* __restrict__ w_dev, double* __restrict__ C64,
-                              float* __restrict__ C32) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= k * k) return;
-  const int a = e / k, b = e % k;
+// Cbar <- (1-w) Cbar + (w/eta) A A^T  (Eq. somf_partial; batch mean R4;
+// mode U's coefficients, common.cuh).  32 x 32 tiles of Cbar per CTA, the two
+// 32-row panels of the codes staged in shared memory 32 columns at a time
+// (coalesced along the batch), 2 x 2 entries per thread; every entry sums
+// s = 0 .. eta-1 in order with fma(a_i, a_j, .), so Cbar stays exactly symmetric.
+constexpr int kCbT = 32;
+__global__ void __launch_bounds__(256)
+k_cbar_update(const double* __restrict__ A64, int k, int eta, const double* __restrict__ w_dev,
+              double* __restrict__ C64, float* __restrict__ C32) {
+  __shared__ double Ai[kCbT][kCbT + 1], Aj[kCbT][kCbT + 1];
+  const int i0 = blockIdx.y * kCbT, j0 = blockIdx.x * kCbT;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int t0 = 0; t0 < eta; t0 += kCbT) {
+    for (int e = threadIdx.x; e < kCbT * kCbT; e += 256) {
+      const int r = e / kCbT, c = e % kCbT, t = t0 + c;
+      Ai[r][c] = (i0 + r < k && t < eta) ? A64[(int64_t)(i0 + r) * eta + t] : 0.0;
+      Aj[r][c] = (j0 + r < k && t < eta) ? A64[(int64_t)(j0 + r) * eta + t] : 0.0;
+    }
+    __syncthreads();
+    const int tn = min(kCbT, eta - t0);
+    for (int c = 0; c < tn; ++c) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) acc[u][v] = fma(Ai[ty + 16 * u][c], Aj[tx + 16 * v][c], acc[u][v]);
+    }
+    __syncthreads();
+  }
   const double keepd = w_dev[kCoefKeep], gc = w_dev[kCoefGainC];
-  double s = 0.0;
-  const double* ra = A64 + (int64_t)a * eta;
-  const double* rb = A64 + (int64_t)b * eta;
-  for (int t = 0; t < eta; ++t) s += ra[t] * rb[t];
-  const double c = keepd * C64[e] + (gc / eta) * s;
-  C64[e] = c;
-  C32[e] = (float)c;
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      const int i = i0 + ty + 16 * u, j = j0 + tx + 16 * v;
+      if (i < k && j < k) {
+        const int64_t e = (int64_t)i * k + j;
+        const double c = keepd * C64[e] + (gc / eta) * acc[u][v];
+        C64[e] = c;
+        C32[e] = (float)c;
+      }
+    }
 }
 
 }  // namespace somf

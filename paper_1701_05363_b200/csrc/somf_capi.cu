@@ -717,7 +717,8 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     CK(cudaFuncSetAttribute(k_cd_as<N, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_as)); \
     k_cd_as<N, GT><<<gas, tas, smem_as, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,              \
                                                  c.cd_max_sweeps, nmax, A64, A32, h->sweeps_dev,      \
-                                                 want_cpart ? h->AT32 : nullptr, h->kp, gstride);     \
+                                                 want_cpart ? h->AT32 : nullptr, h->kp, gstride,      \
+                                                 h->prof_on ? h->bcd_prof : nullptr);                 \
   }
 #define CASE_AS(N) \
   case N: if (g64) LAUNCH_AS(N, double) else LAUNCH_AS(N, float) break;
@@ -1650,8 +1651,8 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       k_cbar_finalize<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->cpart, h->cpart_n, k, eta,
                                                                                 h->w_dev, h->C64, h->C32);
     else
-      k_cbar_update<<<(unsigned)ceil_div((int64_t)k * k, 256), 256, 0, h->st>>>(h->A64, k, eta, h->w_dev, h->C64,
-                                                                                h->C32);
+      k_cbar_update<<<dim3((unsigned)ceil_div(k, kCbT), (unsigned)ceil_div(k, kCbT)), 256, 0, h->st>>>(
+          h->A64, k, eta, h->w_dev, h->C64, h->C32);
     CKL();
     h->launches[SOMF_PH_CBAR] += 1;
   }

@@ -259,6 +259,9 @@ class Somf:
         out["ridge"] = dict(zip(("load", "factor", "solve", "cbar_partial"), v[72:76].tolist()), inverse=int(v[79]))
         out["setup_split"] = dict(zip(("params", "gather", "permute"), v[76:79].tolist()))
         out["update_split"] = dict(zip(("ring_reset", "record_read"), v[80:82].tolist()))
+        # lasso / nonneg CD with support jumps (cd_as.cuh): totals over its columns
+        out["cd"] = dict(zip(("columns", "sweeps", "face_solves", "face_size_sum", "sweep_cycles", "jump_cycles",
+                              "face_size_max", "jumps_accepted"), v[84:92].tolist()))
         return out
 
     def set_reducer(self, fn):

@@ -228,8 +228,11 @@ def test_unbiased_mode_from_scratch_and_renormalised(somf):
     that sigma_t = prod (1 - w_s) falls below 1e-20 within ~20 steps and the
     library folds its lazy scale back into Bbar / Cbar (also on get_state, in
     the middle of the run); 40 steps vs the oracle."""
-    p, k, eta, kw, kind = CASES["ridge_l1_fmri_small"]
-    kw = dict(kw, u=0.05)
+    # (a well-conditioned case: with u = 0.05 the statistics forget within a few
+    # steps, and on the ill-conditioned fMRI case (ridge 1e-3) the fp32 / fp64
+    # trajectories part chaotically after ~20 steps whatever the scale handling)
+    p, k, eta, kw, kind = CASES["ridge_l2_r1"]
+    kw = dict(kw, r=4.0, u=0.05)
     X = _data(kind, p, k + 40 * eta)
     ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=5, b_mode="U", **kw))
     ora.set_components(X[:, :k])
@@ -240,7 +243,7 @@ def test_unbiased_mode_from_scratch_and_renormalised(somf):
         batch = X[:, k + t * eta:k + (t + 1) * eta]
         ora.partial_fit(batch)
         gpu.partial_fit(cuda(batch))
-        if t in (0, 13, 39):
+        if t in (0, 13, 25, 39):
             st = gpu.get_state()
             errs = dict(Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar), D=rel(st["D"], ora.D))
             assert all(v <= 1e-3 for v in errs.values()), (t, errs)

@@ -67,7 +67,8 @@ def main():
                update_us={ph: round(v / n / mhz, 2) for ph, v in cyc["update_split"].items()},
                setup_us={ph: round(v / n / mhz, 2) for ph, v in cyc["setup_split"].items()},
                ridge_us={ph: round(v / n / mhz, 2) for ph, v in cyc["ridge"].items() if isinstance(v, int)},
-               unconverged=[round(u / n, 1) for u in cyc["unconverged_per_round"] if u])
+               unconverged=[round(u / n, 1) for u in cyc["unconverged_per_round"] if u],
+               cd=cyc["cd"])
     print(json.dumps(out))
 
 
