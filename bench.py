@@ -548,7 +548,7 @@ def run_somf(args):
     if bcd_cyc["launches"]:
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
         roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
-                                         if ph not in ("launches", "unconverged_per_round", "frozen_prefix_per_round", "ridge",
+                                         if isinstance(v, int) and ph not in ("launches", "unconverged_per_round", "frozen_prefix_per_round", "ridge",
                                                        "setup_split", "update_split")}
         roof["bcd_update_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["update_split"].items()}
         roof["ridge_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["ridge"].items()}

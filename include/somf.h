@@ -256,8 +256,10 @@ int32_t somf_bcd_variant(somf_handle h);
  * out[4] 1 when mode FULL ran the complement rows on the side stream,
  * out[5], out[6] the simultaneous-threshold kernel's group shape: T threads
  * own M masked rows (1 x 1 and 2 x 1: packed-FFMA2 recurrence; 4 x 2 and
- * 8 x 2: shuffle recurrence), 0 for the other Alg. 4 kernels.
- * 0 before the first step.  Does not synchronise. */
+ * 8 x 2: shuffle recurrence), 0 for the other Alg. 4 kernels,
+ * out[7] 1 when the Alg. 4 kernel was a programmatic dependent launch of the
+ * kernel before it (its prologue overlapping that kernel's tail).
+ * 0 before the first step (out holds 8 entries).  Does not synchronise. */
 somf_status somf_last_kernels(somf_handle h, int32_t* out);
 
 /* SM-cycle breakdown of the simultaneous-threshold BCD kernel (CTA 0), summed
@@ -267,8 +269,15 @@ somf_status somf_last_kernels(somf_handle h, int32_t* out);
  * [7] launches, [8 + r] atoms not yet converged after round r (r < 64);
  * [72..75] ridge code kernel (CTA 0): load, factorisation, substitutions,
  * Cbar partial; [76..78] the setup of [0] split: parameters, row gathers,
- * permutation (the residual GEMM is [0] minus these).  cycles must hold 80 entries.  Synchronises.  Zeros for the
+ * permutation (the residual GEMM is [0] minus these); [84..91] lasso / nonneg
+ * CD (cd_as): columns, sweeps, face solves, summed face size, sweep cycles,
+ * jump cycles, largest face, accepted jumps; [92] k_bcd_big rounds whose first
+ * unconverged atom moved back; k_bcd_big per round r < 64: [8 + r] also holds
+ * the first unconverged position << 16, [96 + r] / [160 + r] its lambda and
+ * next lambda (double bits); at its round cap [72..79] that atom's state.
+ * cycles must hold SOMF_PROF_SLOTS entries.  Synchronises.  Zeros for the
  * kernels not launched. */
+#define SOMF_PROF_SLOTS 224
 somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles);
 
 /* ---- per-phase timing of somf_partial_fit (CUDA events on config.stream) ---- */

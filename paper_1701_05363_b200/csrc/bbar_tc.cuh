@@ -79,6 +79,10 @@ __device__ __forceinline__ uint32_t bt_off(int row, int kk, int nch) {
 }
 
 __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
+  // the BCD kernel may launch now (programmatic dependent launch): its CTAs
+  // take an SM as soon as my CTA there exits, and read what I write only
+  // after griddepcontrol.wait
+  asm volatile("griddepcontrol.launch_dependents;");
   extern __shared__ __align__(128) uint8_t bt_smem[];
   __shared__ uint32_t tmem_s;
   __shared__ __align__(8) uint64_t mbar;

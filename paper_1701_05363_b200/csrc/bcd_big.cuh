@@ -370,6 +370,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
   __shared__ float vlo_s[KPT];
   __shared__ int mode_s[KPT], jmap_s[KPT], pinv_s[KPT];
   __shared__ int mcnt_s;
+  __shared__ int lockF_s, firstU_s, prevF_s;   // locked prefix (R22), first unconverged position
   const int k = P.k, kp = P.kp;
   const int nthr = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -587,6 +588,10 @@ k_bcd_big(NtArgs P, NbArgs A) {
   unsigned nbar = 0;
   int round = 0, cur = 0;
   bool done = q == 0;
+  if (tid == 0) {
+    lockF_s = 0;
+    prevF_s = 0;
+  }
   if (done && P.idx_next) {
     ++nbar;
     nt_barrier(P.bar, nbar * G);
@@ -666,7 +671,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
     }
     // ---- the same Michelot step for every atom in every CTA ----
     int conv = 1, nmode = 0;
-    double nlam = 0.0, cnt = 0.0, S1 = 0.0, S2 = 0.0;
+    double nlam = 0.0, cnt = 0.0, S1 = 0.0, S2 = 0.0, mn_d = 0.0, mx_d = 0.0;
     const int p = tid;
     const bool act = tid < k;
     unsigned long long* rdp = reinterpret_cast<unsigned long long*>(pcn);
@@ -688,11 +693,50 @@ k_bcd_big(NtArgs P, NbArgs A) {
       S2 = sm.S2;
       const double mnv = cnt > 0.0 ? (double)__uint_as_float(sm.mn) : INFINITY;
       const double mxv = (double)__uint_as_float(sm.mx);
+      mn_d = mnv;
+      mx_d = mxv;
       conv = nt_atom_update(a, b, rho_s[p], cnt, S1, S2, mnv, mxv, mode_s[p], lam_s[p], &nmode, &nlam, P.lam_tol,
                             round >= kNtRelaxRound);
+      if (p < lockF_s) conv = 1;                  // locked prefix: parameters final (R22)
     }
+    // first unconverged position; after kNtRelaxRound every position before it
+    // is locked for the rest of the step (R22): in exact arithmetic the prefix
+    // never regresses (the recurrence is triangular and converged atoms keep
+    // their parameters), so the lock only guarantees termination
+    if (tid == 0) firstU_s = k;
+    __syncthreads();
+    if (act && !conv) atomicMin(&firstU_s, p);
     const bool all_conv = __syncthreads_and(conv);
+    if (tid == 0) {
+      if (P.prof && blockIdx.x == 0 && firstU_s < prevF_s)
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.prof + 92), 1ull);   // prefix regressions
+      prevF_s = firstU_s;
+      if (round >= kNtRelaxRound) lockF_s = max(lockF_s, firstU_s);
+    }
     const bool capped = round + 1 >= P.max_rounds && !all_conv;
+    if (P.prof && blockIdx.x == 0) {
+      // diagnostics: unconverged atoms per round (slots 8..71); at the round
+      // cap, the first unconverged position's state (slots 72..79, raw bits)
+      const int nun = __syncthreads_count(act && !conv);
+      if (tid == 0 && round < 64) atomicAdd(reinterpret_cast<unsigned long long*>(P.prof + 8 + round),
+                                            (unsigned long long)nun + ((unsigned long long)firstU_s << 16));
+      if (act && round < 64 && p == firstU_s) {
+        P.prof[96 + round] = __double_as_longlong(lam_s[p]);
+        P.prof[160 + round] = __double_as_longlong(nlam);
+      }
+      if (capped) {
+        if (tid == 0) mcnt_s = k;
+        __syncthreads();
+        if (act && !conv) atomicMin(&mcnt_s, p);
+        __syncthreads();
+        if (act && p == mcnt_s) {
+          const double dv[8] = {(double)p + 1000.0 * nmode + 100000.0 * mode_s[p], lam_s[p], nlam, cnt,
+                                mn_d, mx_d, rho_s[p], S1};
+          for (int i = 0; i < 8; ++i) P.prof[72 + i] = __double_as_longlong(dv[i]);
+        }
+        __syncthreads();
+      }
+    }
     if (act) {
       if (all_conv || capped) {
         if (mode_s[p] != kModeDead && blockIdx.x == 0) {

@@ -105,6 +105,9 @@ struct NtArgs {
   int64_t* nred_out;
   int* err;                 // 2 capacity, 4 round cap
   long long* prof;          // optional: SM cycles per phase, CTA 0 (8 slots), accumulated
+  int pdl;                  // launched as a programmatic dependent of the B-bar kernel: the
+                            // prologue stages what that kernel does not write (index list, D
+                            // rows, warm starts, M_{t+1}) before griddepcontrol.wait
 };
 
 // phase clock of CTA 0 (diagnostics only; prof == nullptr disables it)
@@ -535,31 +538,22 @@ k_bcd_newton(NtArgs P) {
   const double a = P.a, b = P.b;
   if (tid == 0) mcnt_s = 0;
   long long t_mark = clock64();
-  // ---- setup: round 1 (independent loads) ------------------------------------------
-  const bool cstage = (size_t)cap * LD >= (size_t)k * k + 4;
-  if (cstage) {
-    for (int e = tid; e < (k * k + 3) / 4; e += nthr) cp_async16(Rini + 4 * e, P.C32 + 4 * e);
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
+  // ---- setup: round 1 (independent of the B-bar kernel: with programmatic
+  // dependent launch this overlaps its tail) ---------------------------------------
   for (int r = tid; r < nr; r += nthr) rows_s[r] = P.idx[lo + r];
   for (int p = tid; p < k; p += nthr) {
     jmap_s[p] = P.perm_by_value ? P.perm_v[p] : P.perm[p];
-    diag_s[p] = P.C64[(int64_t)p * k + p];
     lws_s[p] = P.lam_ws[p];
     ns_s[p] = P.nslack[p];
   }
   __syncthreads();
-  // ---- round 2: the masked rows of D and Bbar (cp.async, every chunk in flight) ----
-  {
-    const int c4 = kp / 4;
-    for (int e = tid; e < nr * c4; e += nthr) {
-      const int row = e / c4, c = e % c4;
-      const int64_t goff = (int64_t)rows_s[row] * kp + 4 * c;
-      cp_async16(V + (size_t)row * kp + 4 * c, P.D + goff);
-      cp_async16(W + (size_t)row * kp + 4 * c, P.Bbar + goff);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
+  // ---- round 2: the masked rows of D (cp.async, every chunk in flight) ----------
+  const int c4 = kp / 4;
+  for (int e = tid; e < nr * c4; e += nthr) {
+    const int row = e / c4, c = e % c4;
+    cp_async16(V + (size_t)row * kp + 4 * c, P.D + (int64_t)rows_s[row] * kp + 4 * c);
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
   // M_{t+1} of my slice of Philox blocks while the rows are in flight
   uint8_t* mbits_s = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(nt_smem) + P.mbits_off);
   int64_t mb0 = 0;
@@ -577,6 +571,20 @@ k_bcd_newton(NtArgs P) {
     c = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
     if (lane == 0 && c) atomicAdd(&mcnt_s, c);
   }
+  // ---- round 3: what the B-bar kernel writes (Cbar, the masked Bbar rows) ----------
+  if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  const bool cstage = (size_t)cap * LD >= (size_t)k * k + 4;
+  if (cstage) {
+    for (int e = tid; e < (k * k + 3) / 4; e += nthr) cp_async16(Rini + 4 * e, P.C32 + 4 * e);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int e = tid; e < nr * c4; e += nthr) {
+    const int row = e / c4, c = e % c4;
+    cp_async16(W + (size_t)row * kp + 4 * c, P.Bbar + (int64_t)rows_s[row] * kp + 4 * c);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int p = tid; p < k; p += nthr) diag_s[p] = P.C64[(int64_t)p * k + p];
+  __syncthreads();
   if (wid == 0) {
     double dm = 1.0;
     for (int j = lane; j < k; j += 32) dm = fmax(dm, diag_s[j]);
@@ -607,7 +615,7 @@ k_bcd_newton(NtArgs P) {
       par_s[0][p] = par_s[1][p] = nt_make_par<kGen>(kModeDead, a, b, 0.0, -INFINITY);
     }
   }
-  asm volatile("cp.async.wait_group 1;" ::: "memory");     // Cbar staged
+  asm volatile("cp.async.wait_group 1;" ::: "memory");     // D rows and Cbar staged
   __syncthreads();
   for (int e = tid; e < k * KPT; e += nthr) {
     const int p = e / KPT, l = e % KPT;

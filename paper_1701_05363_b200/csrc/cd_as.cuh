@@ -33,6 +33,7 @@
 namespace somf {
 
 constexpr int kAsWarm = 3;          // CD sweeps before the first jump
+constexpr int kAsRowsPerLane = 4;   // face rows per lane in the factorisation (nmax <= 128)
 
 // per-warp scratch: packed lower face matrix, y, a_S, sidx, and a dense k-vector
 __host__ __device__ constexpr size_t cd_as_warp_bytes(int nmax, int k) {
@@ -166,26 +167,38 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
           yv[r] = beta[(int64_t)j * m + s] - l1 * (av[r] > 0.0 ? 1.0 : -1.0);
         }
         __syncwarp();
-        // Cholesky (right-looking, column by column; rows by lane); the
-        // diagonal holds 1 / L_cc (the substitutions multiply)
+        // Cholesky, left-looking (column c: every row r >= c, rows by lane,
+        // takes its dot product with row c over the finished columns q < c:
+        // independent shared-memory loads into register accumulators, no
+        // read-modify-write chain through shared memory); the diagonal holds
+        // 1 / L_cc (the substitutions multiply)
         bool ok = true;
         for (int c = 0; c < n; ++c) {
-          const double d = Af[pl_idx(c, c)];
+          const int cb = pl_idx(c, 0);
+          double sr[kAsRowsPerLane];
+#pragma unroll
+          for (int j = 0; j < kAsRowsPerLane; ++j) {
+            const int r = c + lane + 32 * j;
+            double acc = 0.0;
+            if (r < n) {
+              const int rb = pl_idx(r, 0);
+              acc = Af[rb + c];
+#pragma unroll 4
+              for (int q = 0; q < c; ++q) acc = fma(-Af[rb + q], Af[cb + q], acc);
+            }
+            sr[j] = acc;
+          }
+          const double d = __shfl_sync(0xffffffffu, sr[0], 0);     // row c (lane 0)
           if (!(d > 0.0)) { ok = false; break; }
           const double il = rsqrt(d);
           __syncwarp();
-          for (int r = c + 1 + lane; r < n; r += 32) Af[pl_idx(r, c)] *= il;
-          __syncwarp();
-          if (lane == 0) Af[pl_idx(c, c)] = il;
-          for (int r = c + 1 + lane; r < n; r += 32) {
-            const int rb = pl_idx(r, 0);
-            const double lrc = Af[rb + c];
-#pragma unroll 4
-            for (int q = c + 1; q <= r; ++q) Af[rb + q] = fma(-lrc, Af[pl_idx(q, c)], Af[rb + q]);
+#pragma unroll
+          for (int j = 0; j < kAsRowsPerLane; ++j) {
+            const int r = c + lane + 32 * j;
+            if (r < n) Af[pl_idx(r, c)] = r == c ? il : sr[j] * il;
           }
           __syncwarp();
         }
-        ok = __all_sync(0xffffffffu, ok);
         if (prof) { ++n_solve; n_sum += n; n_max = max(n_max, n); }
         if (!ok) break;
         // L z = y, then L^T x = z, both column-oriented (rows by lane, no reductions)

@@ -109,7 +109,7 @@ struct somf_ctx {
   int* cnt_next = nullptr;
   unsigned* ct_bar = nullptr;   // fused contract reduction barrier [arrivals, exits]
   int ct_launches = 2;          // kernels the last launch_contract issued
-  int kern[7] = {};             // kernel variants of the last step: contract, codes, bbar, bcd, bbar complement, BCD T, M
+  int kern[8] = {};             // kernel variants of the last step: contract, codes, bbar, bcd, bbar complement, BCD T, M, BCD PDL
   int64_t* q_next = nullptr;
   int64_t* t_next = nullptr;
   double* w_next = nullptr;
@@ -160,6 +160,7 @@ struct somf_ctx {
   double* lam_ws = nullptr;
   unsigned long long* nt_acc = nullptr;
   int nt_ncopy = 2;
+  bool nt_pdl = true;            // launch k_bcd_newton as a programmatic dependent (until refused)
   // simultaneous-threshold BCD for k <= 256 / streamed rows (bcd_big.cuh)
   const void* nb_fn = nullptr;
   int nb_kpt = 0, nb_T = 0, nb_ch = 0, nb_blk = 0, nb_tr = 0, nb_threads = 0, nb_rd_h = 1;
@@ -1229,7 +1230,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   A(dalloc(&h->oc_rho, (size_t)4 * k));
   A(dalloc(&h->oc_bar, 4));
   A(dalloc(&h->lam_ws, (size_t)k));
-  A(dalloc(&h->bcd_prof, kProfSlots));
+  A(dalloc(&h->bcd_prof, SOMF_PROF_SLOTS));
   h->nt_ncopy = c.bcd_copies > 0 ? std::min(c.bcd_copies, kNtMaxCopies) : 2;
   A(dalloc(&h->nt_acc, (size_t)(kNtRing + 1) * h->nt_ncopy * k * kNtRec));
   if (c.estimator != 0) {
@@ -1263,7 +1264,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       cudaMemset(h->theta_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->lam_ws, 0, (size_t)k * sizeof(double)) != cudaSuccess ||
       cudaMemset(h->AT32, 0, (size_t)c.eta * ((k + 3) & ~3) * sizeof(float)) != cudaSuccess ||
-      cudaMemset(h->bcd_prof, 0, kProfSlots * sizeof(long long)) != cudaSuccess ||
+      cudaMemset(h->bcd_prof, 0, SOMF_PROF_SLOTS * sizeof(long long)) != cudaSuccess ||
       init_nt_rec(h->nt_acc, (kNtRing + 1) * h->nt_ncopy * k) != cudaSuccess ||
       cudaMemset(h->D, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
       cudaMemset(h->Bbar, 0, (size_t)rows * h->kp * sizeof(float)) != cudaSuccess ||
@@ -1659,6 +1660,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
   {
     PhaseScope ps(h, SOMF_PH_BCD);                                           // Alg. 4
     h->kern[3] = h->reducer ? 4 : h->nt_fn ? 3 : h->nb_fn ? 5 : h->oc_fn ? 2 : 1;
+    h->kern[7] = 0;
     h->kern[5] = h->kern[3] == 3 ? h->nt_T : 0;
     h->kern[6] = h->kern[3] == 3 ? h->nt_M : 0;
     if (h->reducer) {
@@ -1684,7 +1686,7 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.pos = c.pos_dict;
       na.cap_rows = h->nt_cap_rows;
       na.ct_in_w = h->nt_ct_in_w;
-      na.max_rounds = 3 * k + 20;
+      na.max_rounds = 8 * k + 40;          // (R22: the locked prefix advances every few rounds)
       na.lam_tol = h->nt_lam_tol;
       // draw-ahead of t+1 (mask, atom order, t, w) inside the rounds
       na.idx_next = h->idx_next;
@@ -1710,7 +1712,36 @@ static somf_status partial_fit_impl(somf_handle h, const float* X, int64_t ld, b
       na.prof = h->prof_on ? h->bcd_prof : nullptr;
       if (h->nt_fn) {
         void* kargs[] = {&na};
-        CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(h->nt_threads), kargs, h->nt_smem, h->st));
+        // programmatic dependent launch of the cooperative grid: its prologue
+        // (index list, D rows, warm starts, M_{t+1}) overlaps the B-bar
+        // kernel's tail; the driver may refuse the combination (then a plain
+        // cooperative launch, once and for all)
+        bool launched = false;
+        if (h->nt_pdl) {
+          na.pdl = 1;
+          cudaLaunchConfig_t lc = {};
+          lc.gridDim = dim3(h->nsm);
+          lc.blockDim = dim3(h->nt_threads);
+          lc.dynamicSmemBytes = h->nt_smem;
+          lc.stream = h->st;
+          cudaLaunchAttribute at[2];
+          at[0].id = cudaLaunchAttributeCooperative;
+          at[0].val.cooperative = 1;
+          at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[1].val.programmaticStreamSerializationAllowed = 1;
+          lc.attrs = at;
+          lc.numAttrs = 2;
+          launched = cudaLaunchKernelExC(&lc, h->nt_fn, kargs) == cudaSuccess;
+          if (!launched) {
+            cudaGetLastError();
+            h->nt_pdl = false;
+          }
+        }
+        if (!launched) {
+          na.pdl = 0;
+          CK(cudaLaunchCooperativeKernel(h->nt_fn, dim3(h->nsm), dim3(h->nt_threads), kargs, h->nt_smem, h->st));
+        }
+        h->kern[7] = launched ? 1 : 0;
       } else {
         // pi, Cbar in pi order and prescaled per thread parity, then the rounds
         NbPerm pv{};
@@ -2000,10 +2031,10 @@ SOMF_EXPORT somf_status somf_set_reducer(somf_handle h, somf_reduce_fn fn, void*
 SOMF_EXPORT somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles) {
   if (!h || !cycles) return SOMF_E_ARG;
   CK(cudaStreamSynchronize(h->st));
-  long long v[kProfSlots];
+  long long v[SOMF_PROF_SLOTS];
   CK(cudaMemcpy(v, h->bcd_prof, sizeof(v), cudaMemcpyDeviceToHost));
   CK(cudaMemset(h->bcd_prof, 0, sizeof(v)));
-  for (int i = 0; i < kProfSlots; ++i) cycles[i] = v[i];
+  for (int i = 0; i < SOMF_PROF_SLOTS; ++i) cycles[i] = v[i];
   return SOMF_OK;
 }
 
@@ -2011,7 +2042,7 @@ SOMF_EXPORT int32_t somf_bcd_variant(somf_handle h) { return h ? (h->nt_fn ? 3 :
 
 SOMF_EXPORT somf_status somf_last_kernels(somf_handle h, int32_t* out) {
   if (!h || !out) return SOMF_E_ARG;
-  for (int i = 0; i < 7; ++i) out[i] = h->kern[i];
+  for (int i = 0; i < 8; ++i) out[i] = h->kern[i];
   return SOMF_OK;
 }
 

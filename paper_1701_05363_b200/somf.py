@@ -250,15 +250,17 @@ class Somf:
     BCD_PHASES = ("setup", "recurrence", "stats", "barrier", "update", "finish", "writeback")
 
     def bcd_phase_cycles(self):
-        v = np.zeros(96, np.int64)
+        v = np.zeros(224, np.int64)       # SOMF_PROF_SLOTS
         _check(lib().somf_bcd_phase_cycles(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
         out = dict(zip(self.BCD_PHASES, v[:7].tolist()), launches=int(v[7]))
         # slot 8 + r: (frozen prefix F << 16) + unconverged atoms, summed over launches
         out["unconverged_per_round"] = (v[8:72] & 0xFFFF).tolist()
+        out["first_unconverged_per_round"] = (v[8:72] >> 16).tolist()
         out["frozen_prefix_per_round"] = (v[8:72] >> 16).tolist()
         out["ridge"] = dict(zip(("load", "factor", "solve", "cbar_partial"), v[72:76].tolist()), inverse=int(v[79]))
         out["setup_split"] = dict(zip(("params", "gather", "permute"), v[76:79].tolist()))
         out["update_split"] = dict(zip(("ring_reset", "record_read"), v[80:82].tolist()))
+        out["raw"] = v.tolist()
         # lasso / nonneg CD with support jumps (cd_as.cuh): totals over its columns
         out["cd"] = dict(zip(("columns", "sweeps", "face_solves", "face_size_sum", "sweep_cycles", "jump_cycles",
                               "face_size_max", "jumps_accepted"), v[84:92].tolist()))
@@ -296,13 +298,13 @@ class Somf:
     def last_kernels(self):
         """Kernel variants of the last partial_fit (somf_last_kernels): names
         as in CONTRACT_KERNELS / CODES_KERNELS / BBAR_KERNELS."""
-        v = np.zeros(7, np.int32)
+        v = np.zeros(8, np.int32)
         _check(lib().somf_last_kernels(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
         inv = lambda d, x: {i: n for n, i in d.items()}.get(int(x), "none")  # noqa: E731
         return dict(contract=inv(CONTRACT_KERNELS, v[0]), codes=inv(CODES_KERNELS, v[1]),
                     bbar=inv(BBAR_KERNELS, v[2]),
                     bcd={1: "global", 2: "onchip", 3: "newton", 4: "sharded", 5: "big"}.get(int(v[3]), "none"),
-                    bbar_complement=bool(v[4]), bcd_group=(int(v[5]), int(v[6])))
+                    bbar_complement=bool(v[4]), bcd_group=(int(v[5]), int(v[6])), bcd_pdl=bool(v[7]))
 
     def last_step_info(self):
         q, nred, w = C.c_int64(), C.c_int64(), C.c_double()

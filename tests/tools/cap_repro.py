@@ -38,19 +38,29 @@ def main():
     m.set_components(d0)
     m.profile_enable(True)
     for t in range(args.steps):
-        before = m.bcd_phase_cycles()["unconverged_per_round"]
+        m.bcd_phase_cycles()                # (each read resets the counters)
         m.partial_fit(pool[t % len(pool)])
         torch.cuda.synchronize()
-        after = m.bcd_phase_cycles()["unconverged_per_round"]
-        unc = [a - b for a, b in zip(after, before)]
+        cyc = m.bcd_phase_cycles()
+        unc = cyc["unconverged_per_round"]
         try:
             info = m.last_step_info()
             print(json.dumps({"cfg": args.cfg, "r": args.r, "t": t + 1, "ok": True, "q": info["q"],
                               "nred": info["bcd_reductions"], "bcd": m.bcd_variant,
+                              "prefix_regressions": cyc["raw"][92],
                               "unconverged": [u for u in unc if u][:64]}), flush=True)
         except somf_pkg.SomfError as e:
+            import numpy as np
+            # k_bcd_big at its round cap: the first unconverged position's state
+            st = np.array(cyc["raw"][72:80], dtype=np.int64).view(np.float64).tolist()
             print(json.dumps({"cfg": args.cfg, "r": args.r, "t": t + 1, "ok": False, "err": str(e),
-                              "bcd": m.bcd_variant, "unconverged": unc[:64]}), flush=True)
+                              "bcd": m.bcd_variant, "unconverged": unc[:64], "prefix_regressions": cyc["raw"][92],
+                              "cap_state": dict(zip(("p+1000nmode+1e5mode", "lam", "nlam", "cnt", "min_above",
+                                                     "max_below", "rho", "S1"), st)),
+                              "first_unconverged": cyc["first_unconverged_per_round"],
+                              "lam_first": np.array(cyc["raw"][96:160], dtype=np.int64).view(np.float64).tolist(),
+                              "nlam_first": np.array(cyc["raw"][160:224], dtype=np.int64).view(np.float64).tolist()}),
+                  flush=True)
             break
 
 
