@@ -176,6 +176,16 @@ __device__ __forceinline__ int nt_atom_update(double a, double b, double rho, do
     // exact when the active set at the new threshold is still "every nonzero"
     const bool exact = nlam == 0.0 || !(a > 0.0) || a * nlam < mnv || relax;
     conv = exact && nmode == mode && fabs(nlam - lam) <= tol * fmax(nlam, 1e-300);
+  } else if (!(cnt > 0.0) && a > 0.0 && mxv > 0.0 &&
+             a * enet_lambda(a, b, rho, 1.0, mxv, mxv * mxv) >= mxv * (1.0 - 1e-6)) {
+    // every |v| is at or below the threshold (d = 0) and even the largest
+    // entry alone would sit at the threshold to within rounding: rho is below
+    // the resolution of the norm (R11 limit, ~3e-18 seen at cfgE), so d = 0 is
+    // the projection to rounding.  (Restarting from the full set here -- the
+    // overshoot rule below -- would climb back to the same threshold and cycle.)
+    nlam = lam;
+    nmode = mode;
+    conv = 1;
   } else {
     nlam = enet_lambda(a, b, rho, cnt, S1, S2);
     nmode = nlam > 0.0 ? kModeShrink : kModeCopy;
