@@ -119,9 +119,7 @@ typedef struct somf_config {
   int32_t codes_kernel;   /* (a2) codes (Eq. somf_alpha): 0 auto, 1 ridge
                              Cholesky (nu = 1, no positivity, k <= 160),
                              2 coordinate descent with exact support jumps
-                             (k >= 32), 3 plain cyclic coordinate descent,
-                             4 ridge by the sweep operator (Gauss-Jordan
-                             inverse of G + lambda I; same conditions as 1)  */
+                             (k >= 32), 3 plain cyclic coordinate descent     */
   double bcd_lam_tol;     /* simultaneous-threshold Alg. 4: relative
                              tolerance on each projection multiplier between
                              two rounds (0 = default 1e-5)     */

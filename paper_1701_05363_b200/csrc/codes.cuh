@@ -329,124 +329,6 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
 #undef RC_MARK
 }
 
-// ---------------------------------------------------------------------------
-// k_ridge_sweep: alpha = (G + lambda I)^-1 beta by the symmetric sweep
-// operator (Gauss-Jordan inversion in place, no pivoting: G + lambda I is SPD,
-// every pivot is a positive Schur complement).  Sweeping pivot c maps
-//   h_cc -> -1 / d,  h_ic -> h_ic / d,  h_cj -> h_cj / d,
-//   h_ij -> h_ij - h_ic h_cj / d            (i, j != c; d = h_cc)
-// and after all k pivots H = -(G + lambda I)^-1.  Each step is ONE barrier:
-// thread t keeps the entries (i = t / 4, j = 4 u + t % 4) of its row in
-// registers; the pivot column of step c (= the pivot row: the sweep keeps H
-// exactly symmetric, the product h_ic h_cj is formed in the same order for
-// (i, j) and (j, i)) is published by its owners into a ping-pong buffer.
-// Versus the blocked Cholesky + substitutions (k_ridge_codes), the chain is
-// k barrier steps with no triangular solves after it: alpha = -H beta is a
-// plain product (4 threads per row, two shuffles).  Each CTA inverts
-// redundantly and solves cpc right-hand sides, with the Cbar partial as in
-// k_ridge_codes.  NJ = entries per thread = ceil(k / 4).
-// ---------------------------------------------------------------------------
-template <int NJ>
-__global__ void __launch_bounds__(4 * 4 * NJ)
-k_ridge_sweep(const double* __restrict__ G, const double* __restrict__ beta, int k, int m, double lam,
-              double* __restrict__ A64, float* __restrict__ A32, float* __restrict__ AT32, int ldt,
-              double* __restrict__ cpart, int* __restrict__ err, long long* __restrict__ prof,
-              int64_t gstride, int cpc) {
-  asm volatile("griddepcontrol.launch_dependents;");
-  G += (int64_t)blockIdx.x * gstride;
-  extern __shared__ double rs_smem[];
-  double* pc = rs_smem;                        // 2 x k: pivot column ping-pong
-  double* bs = pc + 2 * k;                     // cpc x k: right-hand sides
-  double* Y = bs + (size_t)cpc * k;            // cpc x k: codes (Cbar partial)
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int i = tid >> 2, jq = tid & 3;
-  const bool rowv = i < k;
-  long long t_mark = clock64();
-#define RS_MARK(slot)                                                     \
-  do {                                                                    \
-    if (prof && blockIdx.x == 0 && threadIdx.x == 0) {                    \
-      const long long now_ = clock64();                                   \
-      prof[slot] += now_ - t_mark;                                        \
-      t_mark = now_;                                                      \
-    }                                                                     \
-  } while (0)
-  double h[NJ];
-#pragma unroll
-  for (int u = 0; u < NJ; ++u) {
-    const int j = 4 * u + jq;
-    h[u] = (rowv && j < k) ? __ldg(G + (int64_t)i * k + j) + (i == j ? lam : 0.0) : 0.0;
-    if (rowv && j == 0) pc[i] = h[u];                                 // pivot column of step 0
-  }
-  __syncthreads();
-  RS_MARK(0);
-  bool bad = false;
-  for (int c = 0; c < k; ++c) {
-    const double* col = pc + (c & 1) * k;
-    double* nxt = pc + ((c + 1) & 1) * k;
-    const double d = col[c];
-    bad |= !(d > 0.0);
-    const double id = 1.0 / d;
-    const double hic = rowv ? col[i] : 0.0;
-#pragma unroll
-    for (int u = 0; u < NJ; ++u) {
-      const int j = 4 * u + jq;
-      if (j < k) {
-        const double hcj = col[j];
-        double v;
-        if (i == c) v = j == c ? -id : hcj * id;
-        else if (j == c) v = hic * id;
-        else v = fma(-(hic * hcj), id, h[u]);
-        h[u] = v;
-        if (j == c + 1 && rowv) nxt[i] = v;
-      }
-    }
-    __syncthreads();
-  }
-  if (bad && err && threadIdx.x == 0) atomicExch(err, 1);
-  RS_MARK(1);
-  // alpha = -H beta for my cpc right-hand sides
-  for (int s0 = blockIdx.x * cpc; s0 < m; s0 += gridDim.x * cpc) {
-    const int ns = min(cpc, m - s0);
-    for (int e = tid; e < ns * k; e += blockDim.x) {
-      const int sl = e / k, r = e % k;
-      bs[e] = __ldg(beta + (int64_t)r * m + s0 + sl);
-    }
-    __syncthreads();
-    for (int sl = 0; sl < ns; ++sl) {
-      double acc = 0.0;
-#pragma unroll
-      for (int u = 0; u < NJ; ++u) {
-        const int j = 4 * u + jq;
-        if (j < k) acc = fma(h[u], bs[sl * k + j], acc);
-      }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      const int s = s0 + sl;
-      if (rowv && jq == 0) {
-        const double a = -acc;
-        Y[sl * k + i] = a;
-        A64[(int64_t)i * m + s] = a;
-        A32[(int64_t)i * m + s] = (float)a;
-        if (AT32) AT32[(int64_t)s * ldt + i] = (float)a;
-      }
-    }
-    __syncthreads();
-    if (cpart) {
-      double* out = cpart + (size_t)blockIdx.x * k * k;
-      for (int e = tid; e < k * k; e += blockDim.x) {
-        const int a = e / k, b = e % k;
-        double acc = 0.0;
-        for (int sl = 0; sl < ns; ++sl) acc = fma(Y[sl * k + a], Y[sl * k + b], acc);
-        out[e] = acc;
-      }
-    }
-    __syncthreads();
-  }
-  RS_MARK(2);
-#undef RS_MARK
-  (void)lane;
-}
-
 __global__ void k_cbar_finalize(const double* __restrict__ cpart, int nparts, int k, int eta,
                                 const double* __restrict__ w_dev, double* __restrict__ C64,
                                 float* __restrict__ C32) {

@@ -621,7 +621,7 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
   return SOMF_OK;
 }
 
-// sel: 0 auto, 1 ridge Cholesky, 2 CD with support jumps, 3 plain CD, 4 ridge sweep (somf_config.codes_kernel)
+// sel: 0 auto, 1 ridge Cholesky, 2 CD with support jumps, 3 plain CD (somf_config.codes_kernel)
 // gstride > 0: column s uses the Gram G + s gstride (estimator (b)), one column per CTA
 static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta, int m, double tol,
                                 double* A64, float* A32, bool want_cpart = false, int64_t gstride = 0) {
@@ -633,37 +633,9 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
   const int grid = (int)std::max<int64_t>(1, ceil_div(m, nw));
   h->cpart_n = 0;
   const bool ridge_ok = c.nu == 1.0 && !c.pos_code && k <= kRcMaxK;
-  if ((sel == 1 || sel == 4) && !ridge_ok) {
+  if (sel == 1 && !ridge_ok) {
     set_err(h, "codes_kernel = ridge requires nu = 1, no positivity and k <= %d", kRcMaxK);
     return SOMF_E_UNSUPPORTED;
-  }
-  if (ridge_ok && sel == 4) {
-    // ridge closed form by the sweep operator (Gauss-Jordan inverse, codes.cuh)
-    const int nj = (k + 3) / 4;
-    const int NJ = nj <= 8 ? 8 : nj <= 18 ? 18 : nj <= 24 ? 24 : nj <= 32 ? 32 : 40;
-    const int cpc = gstride > 0 ? 1 : (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(m, h->nsm)));
-    const int g = (want_cpart || gstride > 0) ? (int)ceil_div(m, cpc)
-                                              : (int)std::min<int64_t>(ceil_div(m, cpc), 4 * h->nsm);
-    if (want_cpart) {
-      if (!h->cpart) CK(dalloc(&h->cpart, (size_t)c.eta * k * k));
-      h->cpart_n = g;
-    }
-    double* cp = want_cpart ? h->cpart : nullptr;
-    const size_t smem = ((size_t)2 * k + (size_t)2 * cpc * k) * sizeof(double);
-    const void* fn = NJ == 8 ? (const void*)k_ridge_sweep<8> : NJ == 18 ? (const void*)k_ridge_sweep<18>
-                   : NJ == 24 ? (const void*)k_ridge_sweep<24> : NJ == 32 ? (const void*)k_ridge_sweep<32>
-                                                               : (const void*)k_ridge_sweep<40>;
-    double lam = c.lambda;
-    long long* rprof = h->prof_on ? h->bcd_prof + 72 : nullptr;
-    float* at = want_cpart ? h->AT32 : nullptr;
-    int ldt = h->kp;
-    int cpc_a = cpc;
-    void* args[] = {(void*)&G, (void*)&beta, (void*)&k, (void*)&m, (void*)&lam, (void*)&A64, (void*)&A32,
-                    (void*)&at, (void*)&ldt, (void*)&cp, (void*)&h->err_dev, (void*)&rprof, (void*)&gstride,
-                    (void*)&cpc_a};
-    CK(cudaLaunchKernel(fn, dim3(g), dim3(16 * NJ), args, smem, h->st));
-    h->kern[1] = 4;
-    return SOMF_OK;
   }
   if (ridge_ok && (sel == 0 || sel == 1)) {
     // ridge closed form (v3): every CTA factorises and solves cpc right-hand sides
@@ -1182,7 +1154,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
       !(c.cd_tol > 0.0) || c.cd_max_sweeps < 1 || c.row_hi - c.row_lo > (int64_t)INT32_MAX;
   if (bad) return SOMF_E_ARG;
   if (c.bcd_kernel < 0 || c.bcd_kernel > 4) return SOMF_E_ARG;
-  if (c.codes_kernel < 0 || c.codes_kernel > 4 || c.contract_kernel < 0 || c.contract_kernel > 4 ||
+  if (c.codes_kernel < 0 || c.codes_kernel > 3 || c.contract_kernel < 0 || c.contract_kernel > 4 ||
       c.bbar_kernel < 0 || c.bbar_kernel > 4)
     return SOMF_E_ARG;
   if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL && c.b_mode != SOMF_B_UNBIASED) return SOMF_E_ARG;

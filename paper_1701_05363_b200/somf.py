@@ -54,7 +54,7 @@ B_MODES = {"masked": 0, "unbiased": 1, "full": 2}
 # kernel selection (somf_config *_kernel fields, include/somf.h)
 CONTRACT_KERNELS = {"auto": 0, "tc": 1, "slice": 2, "tiled": 3, "generic": 4}
 BBAR_KERNELS = {"auto": 0, "tc": 1, "slice": 2, "tiled": 3, "generic": 4}
-CODES_KERNELS = {"auto": 0, "ridge": 1, "cd_jump": 2, "cd": 3, "sweep": 4}
+CODES_KERNELS = {"auto": 0, "ridge": 1, "cd_jump": 2, "cd": 3}
 
 
 class _CudaArray:

@@ -234,7 +234,7 @@ def test_bbar_variants(somf, name, variant):
     assert gpu.last_kernels()["bbar"] == variant
 
 
-@pytest.mark.parametrize("variant", ["ridge", "sweep", "cd_jump", "cd"])
+@pytest.mark.parametrize("variant", ["ridge", "cd_jump", "cd"])
 @pytest.mark.parametrize("name", list(VARIANT_CASES))
 def test_codes_variants(somf, name, variant):
     # plain CD stops on max |delta| <= cd_tol; on the ill-conditioned NMF Gram

@@ -272,34 +272,6 @@ def test_masked_api_and_pinned_input_match(somf, name):
         np.testing.assert_array_equal(s3[key], s2[key])
 
 
-@pytest.mark.parametrize("name", ["cfgA_ridge_l1", "ridge_l1_fmri_small", "ridge_l2_r1"])
-def test_ridge_sweep_codes(somf, name):
-    """The sweep-operator ridge solver (codes_kernel 4: Gauss-Jordan inverse of
-    G + lambda I) against the oracle's closed form, three consecutive steps
-    (its Cbar partials feed the B-bar kernel's Cbar fold)."""
-    p, k, eta, kw, kind = CASES[name]
-    X = _data(kind, p, k + 9 * eta)
-    ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=3, **kw))
-    ora.set_components(X[:, :k])
-    for t in range(5):
-        ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
-    ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
-    gpu = somf.Somf(p, k, eta, seed=3, debug=True, codes_kernel="sweep", **kw)
-    gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
-    for s in range(3):
-        batch = X[:, k + (5 + s) * eta:k + (6 + s) * eta]
-        out = ora.partial_fit(batch)
-        gpu.partial_fit(cuda(batch))
-        assert gpu.last_kernels()["codes"] == "sweep"
-        A = gpu.get_codes().cpu().numpy()
-        st = gpu.get_state()
-        errs = dict(alpha=rel(A, out["A"]), Cbar=rel(st["Cbar"], ora.Cbar), Bbar=rel(st["Bbar"], ora.Bbar),
-                    D=rel(st["D"], ora.D))
-        assert all(v <= TOL_STEP for v in errs.values()), (s, errs)
-        ora.D, ora.Bbar, ora.Cbar, ora.n = (st["D"].astype(np.float64), st["Bbar"].astype(np.float64),
-                                            st["Cbar"].astype(np.float64), st["n"].astype(np.float64))
-
-
 def test_empty_mask_step(somf):
     """r so large that S_t is empty: codes are 0 (G = 0, beta = 0), D frozen."""
     p, k, eta = 64, 4, 5
