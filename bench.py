@@ -679,7 +679,8 @@ def run_somf(args):
 
     launches = int(sum(prof["launches"].values()))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": step_ms, "ms_per_step_median": statistics.median(ms),
+            "higher_is_better": True,
             "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (fMRI-shaped stand-in, DESIGN.md §3)",
             "config": {"workload": w["name"], "p": p, "k": k, "eta": eta, "r": r, "lambda": w["lam"],

@@ -142,6 +142,11 @@ typedef struct somf_config {
                              CTA with more rows streams its tiles from an
                              L2 / HBM scratch every round.  Performance /
                              test knob only: the result does not depend on it */
+  int32_t bcd_group;      /* bcd_kernel 3: threads per masked row of the
+                             recurrence (0 auto, 1 one thread per row, 2 two
+                             threads per row, 4 the v5 groups of 4 (8) threads
+                             x 2 rows).  Performance knob; SOMF_E_UNSUPPORTED
+                             when the requested group does not fit        */
 } somf_config;
 
 /* Fills *cfg with defaults: u = 0.917, r = 1, nu = 1, mu = 0,

@@ -96,7 +96,7 @@ class SomfConfig(C.Structure):
         ("contract_kernel", C.c_int32), ("bbar_kernel", C.c_int32), ("codes_kernel", C.c_int32),
         ("bcd_lam_tol", C.c_double), ("bcd_copies", C.c_int32),
         ("estimator", C.c_int32), ("n_samples", C.c_int64), ("v", C.c_double),
-        ("bcd_tile_rows", C.c_int32),
+        ("bcd_tile_rows", C.c_int32), ("bcd_group", C.c_int32),
     ]
 
 

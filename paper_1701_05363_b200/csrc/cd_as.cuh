@@ -181,28 +181,16 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
             const int r = c + lane + 32 * j;
             double acc = 0.0;
             if (r < n) {
-              // four partial sums: the dot product's dependent chain is a quarter as long
               const int rb = pl_idx(r, 0);
-              double a0 = Af[rb + c], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-              int q = 0;
-              for (; q + 4 <= c; q += 4) {
-                a0 = fma(-Af[rb + q], Af[cb + q], a0);
-                a1 = fma(-Af[rb + q + 1], Af[cb + q + 1], a1);
-                a2 = fma(-Af[rb + q + 2], Af[cb + q + 2], a2);
-                a3 = fma(-Af[rb + q + 3], Af[cb + q + 3], a3);
-              }
-              for (; q < c; ++q) a0 = fma(-Af[rb + q], Af[cb + q], a0);
-              acc = (a0 + a1) + (a2 + a3);
+              acc = Af[rb + c];
+#pragma unroll 4
+              for (int q = 0; q < c; ++q) acc = fma(-Af[rb + q], Af[cb + q], acc);
             }
             sr[j] = acc;
           }
           const double d = __shfl_sync(0xffffffffu, sr[0], 0);     // row c (lane 0)
           if (!(d > 0.0)) { ok = false; break; }
-          // 1 / sqrt(d): fp32 seed + two fp64 Newton steps (relative error ~1e-16)
-          double il = (double)rsqrtf((float)d);
-          il = il * fma(-0.5 * d, il * il, 1.5);
-          il = il * fma(-0.5 * d, il * il, 1.5);
-          if (!(d > 1e-30 && d < 1e30)) il = rsqrt(d);          // outside the fp32 seed's range
+          const double il = rsqrt(d);
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < kAsRowsPerLane; ++j) {
@@ -298,16 +286,11 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
 #pragma unroll
       for (int i = 0; i < KPL; ++i) {
         const int row = lane + 32 * i;
-        double acc = 0.0, acc2 = 0.0;
+        double acc = 0.0;
         if (row < k) {
-          int r = 0;
-          for (; r + 2 <= n; r += 2) {
-            acc = fma((double)packed_get(Pk, row, sidx[r], k), av[r], acc);
-            acc2 = fma((double)packed_get(Pk, row, sidx[r + 1], k), av[r + 1], acc2);
-          }
-          if (r < n) acc = fma((double)packed_get(Pk, row, sidx[r], k), av[r], acc);
+          for (int r = 0; r < n; ++r) acc = fma((double)packed_get(Pk, row, sidx[r], k), av[r], acc);
         }
-        g[i] = b[i] - (acc + acc2);
+        g[i] = b[i] - acc;
       }
       __syncwarp();
       if (prof) { const long long t1 = clock64(); c_jump += t1 - t0; t0 = t1; }

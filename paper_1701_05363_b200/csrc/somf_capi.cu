@@ -808,7 +808,9 @@ static void choose_newton(somf_ctx* h) {
     const int cands[3][2] = {{1, 1}, {2, 1}, {v.kpt > 96 ? 8 : 4, 2}};
     for (const auto& tm : cands) {
       const int Tv = tm[0], M = tm[1];
-      if (Tv == 1 && (v.kpt > 96 || cap < 96)) continue;
+      const int want = h->cfg.bcd_group;
+      if (want && !(want == Tv || (want == 4 && M == 2))) continue;
+      if (Tv == 1 && (v.kpt > 96 || (cap < 96 && !want))) continue;
       const int64_t groups = ceil_div(cap, M);
       if (Tv * groups > max_thr) continue;
       // >= k threads: the per-atom statistics and threshold updates run one
@@ -1160,6 +1162,7 @@ SOMF_EXPORT somf_status somf_create(const somf_config* cfg, somf_handle* out) {
   if (c.b_mode != SOMF_B_MASKED && c.b_mode != SOMF_B_FULL && c.b_mode != SOMF_B_UNBIASED) return SOMF_E_ARG;
   if (c.estimator < 0 || c.estimator > 2) return SOMF_E_ARG;
   if (c.bcd_tile_rows < 0) return SOMF_E_ARG;
+  if (c.bcd_group != 0 && c.bcd_group != 1 && c.bcd_group != 2 && c.bcd_group != 4) return SOMF_E_ARG;
   if (c.estimator != 0 && (c.n_samples < 1 || !(c.v > 0.0 && c.v <= 1.0))) return SOMF_E_ARG;
   somf_ctx* h = new somf_ctx();
   h->cfg = c;

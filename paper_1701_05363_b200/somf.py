@@ -92,7 +92,8 @@ class Somf:
                  stream=None, debug: bool = False, bcd_kernel: str = "auto",
                  contract_kernel: str = "auto", bbar_kernel: str = "auto", codes_kernel: str = "auto",
                  bcd_lam_tol: float = 0.0, bcd_copies: int = 0,
-                 estimator: str = "a", n_samples: int = 0, v: float = 0.751, bcd_tile_rows: int = 0):
+                 estimator: str = "a", n_samples: int = 0, v: float = 0.751, bcd_tile_rows: int = 0,
+                 bcd_group: int = 0):
         L = lib()
         cfg = _lib.SomfConfig()
         L.somf_config_default(C.byref(cfg))
@@ -121,6 +122,7 @@ class Somf:
         cfg.n_samples = n_samples
         cfg.v = v
         cfg.bcd_tile_rows = bcd_tile_rows
+        cfg.bcd_group = bcd_group
         h = C.c_void_p()
         st = L.somf_create(C.byref(cfg), C.byref(h))
         if st != 0:

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--copies", type=int, default=0)
     ap.add_argument("--bcd-kernel", default="auto")
     ap.add_argument("--tile-rows", type=int, default=0)
+    ap.add_argument("--group", type=int, default=0)
     ap.add_argument("--codes-kernel", default="auto")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
@@ -46,7 +47,8 @@ def main():
         d0 = gen.batch(k)
         p = gen.p
     m = somf_pkg.Somf(p, k, eta, r=args.r, u=0.917, seed=0, device=0, stream=stream, bcd_copies=args.copies,
-                      bcd_kernel=args.bcd_kernel, bcd_tile_rows=args.tile_rows, codes_kernel=args.codes_kernel, **kw)
+                      bcd_kernel=args.bcd_kernel, bcd_tile_rows=args.tile_rows, codes_kernel=args.codes_kernel,
+                      bcd_group=args.group, **kw)
     m.set_components(d0)
     for i in range(args.burn):
         m.partial_fit(batches[i % len(batches)])
