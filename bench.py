@@ -491,6 +491,15 @@ def run_somf(args):
     bcd_cyc = model.bcd_phase_cycles()
     model.profile_enable(False)
     prof["launches"] = launch_counts["launches"]
+    # host time of one somf_partial_fit call (enqueue only: argument checks,
+    # by-value parameters, launches), the GPU working behind it
+    torch.cuda.synchronize()
+    host_us = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        model.partial_fit(batches[(2 * args.steps + args.warmup + i) % nb])
+        host_us.append((time.perf_counter() - t0) * 1e6)
+    torch.cuda.synchronize()
     step_ms = sum(ms) / len(ms)
     if world > 1:
         tt = torch.tensor([step_ms], device=dev)
@@ -691,6 +700,7 @@ def run_somf(args):
                        "parallelism": "single" if world == 1 else f"row-sharded x{world} ({args.dist_backend} allreduce)"},
             "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "gpu_launches_per_step": launches / steps_prof,
+            "host_us_per_call": statistics.median(host_us),
             "clocks": clk, "sweep": sweep, "workloads": workloads, "wall_s_timed": t_wall}
     if rank == 0:
         print(json.dumps(line), flush=True)

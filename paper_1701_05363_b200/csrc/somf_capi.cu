@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/somf.h"
@@ -161,6 +162,10 @@ struct somf_ctx {
   unsigned long long* nt_acc = nullptr;
   int nt_ncopy = 2;
   bool nt_pdl = true;            // launch k_bcd_newton as a programmatic dependent (until refused)
+  // per-kernel dynamic shared memory already granted and occupancy already
+  // queried (the per-step launch paths ask once, not every partial_fit)
+  std::unordered_map<const void*, int> smem_set;
+  std::unordered_map<uint64_t, int> occ_cache;
   // simultaneous-threshold BCD for k <= 256 / streamed rows (bcd_big.cuh)
   const void* nb_fn = nullptr;
   int nb_kpt = 0, nb_T = 0, nb_ch = 0, nb_blk = 0, nb_tr = 0, nb_threads = 0, nb_rd_h = 1;
@@ -271,6 +276,29 @@ static somf_status post_call(somf_ctx* h) {
   return SOMF_OK;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size
+static cudaError_t smem_attr(somf_ctx* h, const void* fn, size_t smem) {
+  auto it = h->smem_set.find(fn);
+  if (it != h->smem_set.end() && it->second >= (int)smem) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) h->smem_set[fn] = (int)smem;
+  return e;
+}
+
+// resident CTAs per SM of (fn, threads, smem), queried once (0 on error)
+static int occupancy(somf_ctx* h, const void* fn, int threads, size_t smem) {
+  const uint64_t key = (uint64_t)(uintptr_t)fn * 1000003ull ^ ((uint64_t)threads << 40) ^ (uint64_t)smem;
+  auto it = h->occ_cache.find(key);
+  if (it != h->occ_cache.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 0;
+  }
+  h->occ_cache[key] = occ;
+  return occ;
+}
+
 // Device-readable address for a pointer that is device memory or mapped pinned host memory.
 static somf_status resolve_in(somf_ctx* h, const void* p, const void** out, bool* is_host = nullptr) {
   if (is_host) *is_host = false;
@@ -362,8 +390,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
     a.np = (k + 15) & ~15;
     a.ep = (eta + 15) & ~15;
     const size_t smem = tc_smem;
-    if (cudaFuncSetAttribute((const void*)k_bbar_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-            cudaSuccess) {
+    if (smem_attr(h, (const void*)k_bbar_tc, smem) == cudaSuccess) {
       a.idx = all_rows ? nullptr : h->idx;
       a.xcompact = all_rows ? 0 : xcompact;
       a.q_dev = q_dev;
@@ -417,8 +444,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
       if (bv.kc == kc && bv.rt == rt) v3 = &bv;
     if (v3 && smem <= 200 * 1024) {
       Bb3Fn fn = v3->fn[xcompact ? 0 : 1];
-      if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-          cudaSuccess) {
+      if (smem_attr(h, (const void*)fn, smem) == cudaSuccess) {
         CbarFold cf{};
         if (folded && h->cpart_n > 0) {
           cf = CbarFold{h->cpart, h->cpart_n, k * k, h->C64, h->C32, nullptr, k, eta};
@@ -442,7 +468,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
   const int rt = v->rt;
   const size_t smem = ((size_t)2 * kBbWarps * rt * kBbSC + (size_t)2 * kBbSC * 32 * kc) * sizeof(float);
   BbFn fn = v->fn[gather ? (xcompact ? 0 : 1) : 2];
-  if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+  if (smem_attr(h, (const void*)fn, smem) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -486,11 +512,8 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
     a.kn = (k + 15) & ~15;
     const size_t smem = (size_t)2 * (kTcM + a.ep) * kTcK * 4 + (size_t)kTcChunk * (a.ep + h->kp) * 4;
     if (a.ep + a.kn <= 512 && smem <= 226 * 1024 && m % 4 == 0 &&
-        cudaFuncSetAttribute((const void*)k_contract_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-            cudaSuccess) {
-      int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)k_contract_tc, kCtThreads, smem) ==
-              cudaSuccess && occ >= 1) {
+        smem_attr(h, (const void*)k_contract_tc, smem) == cudaSuccess) {
+      if (occupancy(h, (const void*)k_contract_tc, kCtThreads, smem) >= 1) {
         somf_status s = ensure_partial(h, (size_t)h->nsm * k * (a.ep + a.kn));
         if (s) return s;
         a.idx = h->idx;
@@ -532,11 +555,10 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
       if (s) return s;
       const size_t smem = (size_t)seg * LDY * sizeof(float) + (size_t)seg * sizeof(int);
       Ct3Fn fn = v3->fn[xcompact ? 0 : 1];
-      CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      int occ = 0;
+      CK(smem_attr(h, (const void*)fn, smem));
       h->kern[0] = 2;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kCtThreads, smem) == cudaSuccess &&
-          occ >= 1) {
+      const int occ = occupancy(h, (const void*)fn, kCtThreads, smem);
+      if (occ >= 1) {
         // split-K reduction fused behind one grid barrier (cooperative launch)
         CtFuse fz{h->ct_bar, r, beta, G, h->err_dev};
         const int32_t* idxp = h->idx;
@@ -588,7 +610,7 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
     if (s) return s;
     const size_t smem = (size_t)kCtStages * kCtTK * (8 * mt + 32 * nt) * sizeof(float);
     CtFn fn = v->fn[gather ? (xcompact ? 0 : 1) : 2];
-    CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(smem_attr(h, (const void*)fn, smem));
     fn<<<dim3(ta, tc, ns), kCtThreads, smem, h->st>>>(h->idx, q_dev, h->D, h->kp, k, X, ldx, m, h->partial);
     CKL();
     const int64_t tot = (int64_t)k * nc;
@@ -659,7 +681,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
       case 4: fn = (const void*)k_ridge_codes<4>; break;
       default: fn = (const void*)k_ridge_codes<5>; break;
     }
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(smem_attr(h, fn, smem));
     double lam = c.lambda;
     long long* rprof = h->prof_on ? h->bcd_prof + 72 : nullptr;    // slots 72..75 (ridge phases)
     float* at = want_cpart ? h->AT32 : nullptr;
@@ -715,7 +737,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
     const int gas = (int)ceil_div(m, nw_as);
 #define LAUNCH_AS(N, GT)                                                                               \
   {                                                                                                    \
-    CK(cudaFuncSetAttribute(k_cd_as<N, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_as)); \
+    CK(smem_attr(h, (const void*)k_cd_as<N, GT>, smem_as));                                          \
     k_cd_as<N, GT><<<gas, tas, smem_as, h->st>>>(G, beta, k, m, l1, l2, c.pos_code, tol,              \
                                                  c.cd_max_sweeps, nmax, A64, A32, h->sweeps_dev,      \
                                                  want_cpart ? h->AT32 : nullptr, h->kp, gstride,      \
@@ -738,7 +760,7 @@ static somf_status launch_codes(somf_ctx* h, const double* G, const double* beta
   const size_t smem_cd = np * (g64cd ? sizeof(double) : sizeof(float));
 #define LAUNCH_CD(N, GT)                                                                      \
   {                                                                                           \
-    CK(cudaFuncSetAttribute(k_cd<N, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cd)); \
+    CK(smem_attr(h, (const void*)k_cd<N, GT>, smem_cd));                                   \
     k_cd<N, GT><<<gstride > 0 ? m : grid, gstride > 0 ? 32 : kSolveThreads, smem_cd, h->st>>>( \
         G, beta, k, m, l1, l2, c.pos_code, tol, c.cd_max_sweeps, A64, A32, h->sweeps_dev,     \
         want_cpart ? h->AT32 : nullptr, h->kp, gstride);                                     \
@@ -1068,7 +1090,7 @@ static somf_status bcd_sharded(somf_ctx* h) {
   CKL();
   const int rr = k <= 96 ? 128 : 64;
   const size_t smem = (size_t)2 * rr * (k + 1) * sizeof(float);
-  CK(cudaFuncSetAttribute(k_shard_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(smem_attr(h, (const void*)k_shard_round, smem));
   int64_t rounds = 0;
   const int max_rounds = 3 * k + 20;
   for (int r = 0; r < max_rounds; ++r) {
