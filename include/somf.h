@@ -320,8 +320,10 @@ somf_status somf_profile_read(somf_handle h, double* ms, int64_t* launches, int6
  * and of somf_transform / somf_objective: [beta | G] of X, SUM; the residual
  * column sums, m doubles, SUM.  The code solve, Cbar and the threshold
  * updates then run identically on every rank.  fn == NULL restores the
- * single-GPU path.  With a reducer, Alg. 4 runs as one kernel per round with
- * a host read of the convergence flag per round. */
+ * single-GPU path.  With a reducer, Alg. 4 runs as one kernel per round; the
+ * host reads the convergence flag once per 8 rounds (rounds after convergence
+ * are no-ops whose sums are zero, so every rank still makes the same calls):
+ * one or two host synchronisations per step at the configs' round counts. */
 typedef int32_t (*somf_reduce_fn)(void* user, void* buf, int64_t count, int32_t dtype, int32_t op,
                                   void* stream);
 enum { SOMF_DT_F64 = 0, SOMF_DT_I32 = 1 };

@@ -14,7 +14,8 @@
 //                    (count, S1, S2, min above, max below)               (rows)
 //       reducer(sums, SUM); reducer(min, MIN); reducer(max, MAX)
 //     k_shard_update the Michelot step of every atom, convergence flag    (1 CTA)
-//     host reads the flag
+//     host reads the flag every kShBatch rounds (rounds after convergence
+//     are no-ops): one host synchronisation per kShBatch rounds
 //   k_shard_finish   D_M rows back in atom order; slack norms, warm starts (rows)
 //
 // Every rank runs the identical update on identical reduced sums, so the
@@ -32,6 +33,7 @@ __device__ __forceinline__ void nt_red_add(double* p, double v) {
 }
 
 constexpr int kShMaxK = 256;
+constexpr int kShBatch = 8;     // rounds between two host reads of the convergence flag
 // "no element" for the min-above reduction: +inf bits (so the u32 MIN over
 // ranks is also a valid int32 MIN for the collectives, all values >= 0)
 constexpr unsigned kShNone = 0x7f800000u;
@@ -55,7 +57,7 @@ struct ShState {            // device arrays, pi order unless stated
   unsigned* mn;             // k (float bits, MIN over ranks)
   unsigned* mx;             // k (float bits, MAX over ranks)
   double* rho_acc;          // 2k
-  int* conv;                // 1
+  int* conv;                // 2: [0] converged (sticky within a step), [1] rounds run
 };
 
 __global__ void k_shard_init(ShState S, const int32_t* __restrict__ perm, const double* __restrict__ C64,
@@ -95,6 +97,7 @@ __global__ void k_shard_init(ShState S, const int32_t* __restrict__ perm, const 
     S.mn[e] = kShNone;
     S.mx[e] = 0u;
   }
+  if (tid == 0) S.conv[0] = S.conv[1] = 0;
 }
 
 // thread per masked row: D_M and R in pi order; radius partial sums
@@ -140,6 +143,9 @@ __global__ void k_shard_rho(ShState S, int k, double a, double b) {
 // one round of the recurrence: thread per row, R and v in shared memory
 // smem: blockDim x (k + 1) floats (R) + blockDim x (k + 1) floats (v)
 __global__ void k_shard_round(ShState S, const int64_t* __restrict__ q_dev, int k, double a) {
+  // the host checks convergence only every few rounds: rounds after it are
+  // no-ops (their sums stay zero; the update below skips them too)
+  if (*(volatile int*)S.conv) return;
   extern __shared__ float sh_smem[];
   const int LD = k + 1;
   float* R = sh_smem;                               // rows x LD
@@ -202,7 +208,8 @@ __global__ void k_shard_round(ShState S, const int64_t* __restrict__ q_dev, int 
 }
 
 // the Michelot step of every atom (identical on every rank); convergence flag
-__global__ void k_shard_update(ShState S, int k, double a, double b, int round) {
+__global__ void k_shard_update(ShState S, int k, double a, double b, int round, int sticky) {
+  if (sticky && *(volatile int*)S.conv) return;        // converged in an earlier round of this step
   int conv = 1;
   for (int p = threadIdx.x; p < k; p += blockDim.x) {
     const double cnt = S.acc[3 * p], S1 = S.acc[3 * p + 1], S2 = S.acc[3 * p + 2];
@@ -229,7 +236,10 @@ __global__ void k_shard_update(ShState S, int k, double a, double b, int round) 
     S.mx[p] = 0u;
   }
   conv = __syncthreads_and(conv);
-  if (threadIdx.x == 0) *S.conv = conv;
+  if (threadIdx.x == 0) {
+    S.conv[0] = conv;
+    S.conv[1] += 1;
+  }
 }
 
 // D_M rows back (the last round's d, atom order); n_j and warm starts

@@ -14,7 +14,8 @@
 //    slot compute their candidate update from the current gradient, a ballot
 //    finds the FIRST nonzero one in cyclic order, only that one is applied
 //    (broadcast + gradient update), and the lanes after it recompute;
-//  * after kAsWarm sweeps, every sweep is followed by a JUMP towards the
+//  * after kAsWarm sweeps, a sweep that left the support unchanged (or the
+//    kAsForce-th sweep without one) is followed by a JUMP towards the
 //    minimiser of the current orthant face: with S the support and s its signs,
 //    solve (G_SS + l2 I) y = beta_S - l1 s_S (warp Cholesky, fp64).  If every
 //    sign of y agrees, a_S <- y.  Otherwise move a_S along the segment towards
@@ -33,6 +34,8 @@
 namespace somf {
 
 constexpr int kAsWarm = 3;          // CD sweeps before the first jump
+constexpr int kAsForce = 4;         // sweeps without a jump after which one is tried anyway
+constexpr int kAsMaxLs = 3;         // face solves per jump (the line search's re-solves included)
 constexpr int kAsRowsPerLane = 4;   // face rows per lane in the factorisation (nmax <= 128)
 
 // per-warp scratch: packed lower face matrix, y, a_S, sidx, and a dense k-vector
@@ -95,6 +98,13 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
     long long c_sw = 0, c_jump = 0, n_solve = 0, n_sum = 0, n_agree = 0;
     int n_max = 0;
     long long t0 = prof ? clock64() : 0;
+    // support of the previous sweep (one ballot per slot): a jump is tried once
+    // the sweeps stop changing the support (the face solve then usually agrees
+    // in sign at once), or after kAsForce sweeps without one
+    unsigned smask[KPL];
+#pragma unroll
+    for (int i = 0; i < KPL; ++i) smask[i] = 0u;
+    int since_jump = 0;
     for (; sweep < max_sweeps; ++sweep) {
       // ---- one cyclic CD sweep; zero updates skipped by ballot ----
       double maxd = 0.0;
@@ -136,7 +146,16 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
       amax = warp_max(amax);
       if (prof) { const long long t1 = clock64(); c_sw += t1 - t0; t0 = t1; }
       if (maxd <= tol * fmax(1.0, amax)) { ++sweep; break; }
-      if (sweep + 1 < kAsWarm) continue;
+      bool stable = true;
+#pragma unroll
+      for (int slot = 0; slot < KPL; ++slot) {
+        const unsigned cm = __ballot_sync(0xffffffffu, alpha[slot] != 0.0);
+        stable &= cm == smask[slot];
+        smask[slot] = cm;
+      }
+      ++since_jump;
+      if (sweep + 1 < kAsWarm || (!stable && since_jump < kAsForce)) continue;
+      since_jump = 0;
       // ---- jump: exact solve on the current face, with line search ----
       int n = 0;
 #pragma unroll
@@ -152,6 +171,7 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
       if (n == 0 || n > nmax) continue;
       for (int j = lane; j < k; j += 32) anew[j] = 0.0;
       bool moved = false;
+      int nls = 0;
       __syncwarp();
       while (n > 0) {
         // A = G_SS + l2 I (packed lower), y = beta_S - l1 sign(a_S)
@@ -271,6 +291,9 @@ k_cd_as(const double* __restrict__ G, const double* __restrict__ beta, int k, in
           __syncwarp();
         }
         n = nn;
+        // line-search budget spent: keep the point reached (the objective
+        // only decreased along the way) and let the CD sweeps go on
+        if (++nls >= kAsMaxLs) break;
       }
       if (!moved) continue;
       // the jump's point (zeros off the final support) back into the registers

@@ -1032,8 +1032,8 @@ static somf_status shard_alloc(somf_ctx* h) {
   CK(dalloc(&S.mn, (size_t)k));
   CK(dalloc(&S.mx, (size_t)k));
   CK(dalloc(&S.rho_acc, (size_t)2 * k));
-  CK(dalloc(&S.conv, 1));
-  CK(cudaMallocHost((void**)&h->sh_conv_host, sizeof(int)));
+  CK(dalloc(&S.conv, 2));
+  CK(cudaMallocHost((void**)&h->sh_conv_host, 2 * sizeof(int)));
   h->sh_alloc = true;
   return SOMF_OK;
 }
@@ -1055,7 +1055,7 @@ static somf_status project_sharded(somf_ctx* h) {
     if (somf_status s = reduce(h, S.acc, 3 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
     if (somf_status s = reduce(h, S.mn, k, SOMF_DT_I32, SOMF_OP_MIN)) return s;
     if (somf_status s = reduce(h, S.mx, k, SOMF_DT_I32, SOMF_OP_MAX)) return s;
-    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b, it);
+    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b, it, 0);
     CKL();
     CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, sizeof(int), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
@@ -1091,28 +1091,33 @@ static somf_status bcd_sharded(somf_ctx* h) {
   const int rr = k <= 96 ? 128 : 64;
   const size_t smem = (size_t)2 * rr * (k + 1) * sizeof(float);
   CK(smem_attr(h, (const void*)k_shard_round, smem));
-  int64_t rounds = 0;
-  const int max_rounds = 3 * k + 20;
+  int64_t launched = 0;
+  const int max_rounds = 8 * k + 40;
+  h->sh_conv_host[0] = h->sh_conv_host[1] = 0;
   for (int r = 0; r < max_rounds; ++r) {
     k_shard_round<<<(unsigned)ceil_div(qc, rr), rr, smem, h->st>>>(S, h->q_dev, k, a);
     CKL();
     if (somf_status s = reduce(h, S.acc, 3 * k, SOMF_DT_F64, SOMF_OP_SUM)) return s;
     if (somf_status s = reduce(h, S.mn, k, SOMF_DT_I32, SOMF_OP_MIN)) return s;
     if (somf_status s = reduce(h, S.mx, k, SOMF_DT_I32, SOMF_OP_MAX)) return s;
-    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b, r);
+    k_shard_update<<<1, 256, 0, h->st>>>(S, k, a, b, r, 1);
     CKL();
-    CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, sizeof(int), cudaMemcpyDeviceToHost, h->st));
-    CK(cudaStreamSynchronize(h->st));
-    ++rounds;
-    if (*h->sh_conv_host) break;
+    ++launched;
+    if ((r + 1) % kShBatch == 0 || r + 1 == max_rounds) {
+      // one host synchronisation per kShBatch rounds
+      CK(cudaMemcpyAsync(h->sh_conv_host, S.conv, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->st));
+      CK(cudaStreamSynchronize(h->st));
+      if (h->sh_conv_host[0]) break;
+    }
   }
-  const bool capped = !*h->sh_conv_host;
+  const bool capped = !h->sh_conv_host[0];
+  const int64_t rounds = h->sh_conv_host[1];
   k_shard_finish<<<(unsigned)ceil_div(qc, rb), rb, 0, h->st>>>(S, h->idx, h->q_dev, h->D, k, h->kp, a, b,
                                                                h->nslack, h->lam_ws);
   CKL();
   k_set_scalar_i64<<<1, 1, 0, h->st>>>(h->nred_dev, rounds + 1);
   CKL();
-  h->launches[SOMF_PH_BCD] += 4 + 2 * rounds;
+  h->launches[SOMF_PH_BCD] += 4 + 2 * launched;
   if (capped) {
     set_err(h, "projection threshold rounds hit their cap (%d)", max_rounds);
     return SOMF_E_CUDA;

@@ -113,7 +113,11 @@ def test_two_shards_match_single_gpu_and_oracle(k, eta, mu, r):
     # replicated state identical on both ranks (same reduced sums, same updates)
     np.testing.assert_array_equal(st[0]["Cbar"], st[1]["Cbar"])
     np.testing.assert_array_equal(st[0]["n"], st[1]["n"])
-    assert rel(D, s1["D"]) < 1e-5 and rel(B, s1["Bbar"]) < 1e-5
+    # sharded rounds vs the single-GPU kernel: two implementations of the same
+    # threshold iteration, each stopping once every lambda_j is stable to 1e-5
+    # relative (R22: converged atoms keep their lambda), so D agrees to a few
+    # times that over the steps, not bit for bit
+    assert rel(D, s1["D"]) < 5e-5 and rel(B, s1["Bbar"]) < 5e-5
     assert rel(D, ora.D) < 1e-4 and rel(B, ora.Bbar) < 1e-4 and rel(st[0]["Cbar"], ora.Cbar) < 1e-4
     np.testing.assert_allclose(st[0]["n"], ora.n, rtol=0, atol=1e-5)
     f_ref = ora.objective(Xte)
