@@ -2,15 +2,18 @@
 //
 // One SOMF iteration (Alg. 3 + Alg. 4 of arXiv 1701.05363) is the launch
 // sequence below, all on the caller's stream, with no host synchronisation
-// (dynamic sizes such as q = |S_t| stay on the device):
-//   k_step_begin      t <- t+1, w_t = t^-u
-//   k_mask_count/k_mask_scatter  S_t = rows with M_t = r   (Eq. mt)
-//   k_atom_perm       Alg. 4 atom order
-//   k_contract(+reduce) beta = r D_M^T X_M, G = r D_M^T D_M (Eq. a)
-//   k_ridge_chol | k_cd  codes                              (Eq. somf_alpha)
-//   k_cbar_update     Cbar                                   (Eq. somf_partial)
-//   k_bbar_update     P_t Bbar (and P_t^perp Bbar, mode F)
-//   k_bcd_seq         Alg. 4 on S_t (cooperative)
+// (dynamic sizes such as q = |S_t| stay on the device).  Steady state at
+// cfgC: four launches, the mask / t / coefficients / atom order of step t
+// having been drawn by step t-1's BCD kernel (or, first step, by
+// k_step_mask_count + k_mask_scatter: Eq. mt):
+//   k_contract_tc     [beta | G] = r D_M^T [X_M | D_M]        (Eq. a)
+//   k_ridge_codes | k_cd_as | k_cd   codes                    (Eq. somf_alpha)
+//   k_bbar_tc         P_t Bbar (+ P_t^perp Bbar, mode F) and Cbar, as a
+//                     programmatic dependent of the code solver
+//   k_bcd_newton | k_bcd_big | k_bcd_onchip | k_bcd_seq      Alg. 4 on S_t
+//                     (cooperative; draws M_{t+1} ahead)
+// (FFMA fallbacks of each step, the row-sharded rounds and the estimator (b)
+// / (c) kernels are selected by shape and configuration below.)
 #include <cuda_runtime.h>
 
 #include <algorithm>
