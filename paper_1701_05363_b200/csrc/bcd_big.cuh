@@ -281,7 +281,7 @@ __device__ __forceinline__ void nb_blk_pass(float* R, const float* Dold, float* 
 }
 
 // shared-memory layout (floats unless noted), host mirror in somf_capi.cu
-//   NbRec mode:   Dold, Rini, V   3 x (TR + 1) x (KPT + 1); cbuf 2 x CHB or KPT x T x CSTR
+//   NbRec mode:   Dold, Rini, V   3 x (TR + 1) x (KPT + 4); cbuf 2 x CHB or KPT x T x CSTR
 //   blocked mode: Dold, R, V      3 x (TR + 1) x (KPT + 4); cbuf 2 x 16 x KPT; Dl (TR + 1) x 16
 //   part          max(5 H KPT, 12 k) words (stats partials / record read)
 //   rows_s        TR ints; mbits: one byte per Philox block of my slice
@@ -293,35 +293,54 @@ __host__ __device__ constexpr size_t nb_cbuf_floats(int ch, bool blk) {
 
 // One recurrence pass over tile tl: loads it from the scratch when streamed,
 // leaves v in V; returns the tile's row count.
+// Streamed tiles of the unrolled mode (!kBlk) are double buffered through
+// the registers: a tile's d_old / R0 rows are cp.async'd into Dold / Rini
+// while the PREVIOUS tile's recurrence runs (its rows already sit in
+// registers), so the scratch read overlaps the arithmetic.  nb_prefetch
+// issues tile tl's copy; the pass waits for it, loads its registers and
+// issues tile (tl + 1) % ntile's.  (Blocked mode updates R in shared memory
+// during the pass: its loads stay synchronous.)
+template <int KPT>
+__device__ __forceinline__ void nb_prefetch(const float* __restrict__ scr, int tl, int TR, int nr_all, int64_t lo,
+                                            float* Dold, float* Rini, int tid, int nthr) {
+  constexpr int LD = KPT + 4;
+  constexpr int q4 = KPT / 4;
+  const int r0 = tl * TR, nr = min(TR, nr_all - r0);
+  const float* sc = scr + (size_t)(lo + r0) * 2 * KPT;
+  for (int e = tid; e < nr * 2 * q4; e += nthr) {
+    const int row = e / (2 * q4), c = e % (2 * q4);
+    float* dst = c < q4 ? Dold + (size_t)row * LD + 4 * c : Rini + (size_t)row * LD + 4 * (c - q4);
+    nb_cp16(dst, sc + (size_t)row * 2 * KPT + 4 * c);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int KPT, int T, int M, bool kGen, int CH, bool kBlk>
 __device__ __forceinline__ int nb_tile_pass(const float* __restrict__ scr, const float* __restrict__ Cpi,
                                             const float* __restrict__ Ctg, int tl, int TR, int nr_all, int64_t lo,
                                             bool streamed, float* Dold, float* Rini, float* V, float* cbuf, float* Dl,
-                                            const NtPar<kGen>* par, int g, int tq, int ngroups, int tid, int nthr) {
-  constexpr int LD = kBlk ? KPT + 4 : KPT + 1;
+                                            const NtPar<kGen>* par, int g, int tq, int ngroups, int tid, int nthr,
+                                            long long* ld_cyc = nullptr) {
+  constexpr int LD = KPT + 4;
+  const long long t_ld = ld_cyc ? clock64() : 0;
   constexpr int KT = KPT / T;
   constexpr int CSTR = nb_cstr(KPT, T);
   const int r0 = tl * TR, nr = min(TR, nr_all - r0);
-  if (streamed) {
+  if (streamed && kBlk) {
     __syncthreads();                               // V / Dold / Rini of the previous tile consumed
     const float* sc = scr + (size_t)(lo + r0) * 2 * KPT;
     constexpr int q4 = KPT / 4;
     for (int e = tid; e < nr * 2 * q4; e += nthr) {
       const int row = e / (2 * q4), c = e % (2 * q4);
       float* dst = c < q4 ? Dold + (size_t)row * LD + 4 * c : Rini + (size_t)row * LD + 4 * (c - q4);
-      const float4 v4 = __ldcg(reinterpret_cast<const float4*>(sc + (size_t)row * 2 * KPT + 4 * c));
-      if constexpr (kBlk) {
-        *reinterpret_cast<float4*>(dst) = v4;
-      } else {
-        dst[0] = v4.x;
-        dst[1] = v4.y;
-        dst[2] = v4.z;
-        dst[3] = v4.w;
-      }
+      *reinterpret_cast<float4*>(dst) = __ldcg(reinterpret_cast<const float4*>(sc + (size_t)row * 2 * KPT + 4 * c));
     }
+  } else if (streamed) {
+    asm volatile("cp.async.wait_all;" ::: "memory");   // this tile's prefetch
   }
   if constexpr (kBlk) {
     __syncthreads();
+    if (ld_cyc) *ld_cyc += clock64() - t_ld;
     nb_blk_pass<KPT, kGen>(Rini, Dold, V, Dl, cbuf, Cpi, par, nr, tid, nthr);
     return nr;
   } else {
@@ -332,6 +351,7 @@ __device__ __forceinline__ int nb_tile_pass(const float* __restrict__ scr, const
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     __syncthreads();
+    if (ld_cyc) *ld_cyc += clock64() - t_ld;
     int rowx[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) rowx[m] = (g < ngroups && g * M + m < nr) ? g * M + m : TR;
@@ -344,6 +364,12 @@ __device__ __forceinline__ int nb_tile_pass(const float* __restrict__ scr, const
         Do[m][i] = Dold[(size_t)rowx[m] * LD + i * T + tq];
         R[m][i] = Rini[(size_t)rowx[m] * LD + i * T + tq];
       }
+    if (streamed) {
+      // every thread holds its rows: the next tile's rows may overwrite Dold / Rini
+      __syncthreads();
+      const int ntile = (nr_all + TR - 1) / TR;
+      nb_prefetch<KPT>(scr, tl + 1 < ntile ? tl + 1 : 0, TR, nr_all, lo, Dold, Rini, tid, nthr);
+    }
     // threads past the groups: same code on the spare row (their v goes to the spare row)
     constexpr int H1 = KPT > 128 ? 128 : KPT;
     NbRec<KPT, T, M, kGen, CH, 0, H1>::run(R, Do, tq, V + (size_t)rowx[0] * LD, vstride * LD, cbuf, Ctg, par);
@@ -357,7 +383,7 @@ __device__ __forceinline__ int nb_tile_pass(const float* __restrict__ scr, const
 template <int KPT, int T, int M, bool kGen, int CH, bool kBlk>
 __global__ void __launch_bounds__(kNbThreads, 1)
 k_bcd_big(NtArgs P, NbArgs A) {
-  constexpr int LD = kBlk ? KPT + 4 : KPT + 1;
+  constexpr int LD = KPT + 4;                       // 16-byte rows (cp.async of streamed tiles)
   constexpr int KT = KPT / T;
   constexpr int CSTR = nb_cstr(KPT, T);
   static_assert(KPT % T == 0 && M == 2, "groups of T lanes x 2 rows");
@@ -371,6 +397,19 @@ k_bcd_big(NtArgs P, NbArgs A) {
   __shared__ int mode_s[KPT], jmap_s[KPT], pinv_s[KPT];
   __shared__ int mcnt_s;
   __shared__ int lockF_s, firstU_s, prevF_s;   // locked prefix (R22), first unconverged position
+  // phase clock of CTA 0 (slots as k_bcd_newton's 0..7; 8 = streamed tile loads, part of 1)
+  __shared__ long long nbp_s[9];
+  long long t_mark = clock64();
+  long long* const ldp = (P.prof && blockIdx.x == 0 && threadIdx.x == 0) ? &nbp_s[8] : nullptr;
+#define NB_MARK(slot)                                                              \
+  do {                                                                             \
+    if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {                           \
+      const long long now_ = clock64();                                            \
+      nbp_s[slot] += now_ - t_mark;                                                \
+      t_mark = now_;                                                               \
+    }                                                                              \
+  } while (0)
+  if (P.prof && blockIdx.x == 0 && threadIdx.x < 9) nbp_s[threadIdx.x] = 0;
   const int k = P.k, kp = P.kp;
   const int nthr = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -597,6 +636,9 @@ k_bcd_big(NtArgs P, NbArgs A) {
     nt_barrier(P.bar, nbar * G);
   }
 #pragma unroll 1
+  __syncthreads();
+  if (!kBlk && streamed && ntile > 0) nb_prefetch<KPT>(A.scr, 0, TR, nr_all, lo, Dold, Rini, tid, nthr);
+  NB_MARK(0);
   while (!done) {
     const int ring = round % kNtRing;
     for (int p = tid; p < k; p += nthr) {
@@ -607,7 +649,8 @@ k_bcd_big(NtArgs P, NbArgs A) {
     }
     for (int tl = 0; tl < ntile; ++tl) {
       const int nr = nb_tile_pass<KPT, T, M, kGen, CH, kBlk>(A.scr, A.Cpi, A.Ctg, tl, TR, nr_all, lo, streamed, Dold, Rini, V, cbuf,
-                                                            Dl, par_s[cur], g, tq, ngroups, tid, nthr);
+                                                            Dl, par_s[cur], g, tq, ngroups, tid, nthr, ldp);
+      NB_MARK(1);
       // per-atom statistics of the tile, added to the CTA sums in tile order
       if (tid < H * k) {
         const int p = tid % k, h = tid / k;
@@ -649,6 +692,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
         acc2_s[p] += S2;
       }
       __syncthreads();
+      NB_MARK(2);
     }
     if (nr_all > 0 && tid < k) {
       const int p = tid;
@@ -664,6 +708,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
     }
     ++nbar;
     nt_barrier(P.bar, nbar * G);
+    NB_MARK(3);
     {
       const int rz = (round + 2) % kNtRing;          // (see k_bcd_newton)
       for (int e = blockIdx.x + G * tid; e < P.ncopy * k; e += G * nthr)
@@ -766,6 +811,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
     }
     if (!done) cur ^= 1;
     __syncthreads();
+    NB_MARK(4);
   }
   // ---- final D: v of the final round through its parameters (several tiles: one
   // more pass per tile with the final parameters) ----
@@ -790,6 +836,8 @@ k_bcd_big(NtArgs P, NbArgs A) {
       __syncthreads();
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");      // (the last pass prefetched tile 0 again)
+  NB_MARK(5);
   // ---- draw-ahead of t+1: scatter of my slice of M_{t+1}, t+1, w_{t+1} ----
   if (P.idx_next) {
     if (wid == 0) {
@@ -820,6 +868,13 @@ k_bcd_big(NtArgs P, NbArgs A) {
   }
   // ---- exit: last CTA resets counters and accumulators ----
   __syncthreads();
+  NB_MARK(6);
+  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    nbp_s[7] = 1;
+    for (int i = 0; i < 8; ++i) P.prof[i] += nbp_s[i];
+    P.prof[82] += nbp_s[8];
+  }
+#undef NB_MARK
   if (tid == 0) {
     __threadfence();
     const unsigned old = atomicAdd(P.bar + 1, 1u);

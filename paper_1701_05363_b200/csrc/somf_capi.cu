@@ -69,6 +69,25 @@ k_gather_rows(const int32_t* __restrict__ idx, const int64_t* __restrict__ q_dev
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const bool vec = (eta & 3) == 0 && (ldx & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Xm)) & 15) == 0;
+  if (vec) {
+    // 16-byte requests (fewer, larger reads over the host link), all of a row in flight
+    const int e4 = eta >> 2;
+    for (int64_t m = warp; m < q; m += nwarps) {
+      const float4* src = reinterpret_cast<const float4*>(X + (int64_t)idx[m] * ldx);
+      float4* dst = reinterpret_cast<float4*>(Xm + m * eta);
+      float4 v[4];
+      for (int s0 = 0; s0 < e4; s0 += 128) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + 32 * u + lane < e4) v[u] = src[s0 + 32 * u + lane];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (s0 + 32 * u + lane < e4) dst[s0 + 32 * u + lane] = v[u];
+      }
+    }
+    return;
+  }
   for (int64_t m = warp; m < q; m += nwarps) {
     const float* src = X + (int64_t)idx[m] * ldx;
     float* dst = Xm + m * eta;
@@ -917,7 +936,7 @@ static bool choose_big(somf_ctx* h) {
     const void* fn = v.get(gen, &T, &ch, &blk);
     cudaFuncAttributes fa{};
     if (!fn || cudaFuncGetAttributes(&fa, fn) != cudaSuccess) { cudaGetLastError(); return false; }
-    const int kpt = v.kpt, LD = blk ? kpt + 4 : kpt + 1;
+    const int kpt = v.kpt, LD = kpt + 4;          // 16-byte rows (bcd_big.cuh)
     const size_t cstr = (size_t)nb_cstr(kpt, T);
     const size_t cbf = blk ? (size_t)2 * kNbCB * kpt
                            : ch >= kpt ? (size_t)kpt * T * cstr : (size_t)2 * ch * T * cstr;
