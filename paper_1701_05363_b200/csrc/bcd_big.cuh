@@ -328,13 +328,8 @@ __device__ __forceinline__ int nb_tile_pass(const float* __restrict__ scr, const
   const int r0 = tl * TR, nr = min(TR, nr_all - r0);
   if (streamed && kBlk) {
     __syncthreads();                               // V / Dold / Rini of the previous tile consumed
-    const float* sc = scr + (size_t)(lo + r0) * 2 * KPT;
-    constexpr int q4 = KPT / 4;
-    for (int e = tid; e < nr * 2 * q4; e += nthr) {
-      const int row = e / (2 * q4), c = e % (2 * q4);
-      float* dst = c < q4 ? Dold + (size_t)row * LD + 4 * c : Rini + (size_t)row * LD + 4 * (c - q4);
-      *reinterpret_cast<float4*>(dst) = __ldcg(reinterpret_cast<const float4*>(sc + (size_t)row * 2 * KPT + 4 * c));
-    }
+    nb_prefetch<KPT>(scr, tl, TR, nr_all, lo, Dold, Rini, tid, nthr);   // every row in flight at once
+    asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (streamed) {
     asm volatile("cp.async.wait_all;" ::: "memory");   // this tile's prefetch
   }
@@ -397,8 +392,9 @@ k_bcd_big(NtArgs P, NbArgs A) {
   __shared__ int mode_s[KPT], jmap_s[KPT], pinv_s[KPT];
   __shared__ int mcnt_s;
   __shared__ int lockF_s, firstU_s, prevF_s;   // locked prefix (R22), first unconverged position
-  // phase clock of CTA 0 (slots as k_bcd_newton's 0..7; 8 = streamed tile loads, part of 1)
-  __shared__ long long nbp_s[9];
+  // phase clock of CTA 0 (slots as k_bcd_newton's 0..7; 8 = streamed tile loads, part of 1;
+  // 9..12 = setup: staging, pi-order permutes, R0, radii + scratch write, part of 0)
+  __shared__ long long nbp_s[13];
   long long t_mark = clock64();
   long long* const ldp = (P.prof && blockIdx.x == 0 && threadIdx.x == 0) ? &nbp_s[8] : nullptr;
 #define NB_MARK(slot)                                                              \
@@ -409,7 +405,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
       t_mark = now_;                                                               \
     }                                                                              \
   } while (0)
-  if (P.prof && blockIdx.x == 0 && threadIdx.x < 9) nbp_s[threadIdx.x] = 0;
+  if (P.prof && blockIdx.x == 0 && threadIdx.x < 13) nbp_s[threadIdx.x] = 0;
   const int k = P.k, kp = P.kp;
   const int nthr = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -516,6 +512,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncthreads();
     }
+    NB_MARK(9);
     // d_old in pi order
     for (int e = tid; e < nr * KPT; e += nthr) {
       const int row = e / KPT, p = e % KPT;
@@ -529,6 +526,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
       V[(size_t)row * LD + p] = kBlk ? bb * A.invc[p] : bb;
     }
     __syncthreads();
+    NB_MARK(10);
     if constexpr (kBlk) {
       // R0 = Bbar / c - Dold Cpre: rank-16 updates over every chunk of positions
       for (int e = tid; e < nr * LD; e += nthr) Rini[e] = V[e];
@@ -543,35 +541,49 @@ k_bcd_big(NtArgs P, NbArgs A) {
       }
       __syncthreads();
     } else {
-      // R0 = (Bbar - Dold Cpi) * invc : RT rows x 8 positions per item
-      constexpr int RT = 4;
-      const int nrb = (nr + RT - 1) / RT, npb = (k + 7) / 8;
-      for (int it = tid; it < nrb * npb; it += nthr) {
-        const int rb = (it / npb) * RT, p0 = (it % npb) * 8;
-        float acc[RT][8];
+      // R0[l] = Bbar[l] / c_ll - sum_p Dold[p] C[p][l] / c_ll from the resident
+      // prescaled Cbar (cbuf, parity layout: (p, l = i T + t) at
+      // p T CSTR + t CSTR + i; staged at the start, landed with the first
+      // tile's rows).  Item = RT rows x 4 positions (one parity t, i0..i0+3),
+      // 4 p per step: 4 + RT 16-byte shared loads per 16 RT FMAs.  (The
+      // global-memory Cpi version was bound by L2 loads: L1 is ~30 KB next to
+      // this kernel's shared memory; 187 us of setup per step at cfgC r=1.)
+      constexpr int RT = 16, NIB = nb_kts(KPT, T) / 4;
+      const int nrb = (nr + RT - 1) / RT;
+      for (int it = tid; it < nrb * T * NIB; it += nthr) {
+        const int ib = it % NIB, t = (it / NIB) % T, rb = (it / (NIB * T)) * RT;
+        float acc[RT][4];
 #pragma unroll
         for (int i = 0; i < RT; ++i)
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
-        for (int l = 0; l < k; ++l) {
-          const float4 c0 = __ldg(reinterpret_cast<const float4*>(A.Cpi + (size_t)l * KPT + p0));
-          const float4 c1 = __ldg(reinterpret_cast<const float4*>(A.Cpi + (size_t)l * KPT + p0 + 4));
-          const float cv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+        const float* cb = cbuf + (size_t)t * CSTR + 4 * ib;
+        for (int p = 0; p < k; p += 4) {               // Dold and Cbar are zero past k (KPT % 4 == 0)
+          float cv[4][4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 c4 = *reinterpret_cast<const float4*>(cb + (size_t)(p + j) * T * CSTR);
+            cv[j][0] = c4.x; cv[j][1] = c4.y; cv[j][2] = c4.z; cv[j][3] = c4.w;
+          }
 #pragma unroll
           for (int i = 0; i < RT; ++i) {
-            const float d = Dold[(size_t)min(rb + i, TR) * LD + l];
+            const float4 d = *reinterpret_cast<const float4*>(Dold + (size_t)min(rb + i, TR) * LD + p);
+            const float dv[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-            for (int c = 0; c < 8; ++c) acc[i][c] = fmaf(d, cv[c], acc[i][c]);
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc[i][c] = fmaf(dv[j], cv[j][c], acc[i][c]);
           }
         }
 #pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const int row = rb + i;
-          if (row >= nr) continue;
+        for (int c = 0; c < 4; ++c) {
+          const int l = (4 * ib + c) * T + t;
+          if (4 * ib + c >= KPT / T || l >= k) continue;
+          const float iv = A.invc[l];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int p = p0 + c;
-            if (p < k) Rini[(size_t)row * LD + p] = (V[(size_t)row * LD + p] - acc[i][c]) * A.invc[p];
+          for (int i = 0; i < RT; ++i) {
+            const int row = rb + i;
+            if (row < nr) Rini[(size_t)row * LD + l] = V[(size_t)row * LD + l] * iv - acc[i][c];
           }
         }
       }
@@ -581,6 +593,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
       const int p = e % LD;
       if (p >= k) Rini[e] = 0.f;
     }
+    NB_MARK(11);
     // radii sums of this tile (fp64, fixed order: tile by tile)
     {
       const int nwarp = nthr >> 5;
@@ -610,6 +623,7 @@ k_bcd_big(NtArgs P, NbArgs A) {
       }
       __syncthreads();
     }
+    NB_MARK(12);
   }
   if (nr_all > 0 && tid < k) {
     unsigned long long* rr = P.rec + (((size_t)kNtRing * P.ncopy + blockIdx.x % P.ncopy) * k + tid) * kNtRec;
@@ -873,6 +887,10 @@ k_bcd_big(NtArgs P, NbArgs A) {
     nbp_s[7] = 1;
     for (int i = 0; i < 8; ++i) P.prof[i] += nbp_s[i];
     P.prof[82] += nbp_s[8];
+    P.prof[83] += nbp_s[9];
+    P.prof[93] += nbp_s[10];
+    P.prof[94] += nbp_s[11];
+    P.prof[95] += nbp_s[12];
   }
 #undef NB_MARK
   if (tid == 0) {

@@ -70,7 +70,10 @@ def main():
                setup_us={ph: round(v / n / mhz, 2) for ph, v in cyc["setup_split"].items()},
                ridge_us={ph: round(v / n / mhz, 2) for ph, v in cyc["ridge"].items() if isinstance(v, int)},
                unconverged=[round(u / n, 1) for u in cyc["unconverged_per_round"] if u],
-               cd=cyc["cd"])
+               cd=cyc["cd"],
+               big_us={nm: round(cyc["raw"][i] / n / mhz, 2) for nm, i in
+                       (("tile_load", 82), ("setup_stage", 83), ("setup_permute", 93), ("setup_r0", 94),
+                        ("setup_radii_scratch", 95))})
     print(json.dumps(out))
 
 
