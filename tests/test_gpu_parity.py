@@ -8,6 +8,9 @@ Bars (BASELINE.json north_star):
     (float32 inputs, float64 threshold arithmetic).
 The oracle always starts from the same float32-rounded state the GPU holds.
 """
+import copy
+import functools
+
 import numpy as np
 import pytest
 
@@ -120,12 +123,11 @@ def _data(kind, p, n, seed=0):
     return f32(X)
 
 
-def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
+@functools.lru_cache(maxsize=None)
+def _burned_in(name, t0, seed):
+    """The oracle after t0 steps (computed once per case; every BCD-kernel
+    variant of the case starts from a deep copy of it)."""
     p, k, eta, kw, kind = CASES[name]
-    gkw = {}
-    if bcd_kernel == "big_streamed":
-        # the k <= 256 kernel with 4-row tiles: every CTA streams its rows
-        bcd_kernel, gkw = "big", dict(bcd_tile_rows=4)
     X = _data(kind, p, k + (t0 + 3) * eta)
     ora = SomfOracle(OracleConfig(p=p, k=k, eta=eta, seed=seed, **kw))
     ora.set_components(X[:, :k])
@@ -133,6 +135,17 @@ def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
         ora.partial_fit(X[:, k + t * eta:k + (t + 1) * eta])
     # the oracle continues from the float32-rounded state the GPU holds
     ora.D, ora.Bbar = f32(ora.D), f32(ora.Bbar)
+    return ora, X
+
+
+def _pair(somf, name, t0=5, seed=3, bcd_kernel="auto"):
+    p, k, eta, kw, kind = CASES[name]
+    gkw = {}
+    if bcd_kernel == "big_streamed":
+        # the k <= 256 kernel with 4-row tiles: every CTA streams its rows
+        bcd_kernel, gkw = "big", dict(bcd_tile_rows=4)
+    ora, X = _burned_in(name, t0, seed)
+    ora = copy.deepcopy(ora)
     gpu = somf.Somf(p, k, eta, seed=seed, debug=True, bcd_kernel=bcd_kernel, **kw, **gkw)
     gpu.set_state(ora.D, ora.Bbar, ora.Cbar, ora.n, ora.t)
     return ora, gpu, X, (p, k, eta)
