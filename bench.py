@@ -558,9 +558,13 @@ def run_somf(args):
         mhz = (clk or {}).get("sm_mhz") or peaks["sm_max_mhz"]
         roof["bcd_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc.items()
                                          if isinstance(v, int) and ph not in ("launches", "unconverged_per_round", "frozen_prefix_per_round", "ridge",
-                                                       "setup_split", "update_split")}
+                                                       "setup_split", "update_split", "contract", "bbar")}
         roof["bcd_update_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["update_split"].items()}
         roof["ridge_phase_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["ridge"].items()}
+        for ph in ("contract", "bbar"):
+            n = bcd_cyc[ph].pop("launches")
+            if n:
+                roof[ph + "_phase_us_per_step"] = {x: v / n / mhz for x, v in bcd_cyc[ph].items()}
         roof["bcd_setup_us_per_step"] = {ph: v / bcd_cyc["launches"] / mhz for ph, v in bcd_cyc["setup_split"].items()}
         unc = [u / bcd_cyc["launches"] for u in bcd_cyc["unconverged_per_round"]]
         while unc and unc[-1] == 0:

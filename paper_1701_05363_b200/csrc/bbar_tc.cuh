@@ -40,6 +40,7 @@ struct BtArgs {
   int ep;                   // eta rounded up to 16
   CbarFold cf;
   int pdl;                  // launched as a programmatic dependent of the code solver
+  long long* prof;          // optional: SM cycles per phase of CTA 0 (8 slots, somf_bcd_phase_cycles [232..239])
 };
 
 __device__ __forceinline__ void bt_split(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
@@ -88,6 +89,17 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
   __shared__ __align__(8) uint64_t mbar;
   __shared__ int grow[kBtM];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // phase clock of CTA 0, thread 0 (diagnostics; accumulated in registers, flushed once)
+  const bool clk_on = P.prof && blockIdx.x == 0 && tid == 0;
+  long long t_mark = clock64(), t_ph[7] = {0, 0, 0, 0, 0, 0, 0};
+#define BT_MARK(slot)                   \
+  do {                                  \
+    if (clk_on) {                       \
+      const long long now_ = clock64(); \
+      t_ph[slot] += now_ - t_mark;      \
+      t_mark = now_;                    \
+    }                                   \
+  } while (0)
   const int eta = P.eta, k = P.k, kp = P.kp, np = P.np, ep = P.ep, nch = ep / 8;
   const int G = gridDim.x;
   const int64_t q = *P.q_dev;
@@ -103,30 +115,50 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
   // Everything the code solver writes (the codes A, the Cbar partials) is read
   // only after griddepcontrol.wait: with programmatic dependent launch the CTAs
   // start while the solver still runs and stage their first tile of X rows and
-  // old Bbar rows (written by earlier kernels) in the meantime.
-  auto after_solver = [&]() {
+  // old Bbar rows (written by earlier kernels) in the meantime.  The Cbar
+  // update runs AFTER the first tile's MMAs are issued (under the tensor pipe
+  // and the old-Bbar cp.async), off the path wait -> codes -> MMA -> epilogue.
+  auto wait_solver = [&]() {
     if (P.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+  };
+  auto fold_cbar = [&]() {
     if (P.cf.A64) {
       // my slice of the Cbar entries (Eq. somf_partial) straight from the
       // fp64 codes: sum_s a_s a_s^T, s in column order, 8 threads per entry
-      // (strided columns) combined in fixed order
-      const int e0 = (int)((int64_t)P.cf.kk * blockIdx.x / G), e1 = (int)((int64_t)P.cf.kk * (blockIdx.x + 1) / G);
+      // (strided columns) combined in fixed order.  Only the lower triangle
+      // (a >= b) is summed; entry (b, a) gets the same bits (the products
+      // commute), so Cbar stays exactly symmetric and a CTA's slice
+      // (k (k + 1) / 2 / G entries: 17 at cfgC) is one pass of 32 entries.
       const int kq = P.cf.k, ne = P.cf.eta;
+      const int ntri = kq * (kq + 1) / 2;
+      const int e0 = (int)((int64_t)ntri * blockIdx.x / G), e1 = (int)((int64_t)ntri * (blockIdx.x + 1) / G);
       for (int eb = e0; eb < e1; eb += kBtThreads / 8) {
         const int e = eb + tid / 8, h = tid % 8;
         double s = 0.0;
+        int ia = 0, ib = 0;
         if (e < e1) {
-          const double* ra = P.cf.A64 + (int64_t)(e / kq) * ne;
-          const double* rb = P.cf.A64 + (int64_t)(e % kq) * ne;
+          // e = ia (ia + 1) / 2 + ib, ib <= ia
+          ia = (int)((sqrtf(8.f * (float)e + 1.f) - 1.f) * 0.5f);
+          while (ia * (ia + 1) / 2 > e) --ia;
+          while ((ia + 1) * (ia + 2) / 2 <= e) ++ia;
+          ib = e - ia * (ia + 1) / 2;
+          const double* ra = P.cf.A64 + (int64_t)ia * ne;
+          const double* rb = P.cf.A64 + (int64_t)ib * ne;
+#pragma unroll 8
           for (int c = h; c < ne; c += 8) s = fma(__ldg(ra + c), __ldg(rb + c), s);
         }
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
         s += __shfl_xor_sync(0xffffffffu, s, 4);
         if (e < e1 && h == 0) {
-          const double c = keepd * P.cf.C64[e] + (gc / eta) * s;
-          P.cf.C64[e] = c;
-          P.cf.C32[e] = (float)c;
+          const int eab = ia * kq + ib, eba = ib * kq + ia;
+          const double c = keepd * P.cf.C64[eab] + (gc / eta) * s;
+          P.cf.C64[eab] = c;
+          P.cf.C32[eab] = (float)c;
+          if (ia != ib) {
+            P.cf.C64[eba] = c;
+            P.cf.C32[eba] = (float)c;
+          }
         }
       }
     } else if (P.cf.cpart) {
@@ -142,12 +174,13 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
     }
   };
   if (hi <= lo) {
-    after_solver();
+    wait_solver();
+    fold_cbar();
     return;
   }
   if (wid == 0) tc_alloc(&tmem_s, np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256);
   if (tid == 0) mbar_init(&mbar, 1);
-  bool waited = false;
+  bool waited = false, folded = false;
   const uint32_t idesc = tc_idesc_bf16(kBtM, np);
   uint32_t phase = 0;
   for (int64_t t0 = lo; t0 < hi; t0 += kBtM) {
@@ -190,8 +223,10 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
         }
       }
     }
+    BT_MARK(0);                                        // X rows gathered, split, stored (+ old Bbar issue)
     if (!waited) {
-      after_solver();
+      wait_solver();
+      BT_MARK(1);                                      // waiting for the code solver
       waited = true;
       // ---- B = codes (N = np x K = ep), split, once per CTA ----
       for (int e = tid; e < np * nch; e += kBtThreads) {
@@ -208,6 +243,7 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
     tc_sync_before();
     __syncthreads();
     tc_sync_after();
+    BT_MARK(2);                                        // codes staged (B operand)
     const uint32_t tmem = tmem_s;
     if (tid == 0) {
       // D = Ahi Bhi^T + Ahi Blo^T + Alo Bhi^T over K = ep (2 chunks of 8 per instruction)
@@ -222,11 +258,18 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
       }
       tc_commit(&mbar);
     }
+    BT_MARK(3);                                        // MMA issue
+    if (!folded) {
+      fold_cbar();
+      folded = true;
+    }
+    BT_MARK(4);                                        // Cbar update
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     mbar_wait(&mbar, phase);
     phase ^= 1;
     __syncthreads();                                   // Bold rows of every thread landed
     tc_sync_after();
+    BT_MARK(5);                                        // MMAs done, old rows landed
     // ---- epilogue: warp w reads lanes 32 (w % 4) .. (rows), column half w / 4 ----
     {
       const int row = 32 * (wid & 3) + lane;
@@ -252,9 +295,16 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
       }
     }
     tc_sync_before();
+    BT_MARK(6);                                        // epilogue: TMEM -> keep * old + add * acc -> Bbar rows
   }
   __syncthreads();
   if (wid == 0) tc_dealloc(tmem_s, np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256);
+  if (clk_on) {
+#pragma unroll
+    for (int i = 0; i < 7; ++i) P.prof[i] += t_ph[i];
+    P.prof[7] += 1;
+  }
+#undef BT_MARK
 }
 
 }  // namespace somf

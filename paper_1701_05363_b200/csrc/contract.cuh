@@ -204,9 +204,11 @@ __device__ __forceinline__ void ct_store_out(const CtFuse& fz, int64_t e, double
 
 // scratch: >= 16 KB of shared memory the caller no longer needs
 __device__ __forceinline__ void ct_fused_reduce(const float* __restrict__ partial, int k, int eta, int ncp, int ep,
-                                                const CtFuse& fz, double* scratch) {
+                                                const CtFuse& fz, double* scratch,
+                                                long long* barrier_cycles = nullptr) {
   const int tid = threadIdx.x, ta = tid >> 5, tc = tid & 31;
   const int G = gridDim.x;
+  const long long tb0 = barrier_cycles ? clock64() : 0;
   __syncthreads();
   if (tid == 0) {
     __threadfence();
@@ -220,31 +222,46 @@ __device__ __forceinline__ void ct_fused_reduce(const float* __restrict__ partia
     }
   }
   __syncthreads();
+  if (barrier_cycles) *barrier_cycles += clock64() - tb0;      // the calling thread's wait (diagnostics)
   const int64_t tot = (int64_t)k * ncp;
   if ((ncp & 3) == 0) {
-    // lane = 4 consecutive outputs (16-byte loads), every split's load in flight
-    double (*ws4)[32][4] = reinterpret_cast<double (*)[32][4]>(scratch);     // [8][32][4]
+    // lane = 2 x 4 consecutive outputs (16-byte loads; outputs e and e + 32),
+    // up to 20 loads of a thread in flight: a CTA's ~tot / (4 G) outputs (34 at
+    // cfgC) take ONE pass of two L2 round trips (a 32-output pass needed two
+    // passes of three)
+    static_assert(kCtThreads == 256, "8 warps; 64 outputs x 4 in the combine");
+    double (*ws4)[64][4] = reinterpret_cast<double (*)[64][4]>(scratch);     // [8][64][4]
     const int64_t t4 = tot / 4;
     const int64_t e0 = t4 * blockIdx.x / G, e1 = t4 * (blockIdx.x + 1) / G;
-    for (int64_t g0 = e0; g0 < e1; g0 += 32) {
-      const int64_t e = g0 + tc;
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-      if (e < e1) {
-        const float4* p4 = reinterpret_cast<const float4*>(partial) + e;
-#pragma unroll 8
-        for (int i = ta; i < G; i += 8) {
-          const float4 v = __ldcg(p4 + (int64_t)i * t4);
-          s[0] += (double)v.x;
-          s[1] += (double)v.y;
-          s[2] += (double)v.z;
-          s[3] += (double)v.w;
-        }
+    for (int64_t g0 = e0; g0 < e1; g0 += 64) {
+      const int64_t ea = g0 + tc, eb = ea + 32;
+      double s[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+      const float4* p4 = reinterpret_cast<const float4*>(partial);
+      // (predicated loads, no branch on the lane: a divergent second output
+      // would serialise the two groups of lanes)
+      const bool ha = ea < e1, hb = eb < e1;
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 10
+      for (int i = ta; i < G; i += 8) {
+        const float4 v = ha ? __ldcg(p4 + (int64_t)i * t4 + ea) : z4;
+        const float4 u = hb ? __ldcg(p4 + (int64_t)i * t4 + eb) : z4;
+        s[0][0] += (double)v.x;
+        s[0][1] += (double)v.y;
+        s[0][2] += (double)v.z;
+        s[0][3] += (double)v.w;
+        s[1][0] += (double)u.x;
+        s[1][1] += (double)u.y;
+        s[1][2] += (double)u.z;
+        s[1][3] += (double)u.w;
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) ws4[ta][tc][j] = s[j];
+      for (int j = 0; j < 4; ++j) {
+        ws4[ta][tc][j] = s[0][j];
+        ws4[ta][tc + 32][j] = s[1][j];
+      }
       __syncthreads();
-      if (tid < 128) {
-        const int l = tid >> 2, j = tid & 3;
+      {
+        const int l = tid >> 2, j = tid & 3;         // 256 threads = 64 outputs x 4
         const int64_t ee = g0 + l;
         if (ee < e1) {
           double t = 0.0;

@@ -37,6 +37,7 @@ struct CtTcArgs {
   int kn;                   // k rounded up to 16 (N of the G product)
   float* partial;           // G x k x (ep + kn): [beta | pad | G | pad] rows
   CtFuse fz;
+  long long* prof;          // optional: SM cycles per phase of CTA 0 (8 slots, somf_bcd_phase_cycles [224..231])
 };
 
 // fp32 -> (hi, lo) for 3xTF32: hi = x with the 13 low mantissa bits cleared
@@ -70,6 +71,17 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
   __shared__ __align__(8) uint64_t mbar;
   __shared__ int grow[kTcChunk];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // phase clock of CTA 0, thread 0 (diagnostics; accumulated in registers, flushed once)
+  const bool clk_on = P.prof && blockIdx.x == 0 && tid == 0;
+  long long t_mark = clock64(), t_ph[7] = {0, 0, 0, 0, 0, 0, 0};
+#define CTC_MARK(slot)                 \
+  do {                                 \
+    if (clk_on) {                      \
+      const long long now_ = clock64(); \
+      t_ph[slot] += now_ - t_mark;     \
+      t_mark = now_;                   \
+    }                                  \
+  } while (0)
   const int k = P.k, kp = P.kp, eta = P.eta, ep = P.ep, kn = P.kn;
   const int LDR = ep + kp;                            // raw row: [X row (ep) | D row (kp)]
   const int G = gridDim.x;
@@ -112,14 +124,17 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
+    CTC_MARK(0);                                      // row indices + cp.async issue
     for (int j = 0; j < ntile; ++j) {
       cp_async_wait_upto(ntile - 1 - j);
+      CTC_MARK(1);                                    // rows of tile j landed (mine)
       if (issued > 0) {                               // tile j-1's MMAs have read the operand buffers
         mbar_wait(&mbar, phase);
         phase ^= 1;
         issued = 0;
       }
       __syncthreads();
+      CTC_MARK(2);                                    // previous tile's MMAs + every thread's rows
       // ---- transpose + split tile j into K-major tf32 hi / lo operands ----
       // thread -> one operand row m (atom, or X column), all kTcK / 4 chunks
       for (int m = tid; m < kTcM + ep; m += kCtThreads) {
@@ -178,6 +193,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
         tc_commit(&mbar);
       }
       issued = 1;
+      CTC_MARK(3);                                    // transpose + split + MMA issue
     }
   }
   const int ntile_all = hi > lo ? 1 : 0;
@@ -185,6 +201,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
     mbar_wait(&mbar, phase);
     tc_sync_after();
   }
+  CTC_MARK(2);
   // ---- epilogue: partial tile [beta | pad | G | pad] of my rows (fp32), lane = atom ----
   const int ncp = ep + kn;
   float* out = P.partial + (int64_t)blockIdx.x * k * ncp;
@@ -207,7 +224,19 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
   tc_sync_before();
   __syncthreads();
   if (wid == 0) tc_dealloc(tmem_s, ncols);
-  ct_fused_reduce(P.partial, k, eta, ep + kn, ep, P.fz, reinterpret_cast<double*>(ctc_smem));
+  CTC_MARK(4);                                        // epilogue: TMEM -> fp32 partial tile
+  long long t_bar = 0;
+  ct_fused_reduce(P.partial, k, eta, ep + kn, ep, P.fz, reinterpret_cast<double*>(ctc_smem),
+                  clk_on ? &t_bar : nullptr);
+  if (clk_on) {
+    CTC_MARK(6);                                      // barrier + fixed-order reduction
+    t_ph[5] = t_bar;                                  // the grid barrier's share
+    t_ph[6] -= t_bar;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) P.prof[i] += t_ph[i];
+    P.prof[7] += 1;
+  }
+#undef CTC_MARK
 }
 
 }  // namespace somf

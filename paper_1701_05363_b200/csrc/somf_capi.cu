@@ -432,6 +432,7 @@ static bool launch_bbar_v2(somf_ctx* h, bool gather, bool xcompact, const int64_
       // programmatic dependent launch: the CTAs stage their first X tile while
       // the code solver still runs (k_bbar_tc waits before reading the codes)
       a.pdl = 1;
+      a.prof = h->prof_on ? h->bcd_prof + 232 : nullptr;   // slots 232..239 (B-bar phases)
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(h->nsm);
       cfg.blockDim = dim3(kBtThreads);
@@ -549,6 +550,7 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
         a.xcompact = xcompact;
         a.partial = h->partial;
         a.fz = CtFuse{h->ct_bar, r, beta, G, h->err_dev};
+        a.prof = h->prof_on ? h->bcd_prof + 224 : nullptr;  // slots 224..231 (contraction phases)
         void* args[] = {&a};
         CK(cudaLaunchCooperativeKernel((const void*)k_contract_tc, dim3(h->nsm), dim3(kCtThreads), args, smem,
                                        h->st));
