@@ -281,13 +281,14 @@ somf_status somf_last_kernels(somf_handle h, int32_t* out);
  * the first unconverged position << 16, [96 + r] / [160 + r] its lambda and
  * next lambda (double bits); at its round cap [72..79] that atom's state;
  * [224..231] tcgen05 contraction (CTA 0): row indices + load issue, wait for
- * the rows, wait for the previous tile's MMAs, transpose / split / MMA issue,
- * epilogue, grid barrier, fixed-order reduction, launches; [232..239] tcgen05
+ * the rows, wait for a buffer's previous MMAs, transpose / split, epilogue,
+ * grid barrier, fixed-order reduction, launches, and [240] fence + CTA
+ * barrier after the operand stores, [241] MMA issue; [232..239] tcgen05
  * B-bar kernel (CTA 0): X rows staged, wait for the code solver, codes
  * staged, MMA issue, Cbar update, MMA + old rows wait, epilogue, launches.
  * cycles must hold SOMF_PROF_SLOTS entries.  Synchronises.  Zeros for the
  * kernels not launched. */
-#define SOMF_PROF_SLOTS 240
+#define SOMF_PROF_SLOTS 248
 somf_status somf_bcd_phase_cycles(somf_handle h, int64_t* cycles);
 
 /* ---- per-phase timing of somf_partial_fit (CUDA events on config.stream) ---- */

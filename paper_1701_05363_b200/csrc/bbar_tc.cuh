@@ -229,14 +229,27 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
       BT_MARK(1);                                      // waiting for the code solver
       waited = true;
       // ---- B = codes (N = np x K = ep), split, once per CTA ----
-      for (int e = tid; e < np * nch; e += kBtThreads) {
-        const int n = e % np, c = e / np;            // n fastest: conflict-free 16-byte stores
-        float v[8];
-        if (n < k) bt_load8(P.A + (int64_t)n * eta, 8 * c, eta, false, v);
-        else
+      // (UB chunks of a thread in flight before the stores: the codes sit in
+      // L2 and the loop is latency-bound -- one round trip, not np nch / 256)
+      {
+        constexpr int UB = 9;
+        for (int e0 = tid; e0 < np * nch; e0 += kBtThreads * UB) {
+          float v[UB][8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 0.f;
-        bt_store_chunk(v, Bhi, Blo, bt_off(n, 8 * c, nch));
+          for (int u = 0; u < UB; ++u) {
+            const int e = e0 + u * kBtThreads;
+            const int n = e % np, c = e / np;          // n fastest: conflict-free 16-byte stores
+            if (e < np * nch && n < k) bt_load8(P.A + (int64_t)n * eta, 8 * c, eta, false, v[u]);
+            else
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[u][i] = 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < UB; ++u) {
+            const int e = e0 + u * kBtThreads;
+            if (e < np * nch) bt_store_chunk(v[u], Bhi, Blo, bt_off(e % np, 8 * (e / np), nch));
+          }
+        }
       }
     }
     tc_fence_smem_to_async();

@@ -8,9 +8,12 @@
 // hi.hi + hi.lo + lo.hi are accumulated in fp32 in TMEM, kind::tf32 (bf16x3
 // was measured too coarse for the ridge solve at cfgC: alpha off by 2.5e-3).
 // Rows arrive by 16-byte cp.async, all 128 rows of a chunk in flight at once
-// ([X row | D row] raw rows, one commit group per 32-row tile); each tile is
+// ([X row | D row] raw rows, one commit group per 32 rows); each 16-row tile is
 // transposed and split in shared memory into the K-major operands (a 16-byte
-// K chunk = 4 rows of one atom / column) as soon as it lands.  The partial tiles are written in fp32 and
+// K chunk = 4 rows of one atom / column) as soon as it lands, into one of two
+// operand buffers: tile j + 1 is transposed while tile j's MMAs run (the
+// 3xTF32 products of a 32-row tile take ~1 us of tensor time per SM, which
+// was serial with the ~1 us transposition).  The partial tiles are written in fp32 and
 // reduced in fixed order behind one grid barrier (ct_fused_reduce,
 // cooperative launch) into r [beta | G] in fp64.
 #pragma once
@@ -23,7 +26,9 @@
 namespace somf {
 
 constexpr int kTcM = 128;           // atoms per accumulator (k <= 128)
-constexpr int kTcK = 32;            // masked rows per tile (K of one tile)
+constexpr int kTcK = 16;            // masked rows per tile (K of one tile)
+constexpr int kTcBuf = 2;           // operand buffers: tile j + 1 is transposed / split while tile j's MMAs run
+constexpr int kTcGrp = 32;          // masked rows per cp.async commit group (2 tiles)
 
 struct CtTcArgs {
   const int32_t* idx;
@@ -68,12 +73,12 @@ constexpr int kTcChunk = 128;       // masked rows whose raw data is resident at
 __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
   extern __shared__ __align__(128) uint8_t ctc_smem[];
   __shared__ uint32_t tmem_s;
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ __align__(8) uint64_t mbar[kTcBuf];
   __shared__ int grow[kTcChunk];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // phase clock of CTA 0, thread 0 (diagnostics; accumulated in registers, flushed once)
   const bool clk_on = P.prof && blockIdx.x == 0 && tid == 0;
-  long long t_mark = clock64(), t_ph[7] = {0, 0, 0, 0, 0, 0, 0};
+  long long t_mark = clock64(), t_ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #define CTC_MARK(slot)                 \
   do {                                 \
     if (clk_on) {                      \
@@ -88,53 +93,59 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
   const int64_t q = *P.q_dev;
   const int64_t lo = q * blockIdx.x / G, hi = q * (blockIdx.x + 1) / G;
   const size_t a_bytes = (size_t)kTcM * kTcK * 4, x_bytes = (size_t)ep * kTcK * 4;
-  uint8_t* Ahi = ctc_smem;                            // atoms x rows (K-major tf32)
-  uint8_t* Alo = Ahi + a_bytes;
-  uint8_t* Xhi = Alo + a_bytes;                       // X columns x rows
-  uint8_t* Xlo = Xhi + x_bytes;
-  float* raw = reinterpret_cast<float*>(Xlo + x_bytes);          // kTcChunk x LDR (fp32 rows)
+  const size_t set_bytes = 2 * (a_bytes + x_bytes);   // one operand buffer: A hi / lo, X hi / lo
+  // buffer b: Ahi (atoms x rows, K-major tf32) | Alo | Xhi (X columns x rows) | Xlo
+  float* raw = reinterpret_cast<float*>(ctc_smem + kTcBuf * set_bytes);   // kTcChunk x LDR (fp32 rows)
   // TMEM: columns [0, ep) beta, [ep, ep + kn) G
   const uint32_t ncols = (ep + kn) <= 256 ? 256 : 512;
   if (wid == 0) tc_alloc(&tmem_s, ncols);
-  if (tid == 0) mbar_init(&mbar, 1);
-  uint32_t phase = 0;
-  int issued = 0;                                     // MMA batches committed (one per tile)
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < kTcBuf; ++b) mbar_init(&mbar[b], 1);
+  }
+  uint32_t phase_bits = 0;                            // bit b: parity of buffer b's mbarrier
+  uint32_t pend_bits = 0;                             // bit b: MMAs committed on buffer b, not yet waited for
+  int jt = 0;                                         // tiles issued so far (buffer = jt % kTcBuf)
+  const uint64_t dbase = tc_sdesc(ctc_smem, 128, 128u * (kTcK / 4));
+  const uint32_t idg = tc_idesc_tf32(kTcM, kn);
   const int cx = eta / 4, cd = kp / 4, cr = cx + cd;  // 16-byte chunks of a raw row (eta % 4 == 0)
   for (int64_t c0 = lo; c0 < hi; c0 += kTcChunk) {
     const int nrow = (int)(hi - c0 < (int64_t)kTcChunk ? hi - c0 : (int64_t)kTcChunk);
-    const int ntile = (nrow + kTcK - 1) / kTcK;
-    if (issued > 0) {                                 // the previous chunk's MMAs read raw-derived operands
-      mbar_wait(&mbar, phase);
-      phase ^= 1;
-      issued = 0;
-    }
+    const int ntile = (nrow + kTcK - 1) / kTcK, ngrp = (nrow + kTcGrp - 1) / kTcGrp;
+    // (the previous chunk's raw rows were last read by the transposition of
+    // its last tile, before that tile's __syncthreads)
     __syncthreads();
     for (int r = tid; r < kTcChunk; r += kCtThreads) grow[r] = r < nrow ? P.idx[c0 + r] : -1;
     __syncthreads();
-    // every row of the chunk in flight at once: one commit group per tile
-    for (int j = 0; j < ntile; ++j) {
-      const int r0 = j * kTcK, r1 = min(nrow, r0 + kTcK);
+    // every row of the chunk in flight at once: one commit group per 32 rows
+    for (int g = 0; g < ngrp; ++g) {
+      const int r0 = g * kTcGrp, r1 = min(nrow, r0 + kTcGrp);
       for (int e = tid; e < (r1 - r0) * cr; e += kCtThreads) {
         const int r = r0 + e / cr, c = e % cr;
-        const int64_t g = grow[r];
+        const int64_t gr = grow[r];
         const float* src =
-            c < cx ? P.X + (P.xcompact ? c0 + r : g) * P.ldx + 4 * c : P.D + g * kp + 4 * (c - cx);
+            c < cx ? P.X + (P.xcompact ? c0 + r : gr) * P.ldx + 4 * c : P.D + gr * kp + 4 * (c - cx);
         float* dst = raw + (size_t)r * LDR + (c < cx ? 4 * c : ep + 4 * (c - cx));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     CTC_MARK(0);                                      // row indices + cp.async issue
-    for (int j = 0; j < ntile; ++j) {
-      cp_async_wait_upto(ntile - 1 - j);
+    for (int j = 0; j < ntile; ++j, ++jt) {
+      const int b = jt % kTcBuf;
+      uint8_t* Ahi = ctc_smem + (size_t)b * set_bytes;
+      uint8_t* Alo = Ahi + a_bytes;
+      uint8_t* Xhi = Alo + a_bytes;
+      uint8_t* Xlo = Xhi + x_bytes;
+      if ((j * kTcK) % kTcGrp == 0) cp_async_wait_upto(ngrp - 1 - (j * kTcK) / kTcGrp);
       CTC_MARK(1);                                    // rows of tile j landed (mine)
-      if (issued > 0) {                               // tile j-1's MMAs have read the operand buffers
-        mbar_wait(&mbar, phase);
-        phase ^= 1;
-        issued = 0;
+      if ((pend_bits >> b) & 1u) {                    // tile jt - 2's MMAs have read this operand buffer
+        mbar_wait(&mbar[b], (phase_bits >> b) & 1u);
+        phase_bits ^= 1u << b;
+        pend_bits &= ~(1u << b);
       }
       __syncthreads();
-      CTC_MARK(2);                                    // previous tile's MMAs + every thread's rows
+      CTC_MARK(2);                                    // this buffer's previous MMAs + every thread's rows
       // ---- transpose + split tile j into K-major tf32 hi / lo operands ----
       // thread -> one operand row m (atom, or X column), all kTcK / 4 chunks
       for (int m = tid; m < kTcM + ep; m += kCtThreads) {
@@ -162,45 +173,50 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
           *reinterpret_cast<float4*>(lb + off) = l;
         }
       }
+      CTC_MARK(3);                                    // transpose + split
       tc_fence_smem_to_async();
       tc_sync_before();
       __syncthreads();
       tc_sync_after();
+      CTC_MARK(8);                                    // operands of every thread stored (fence + barrier)
       const uint32_t tmem = tmem_s;
       if (tid == 0) {
-        const uint32_t sbo = 128u * (kTcK / 4);
-        const bool first = (c0 == lo && j == 0);
+        // descriptors: buffer 0's Ahi descriptor + 16-byte offsets (the address
+        // field holds addr >> 4; no carry out of it below 256 KB of shared memory)
+        const uint64_t dAh = dbase + (uint64_t)(((size_t)b * set_bytes) >> 4), dAl = dAh + (a_bytes >> 4);
+        const uint64_t dXh = dAl + (a_bytes >> 4), dXl = dXh + (x_bytes >> 4);
+        const bool first = jt == 0;
+#pragma unroll
         for (int ks = 0; ks < kTcK / 8; ++ks) {
-          const size_t ko = (size_t)ks * 256;
-          const uint64_t ah = tc_sdesc(Ahi + ko, 128, sbo), al = tc_sdesc(Alo + ko, 128, sbo);
+          const uint64_t kq = (uint64_t)ks * 16;      // 256 bytes of K per instruction
+          const uint64_t ah = dAh + kq, al = dAl + kq;
           const bool acc0 = !first || ks > 0;
           // beta: N = ep in pieces of <= 256 (multiples of 16)
           for (int n0 = 0; n0 < ep; n0 += 256) {
             const int nn = ep - n0 < 256 ? ep - n0 : 256;
             const uint32_t id = tc_idesc_tf32(kTcM, nn);
-            const uint64_t xh = tc_sdesc(Xhi + (size_t)n0 * 16 * (kTcK / 4) + ko, 128, sbo);
-            const uint64_t xl = tc_sdesc(Xlo + (size_t)n0 * 16 * (kTcK / 4) + ko, 128, sbo);
-            tc_mma_tf32(tmem + n0, ah, xh, id, acc0);
-            tc_mma_tf32(tmem + n0, ah, xl, id, true);
-            tc_mma_tf32(tmem + n0, al, xh, id, true);
+            const uint64_t xo = kq + (uint64_t)n0 * (kTcK / 4);          // n0 rows of 16 (kTcK / 4) bytes
+            tc_mma_tf32(tmem + n0, ah, dXh + xo, id, acc0);
+            tc_mma_tf32(tmem + n0, ah, dXl + xo, id, true);
+            tc_mma_tf32(tmem + n0, al, dXh + xo, id, true);
           }
           // G: B = the same D rows (the A operand), N = kn
-          const uint32_t idg = tc_idesc_tf32(kTcM, kn);
           tc_mma_tf32(tmem + ep, ah, ah, idg, acc0);
           tc_mma_tf32(tmem + ep, ah, al, idg, true);
           tc_mma_tf32(tmem + ep, al, ah, idg, true);
         }
-        tc_commit(&mbar);
+        tc_commit(&mbar[b]);
       }
-      issued = 1;
-      CTC_MARK(3);                                    // transpose + split + MMA issue
+      pend_bits |= 1u << b;
+      CTC_MARK(9);                                    // MMA issue (thread 0)
     }
   }
   const int ntile_all = hi > lo ? 1 : 0;
-  if (issued > 0) {
-    mbar_wait(&mbar, phase);
-    tc_sync_after();
-  }
+  // MMAs complete in issue order, commits arrive in order: wait for both buffers
+#pragma unroll
+  for (int b = 0; b < kTcBuf; ++b)
+    if ((pend_bits >> b) & 1u) mbar_wait(&mbar[b], (phase_bits >> b) & 1u);
+  tc_sync_after();
   CTC_MARK(2);
   // ---- epilogue: partial tile [beta | pad | G | pad] of my rows (fp32), lane = atom ----
   const int ncp = ep + kn;
@@ -235,6 +251,8 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
 #pragma unroll
     for (int i = 0; i < 7; ++i) P.prof[i] += t_ph[i];
     P.prof[7] += 1;
+    P.prof[16] += t_ph[8];                            // slots 240, 241
+    P.prof[17] += t_ph[9];
   }
 #undef CTC_MARK
 }

@@ -533,7 +533,7 @@ static somf_status launch_contract(somf_ctx* h, bool gather, bool xcompact, cons
     CtTcArgs a{};
     a.ep = (m + 15) & ~15;
     a.kn = (k + 15) & ~15;
-    const size_t smem = (size_t)2 * (kTcM + a.ep) * kTcK * 4 + (size_t)kTcChunk * (a.ep + h->kp) * 4;
+    const size_t smem = (size_t)kTcBuf * 2 * (kTcM + a.ep) * kTcK * 4 + (size_t)kTcChunk * (a.ep + h->kp) * 4;
     if (a.ep + a.kn <= 512 && smem <= 226 * 1024 && m % 4 == 0 &&
         smem_attr(h, (const void*)k_contract_tc, smem) == cudaSuccess) {
       if (occupancy(h, (const void*)k_contract_tc, kCtThreads, smem) >= 1) {

@@ -252,7 +252,7 @@ class Somf:
     BCD_PHASES = ("setup", "recurrence", "stats", "barrier", "update", "finish", "writeback")
 
     def bcd_phase_cycles(self):
-        v = np.zeros(240, np.int64)       # SOMF_PROF_SLOTS
+        v = np.zeros(248, np.int64)       # SOMF_PROF_SLOTS
         _check(lib().somf_bcd_phase_cycles(self._h, v.ctypes.data_as(C.c_void_p)), self._h)
         out = dict(zip(self.BCD_PHASES, v[:7].tolist()), launches=int(v[7]))
         # slot 8 + r: (frozen prefix F << 16) + unconverged atoms, summed over launches
@@ -264,7 +264,8 @@ class Somf:
         out["update_split"] = dict(zip(("ring_reset", "record_read"), v[80:82].tolist()))
         out["raw"] = v.tolist()
         out["contract"] = dict(zip(("issue", "rows_wait", "mma_wait", "transpose_split", "epilogue", "barrier",
-                                    "reduce"), v[224:231].tolist()), launches=int(v[231]))
+                                    "reduce"), v[224:231].tolist()), operand_sync=int(v[240]), mma_issue=int(v[241]),
+                               launches=int(v[231]))
         out["bbar"] = dict(zip(("x_stage", "solver_wait", "codes_stage", "mma_issue", "cbar", "mma_wait", "epilogue"),
                                v[232:239].tolist()), launches=int(v[239]))
         # lasso / nonneg CD with support jumps (cd_as.cuh): totals over its columns
