@@ -282,8 +282,8 @@ somf_status somf_last_kernels(somf_handle h, int32_t* out);
  * next lambda (double bits); at its round cap [72..79] that atom's state;
  * [224..231] tcgen05 contraction (CTA 0): row indices + load issue, wait for
  * the rows, wait for a buffer's previous MMAs, transpose / split, epilogue,
- * grid barrier, fixed-order reduction, launches, and [240] fence + CTA
- * barrier after the operand stores, [241] MMA issue; [232..239] tcgen05
+ * grid barrier, fixed-order reduction, launches, and [241] the MMA warp's
+ * issue time ([240] reserved); [232..239] tcgen05
  * B-bar kernel (CTA 0): X rows staged, wait for the code solver, codes
  * staged, MMA issue, Cbar update, MMA + old rows wait, epilogue, launches.
  * cycles must hold SOMF_PROF_SLOTS entries.  Synchronises.  Zeros for the

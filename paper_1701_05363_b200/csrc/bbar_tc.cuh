@@ -197,18 +197,28 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
                    : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    // A = masked X rows (M = 128 x K = ep), split; rows fastest (conflict-free
-    // 16-byte stores), U chunks of every thread in flight before the stores
-    // (the gather is latency-bound: one round of loads, not several)
+    // A = masked X rows (M = 128 x K = ep), split.  A warp's 32 items are 8
+    // rows x 4 consecutive K chunks: the loads read 128 contiguous bytes of
+    // each row (8 lines per instruction instead of 32 scattered sectors) and
+    // the 16-byte stores cover 512 contiguous bytes (conflict-free); U chunks
+    // of every thread in flight before the stores (the gather is
+    // latency-bound: one round of loads, not several)
     {
       constexpr int U = 14;                         // every chunk of a thread in flight (eta <= 224)
-      for (int e0 = tid; e0 < kBtM * nch; e0 += kBtThreads * U) {
+      const int ncg = (nch + 3) / 4;                // groups of 4 chunks
+      auto item = [&](int e, int& r, int& c) {
+        const int blk = e >> 5;
+        r = (blk % (kBtM / 8)) * 8 + (e & 7);
+        c = (blk / (kBtM / 8)) * 4 + ((e >> 3) & 3);
+      };
+      for (int e0 = tid; e0 < kBtM * 4 * ncg; e0 += kBtThreads * U) {
         float v[U][8];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int e = e0 + u * kBtThreads;
-          const int r = e % kBtM, c = e / kBtM;
-          if (e < kBtM * nch && r < n) {
+          int r, c;
+          item(e, r, c);
+          if (e < kBtM * 4 * ncg && c < nch && r < n) {
             const int64_t xr = P.xcompact ? t0 + r : (int64_t)grow[r];
             bt_load8(P.X + xr * P.ldx, 8 * c, eta, true, v[u]);
           } else {
@@ -219,7 +229,9 @@ __global__ void __launch_bounds__(kBtThreads, 1) k_bbar_tc(BtArgs P) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int e = e0 + u * kBtThreads;
-          if (e < kBtM * nch) bt_store_chunk(v[u], Ahi, Alo, bt_off(e % kBtM, 8 * (e / kBtM), nch));
+          int r, c;
+          item(e, r, c);
+          if (e < kBtM * 4 * ncg && c < nch) bt_store_chunk(v[u], Ahi, Alo, bt_off(r, 8 * c, nch));
         }
       }
     }

@@ -241,18 +241,28 @@ __device__ __forceinline__ void ct_fused_reduce(const float* __restrict__ partia
       // would serialise the two groups of lanes)
       const bool ha = ea < e1, hb = eb < e1;
       const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 10
-      for (int i = ta; i < G; i += 8) {
-        const float4 v = ha ? __ldcg(p4 + (int64_t)i * t4 + ea) : z4;
-        const float4 u = hb ? __ldcg(p4 + (int64_t)i * t4 + eb) : z4;
-        s[0][0] += (double)v.x;
-        s[0][1] += (double)v.y;
-        s[0][2] += (double)v.z;
-        s[0][3] += (double)v.w;
-        s[1][0] += (double)u.x;
-        s[1][1] += (double)u.y;
-        s[1][2] += (double)u.z;
-        s[1][3] += (double)u.w;
+      // batches of 10 splits, fully unrolled with predicated loads (a partial
+      // unroll of the runtime-length loop leaves a one-load-at-a-time remainder:
+      // 9 serial L2 round trips at G = 148)
+      for (int i0 = ta; i0 < G; i0 += 80) {
+        float4 v[10], u[10];
+#pragma unroll
+        for (int x = 0; x < 10; ++x) {
+          const int i = i0 + 8 * x;
+          v[x] = (ha && i < G) ? __ldcg(p4 + (int64_t)i * t4 + ea) : z4;
+          u[x] = (hb && i < G) ? __ldcg(p4 + (int64_t)i * t4 + eb) : z4;
+        }
+#pragma unroll
+        for (int x = 0; x < 10; ++x) {
+          s[0][0] += (double)v[x].x;
+          s[0][1] += (double)v[x].y;
+          s[0][2] += (double)v[x].z;
+          s[0][3] += (double)v[x].w;
+          s[1][0] += (double)u[x].x;
+          s[1][1] += (double)u[x].y;
+          s[1][2] += (double)u[x].z;
+          s[1][3] += (double)u[x].w;
+        }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {

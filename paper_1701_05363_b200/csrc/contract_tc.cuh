@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // phase clock of CTA 0, thread 0 (diagnostics; accumulated in registers, flushed once)
   const bool clk_on = P.prof && blockIdx.x == 0 && tid == 0;
-  long long t_mark = clock64(), t_ph[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_mark = clock64(), t_ph[7] = {0, 0, 0, 0, 0, 0, 0};
 #define CTC_MARK(slot)                 \
   do {                                 \
     if (clk_on) {                      \
@@ -103,24 +103,78 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
 #pragma unroll
     for (int b = 0; b < kTcBuf; ++b) mbar_init(&mbar[b], 1);
   }
+  // Warp roles in the tile loop: warps 0..6 (kTcWorkers threads) gather,
+  // transpose and split; warp 7 only issues the MMAs (a tile's 12 tcgen05.mma
+  // take ~0.5 us to issue -- as long as its transposition -- so an issuing
+  // thread that also transposes would serialise the two).  Named barriers:
+  // 1 = workers only; 2 + b = "operands of buffer b stored" (workers arrive
+  // without waiting, the MMA warp syncs).
+  constexpr int kTcWorkers = kCtThreads - 32;
+  const bool worker = tid < kTcWorkers;
+  auto bar_workers = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(kTcWorkers) : "memory"); };
   uint32_t phase_bits = 0;                            // bit b: parity of buffer b's mbarrier
   uint32_t pend_bits = 0;                             // bit b: MMAs committed on buffer b, not yet waited for
   int jt = 0;                                         // tiles issued so far (buffer = jt % kTcBuf)
   const uint64_t dbase = tc_sdesc(ctc_smem, 128, 128u * (kTcK / 4));
   const uint32_t idg = tc_idesc_tf32(kTcM, kn);
   const int cx = eta / 4, cd = kp / 4, cr = cx + cd;  // 16-byte chunks of a raw row (eta % 4 == 0)
+  tc_sync_before();
+  __syncthreads();                                    // TMEM address, mbarriers initialised
+  tc_sync_after();
+  long long t_issue = 0;                              // MMA warp, lane 0: cycles spent issuing
   for (int64_t c0 = lo; c0 < hi; c0 += kTcChunk) {
     const int nrow = (int)(hi - c0 < (int64_t)kTcChunk ? hi - c0 : (int64_t)kTcChunk);
     const int ntile = (nrow + kTcK - 1) / kTcK, ngrp = (nrow + kTcGrp - 1) / kTcGrp;
+    if (!worker) {
+      // ---- MMA warp: per tile, wait for its operands, issue, commit ----
+      for (int j = 0; j < ntile; ++j, ++jt) {
+        const int b = jt % kTcBuf;
+        asm volatile("bar.sync %0, %1;" ::"r"(2 + b), "r"(kCtThreads) : "memory");
+        tc_sync_after();
+        if (lane == 0) {
+          const long long ti0 = P.prof && blockIdx.x == 0 ? clock64() : 0;
+          const uint32_t tmem = tmem_s;
+          // descriptors: buffer 0's Ahi descriptor + 16-byte offsets (the address
+          // field holds addr >> 4; no carry out of it below 256 KB of shared memory)
+          const uint64_t dAh = dbase + (uint64_t)(((size_t)b * set_bytes) >> 4), dAl = dAh + (a_bytes >> 4);
+          const uint64_t dXh = dAl + (a_bytes >> 4), dXl = dXh + (x_bytes >> 4);
+          const bool first = jt == 0;
+#pragma unroll
+          for (int ks = 0; ks < kTcK / 8; ++ks) {
+            const uint64_t kq = (uint64_t)ks * 16;    // 256 bytes of K per instruction
+            const uint64_t ah = dAh + kq, al = dAl + kq;
+            const bool acc0 = !first || ks > 0;
+            // beta: N = ep in pieces of <= 256 (multiples of 16)
+            for (int n0 = 0; n0 < ep; n0 += 256) {
+              const int nn = ep - n0 < 256 ? ep - n0 : 256;
+              const uint32_t id = tc_idesc_tf32(kTcM, nn);
+              const uint64_t xo = kq + (uint64_t)n0 * (kTcK / 4);        // n0 rows of 16 (kTcK / 4) bytes
+              tc_mma_tf32(tmem + n0, ah, dXh + xo, id, acc0);
+              tc_mma_tf32(tmem + n0, ah, dXl + xo, id, true);
+              tc_mma_tf32(tmem + n0, al, dXh + xo, id, true);
+            }
+            // G: B = the same D rows (the A operand), N = kn
+            tc_mma_tf32(tmem + ep, ah, ah, idg, acc0);
+            tc_mma_tf32(tmem + ep, ah, al, idg, true);
+            tc_mma_tf32(tmem + ep, al, ah, idg, true);
+          }
+          tc_commit(&mbar[b]);
+          if (P.prof && blockIdx.x == 0) t_issue += clock64() - ti0;
+        }
+        __syncwarp();
+      }
+      continue;
+    }
+    // ---- workers ----
     // (the previous chunk's raw rows were last read by the transposition of
-    // its last tile, before that tile's __syncthreads)
-    __syncthreads();
-    for (int r = tid; r < kTcChunk; r += kCtThreads) grow[r] = r < nrow ? P.idx[c0 + r] : -1;
-    __syncthreads();
+    // its last tile, before that tile's arrive; this barrier orders them)
+    bar_workers();
+    for (int r = tid; r < kTcChunk; r += kTcWorkers) grow[r] = r < nrow ? P.idx[c0 + r] : -1;
+    bar_workers();
     // every row of the chunk in flight at once: one commit group per 32 rows
     for (int g = 0; g < ngrp; ++g) {
       const int r0 = g * kTcGrp, r1 = min(nrow, r0 + kTcGrp);
-      for (int e = tid; e < (r1 - r0) * cr; e += kCtThreads) {
+      for (int e = tid; e < (r1 - r0) * cr; e += kTcWorkers) {
         const int r = r0 + e / cr, c = e % cr;
         const int64_t gr = grow[r];
         const float* src =
@@ -137,18 +191,20 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
       uint8_t* Alo = Ahi + a_bytes;
       uint8_t* Xhi = Alo + a_bytes;
       uint8_t* Xlo = Xhi + x_bytes;
-      if ((j * kTcK) % kTcGrp == 0) cp_async_wait_upto(ngrp - 1 - (j * kTcK) / kTcGrp);
-      CTC_MARK(1);                                    // rows of tile j landed (mine)
+      if ((j * kTcK) % kTcGrp == 0) {
+        cp_async_wait_upto(ngrp - 1 - (j * kTcK) / kTcGrp);
+        CTC_MARK(1);                                  // rows of the group landed (mine)
+        bar_workers();                                // ... and every worker's
+      }
       if ((pend_bits >> b) & 1u) {                    // tile jt - 2's MMAs have read this operand buffer
         mbar_wait(&mbar[b], (phase_bits >> b) & 1u);
         phase_bits ^= 1u << b;
         pend_bits &= ~(1u << b);
       }
-      __syncthreads();
-      CTC_MARK(2);                                    // this buffer's previous MMAs + every thread's rows
+      CTC_MARK(2);                                    // group barrier + this buffer's previous MMAs
       // ---- transpose + split tile j into K-major tf32 hi / lo operands ----
       // thread -> one operand row m (atom, or X column), all kTcK / 4 chunks
-      for (int m = tid; m < kTcM + ep; m += kCtThreads) {
+      for (int m = tid; m < kTcM + ep; m += kTcWorkers) {
         const bool isA = m < kTcM;
         const int col = isA ? ep + m : m - kTcM;     // column of the raw row
         const bool valid = isA ? m < k : col < eta;
@@ -175,53 +231,34 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
       }
       CTC_MARK(3);                                    // transpose + split
       tc_fence_smem_to_async();
-      tc_sync_before();
-      __syncthreads();
-      tc_sync_after();
-      CTC_MARK(8);                                    // operands of every thread stored (fence + barrier)
-      const uint32_t tmem = tmem_s;
-      if (tid == 0) {
-        // descriptors: buffer 0's Ahi descriptor + 16-byte offsets (the address
-        // field holds addr >> 4; no carry out of it below 256 KB of shared memory)
-        const uint64_t dAh = dbase + (uint64_t)(((size_t)b * set_bytes) >> 4), dAl = dAh + (a_bytes >> 4);
-        const uint64_t dXh = dAl + (a_bytes >> 4), dXl = dXh + (x_bytes >> 4);
-        const bool first = jt == 0;
-#pragma unroll
-        for (int ks = 0; ks < kTcK / 8; ++ks) {
-          const uint64_t kq = (uint64_t)ks * 16;      // 256 bytes of K per instruction
-          const uint64_t ah = dAh + kq, al = dAl + kq;
-          const bool acc0 = !first || ks > 0;
-          // beta: N = ep in pieces of <= 256 (multiples of 16)
-          for (int n0 = 0; n0 < ep; n0 += 256) {
-            const int nn = ep - n0 < 256 ? ep - n0 : 256;
-            const uint32_t id = tc_idesc_tf32(kTcM, nn);
-            const uint64_t xo = kq + (uint64_t)n0 * (kTcK / 4);          // n0 rows of 16 (kTcK / 4) bytes
-            tc_mma_tf32(tmem + n0, ah, dXh + xo, id, acc0);
-            tc_mma_tf32(tmem + n0, ah, dXl + xo, id, true);
-            tc_mma_tf32(tmem + n0, al, dXh + xo, id, true);
-          }
-          // G: B = the same D rows (the A operand), N = kn
-          tc_mma_tf32(tmem + ep, ah, ah, idg, acc0);
-          tc_mma_tf32(tmem + ep, ah, al, idg, true);
-          tc_mma_tf32(tmem + ep, al, ah, idg, true);
-        }
-        tc_commit(&mbar[b]);
-      }
+      asm volatile("bar.arrive %0, %1;" ::"r"(2 + b), "r"(kCtThreads) : "memory");
       pend_bits |= 1u << b;
-      CTC_MARK(9);                                    // MMA issue (thread 0)
     }
   }
-  const int ntile_all = hi > lo ? 1 : 0;
-  // MMAs complete in issue order, commits arrive in order: wait for both buffers
+  // MMAs complete in issue order, commits arrive in order: the workers wait for
+  // both buffers; the CTA barrier then covers the MMA warp
+  if (worker) {
 #pragma unroll
-  for (int b = 0; b < kTcBuf; ++b)
-    if ((pend_bits >> b) & 1u) mbar_wait(&mbar[b], (phase_bits >> b) & 1u);
+    for (int b = 0; b < kTcBuf; ++b)
+      if ((pend_bits >> b) & 1u) mbar_wait(&mbar[b], (phase_bits >> b) & 1u);
+  }
+  tc_sync_before();
+  __syncthreads();
   tc_sync_after();
   CTC_MARK(2);
+  const int ntile_all = hi > lo ? 1 : 0;
   // ---- epilogue: partial tile [beta | pad | G | pad] of my rows (fp32), lane = atom ----
   const int ncp = ep + kn;
   float* out = P.partial + (int64_t)blockIdx.x * k * ncp;
   if (ntile_all > 0) {
+    // TMEM -> shared memory (lane = atom row, 16 columns per tcgen05.ld; row
+    // stride ncp + 4 words so the 16-byte stores of a quarter-warp cover all
+    // banks) -> global memory with consecutive threads on consecutive 16 bytes
+    // (a direct store from the TMEM fragment is 32 scattered 16-byte requests
+    // per instruction: 4.6 us for the 80 KB tile at cfgC).  The operand
+    // buffers and raw rows are free: every MMA has completed.
+    float* stage = reinterpret_cast<float*>(ctc_smem);
+    const int lds = ncp + 4;
     const int a = 32 * (wid & 3) + lane;
     const uint32_t tl = tmem_s + ((uint32_t)(32 * (wid & 3)) << 16);
     const int nchunk = ncp / 16;
@@ -229,10 +266,16 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
       float v[16];
       tc_ld16(tl + 16 * cc, v);
       if (a < k) {
-        float4* o4 = reinterpret_cast<float4*>(out + (int64_t)a * ncp + 16 * cc);
+        float4* o4 = reinterpret_cast<float4*>(stage + (size_t)a * lds + 16 * cc);
 #pragma unroll
         for (int j = 0; j < 4; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
+    }
+    __syncthreads();
+    const int n4 = ncp / 4;
+    for (int e = tid; e < k * n4; e += kCtThreads) {
+      const int r = e / n4, c = e % n4;
+      reinterpret_cast<float4*>(out)[e] = *reinterpret_cast<const float4*>(stage + (size_t)r * lds + 4 * c);
     }
   } else {
     for (int e = tid; e < k * ncp; e += kCtThreads) out[e] = 0.f;
@@ -251,9 +294,8 @@ __global__ void __launch_bounds__(kCtThreads, 1) k_contract_tc(CtTcArgs P) {
 #pragma unroll
     for (int i = 0; i < 7; ++i) P.prof[i] += t_ph[i];
     P.prof[7] += 1;
-    P.prof[16] += t_ph[8];                            // slots 240, 241
-    P.prof[17] += t_ph[9];
   }
+  if (P.prof && blockIdx.x == 0 && tid == kTcWorkers) P.prof[17] += t_issue;    // slot 241: MMA issue (MMA warp)
 #undef CTC_MARK
 }
 

@@ -264,7 +264,7 @@ class Somf:
         out["update_split"] = dict(zip(("ring_reset", "record_read"), v[80:82].tolist()))
         out["raw"] = v.tolist()
         out["contract"] = dict(zip(("issue", "rows_wait", "mma_wait", "transpose_split", "epilogue", "barrier",
-                                    "reduce"), v[224:231].tolist()), operand_sync=int(v[240]), mma_issue=int(v[241]),
+                                    "reduce"), v[224:231].tolist()), mma_issue=int(v[241]),
                                launches=int(v[231]))
         out["bbar"] = dict(zip(("x_stage", "solver_wait", "codes_stage", "mma_issue", "cbar", "mma_wait", "epilogue"),
                                v[232:239].tolist()), launches=int(v[239]))
