@@ -411,3 +411,39 @@ def test_full_size_fmri_step(somf):
                 Bbar_S=rel(st["Bbar"][S], ora.Bbar[S]), D_S=rel(st["D"][S], ora.D[S]))
     assert all(v <= TOL_STEP for v in errs.values()), errs
     np.testing.assert_allclose(st["n"], ora.n, rtol=0, atol=1e-5)
+
+
+# ---------------------------------------------------------------------------
+# phase clocks (somf_bcd_phase_cycles): diagnostics must not change results
+# ---------------------------------------------------------------------------
+def test_phase_clocks_count_launches_and_keep_results(somf):
+    """With somf_profile_enable on, the CTA-0 clocks of the tensor-core
+    contraction / B-bar kernels, the ridge solve and Alg. 4 count one launch
+    per step with non-zero cycles, and the state is bit-identical to a run
+    without profiling (the clocks only read clock64)."""
+    name = "ridge_l1_fmri_small"
+    p, k, eta, kw, kind = CASES[name]
+    X = _data(kind, p, k + 4 * eta)
+    states = []
+    for prof in (False, True):
+        gpu = somf.Somf(p, k, eta, seed=3, **kw)
+        gpu.set_components(cuda(X[:, :k]))
+        gpu.profile_enable(prof)
+        for t in range(3):
+            gpu.partial_fit(cuda(X[:, k + t * eta:k + (t + 1) * eta]))
+        kern = gpu.last_kernels()
+        cyc = gpu.bcd_phase_cycles()
+        if prof:
+            assert kern["contract"] == "tc" and kern["bbar"] == "tc", kern
+            assert cyc["contract"]["launches"] == 3 and cyc["bbar"]["launches"] == 3, cyc
+            assert cyc["launches"] == 3
+            for key in ("issue", "transpose_split", "epilogue", "barrier", "reduce", "mma_issue"):
+                assert cyc["contract"][key] > 0, (key, cyc["contract"])
+            for key in ("x_stage", "codes_stage", "mma_issue", "epilogue"):
+                assert cyc["bbar"][key] > 0, (key, cyc["bbar"])
+            assert cyc["ridge"]["factor"] > 0
+        else:
+            assert cyc["contract"]["launches"] == 0 and cyc["bbar"]["launches"] == 0
+        states.append(gpu.get_state())
+    for key in ("D", "Bbar", "Cbar", "n"):
+        np.testing.assert_array_equal(states[0][key], states[1][key])
