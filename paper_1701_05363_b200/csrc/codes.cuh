@@ -91,17 +91,20 @@ k_ridge_codes(const double* __restrict__ G, const double* __restrict__ beta, int
   double* Wb = M + (size_t)K * ld;                  // (K / 8) x 64
   double* Y = Wb + (size_t)(K / kRcB) * 64;         // 8 x K
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  // ---- load G + lambda I (lower triangle, identity padding), 8 loads in flight per thread
-  for (int e0 = tid; e0 < K * K; e0 += 8 * kRcThreads) {
-    double g[8];
+  // ---- load G + lambda I (lower triangle, identity padding), up to kRcLd
+  // entries per thread in flight (k = 70: all 21 of a thread, one L2 round
+  // trip; only the j <= i half actually loads)
+  constexpr int kRcLd = 21;
+  for (int e0 = tid; e0 < K * K; e0 += kRcLd * kRcThreads) {
+    double g[kRcLd];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kRcLd; ++u) {
       const int e = e0 + u * kRcThreads;
       const int i = e / K, j = e % K;
       g[u] = (e < K * K && j <= i && i < kr && j < kr) ? __ldg(G + (int64_t)i * kr + j) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kRcLd; ++u) {
       const int e = e0 + u * kRcThreads;
       const int i = e / K, j = e % K;
       if (e < K * K && j <= i) M[i * ld + j] = (i < kr && j < kr) ? g[u] + (i == j ? lam : 0.0) : (i == j ? 1.0 : 0.0);
